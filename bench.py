@@ -1,0 +1,299 @@
+#!/usr/bin/env python
+"""Benchmark of the CBP hot path (BASELINE.json metric) -- one JSON line on rank 0.
+
+A step = one fused cbp_ber_sim launch (Philox info bits -> encoder -> BPSK/AWGN
+-> CBP decode -> error counting) per Eb/N0 point of BASELINE configs[1]
+(C2: N=648 rate-1/2 QC-LDPC, Eb/N0 1.0..3.0 dB, 1e6 frames per point per GPU,
+max_iter 30) followed by the NCCL all-reduce of the 8 counters per point.
+
+  python bench.py [--gpus N --steps K --warmup W]          (N>1: under torchrun)
+  python bench.py --impl reference ...                     (CPU oracle on the host cores)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "CBP info Gbit/s and frames/s per GPU and 8×B200 at Eb/N0, % of roofline"
+UNIT = "info Gbit/s"
+I_EDGE = 68            # algorithmic fp32/int ops per edge visit of the contract
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cbp", choices=["cbp", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--frames", type=int, default=None, help="frames per Eb/N0 point per GPU (default: BASELINE)")
+    ap.add_argument("--ebn0", type=str, default=None, help="comma list (default: the config's points)")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--llr-mode", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-frames", type=int, default=200_000)
+    ap.add_argument("--cpu-frames", type=int, default=400, help="oracle frames per Eb/N0 point (cpu_baseline)")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        import statistics
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 4 + k and r[4 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------ reference arm (CPU oracle)
+def run_reference(args, cfg, ebn0s):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import inputs
+    import oracle
+    base, Z = inputs.config_base(cfg.name)
+    o = oracle.OracleCode(base, Z)
+    frames = args.cpu_frames
+    for _ in range(args.warmup):
+        o.ber_sim(ebn0s[0], args.seed, 0, 8, cfg.max_iter)
+    times = []
+    tot = np.zeros(8, np.int64)
+    for s in range(args.steps):
+        t0 = time.perf_counter()
+        for eb in ebn0s:
+            tot += o.ber_sim(eb, args.seed, s * frames, frames, cfg.max_iter, llr_mode=args.llr_mode)
+        times.append(time.perf_counter() - t0)
+    T = sum(times)
+    fps = tot[0] / T
+    gbps = fps * o.K / 1e9
+    sample = f"{frames} frames x {len(ebn0s)} Eb/N0 points per step ({cfg.name}), single-threaded oracle"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": gbps, "unit": UNIT, "frames_per_s": fps,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_block(cfg, ebn0s, frames, args, n_gpus=1),
+        "cpu_baseline": {"value": gbps, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": gbps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def config_block(cfg, ebn0s, frames, args, n_gpus):
+    return {"workload": f"{cfg.name}: QC-LDPC N={cfg.spec[1] * cfg.spec[2]} rate {1 - cfg.spec[0] / cfg.spec[1]:.3f} "
+                        f"(BASELINE configs[1]) fused cbp_ber_sim, {len(ebn0s)} Eb/N0 points",
+            "ebn0_db": list(ebn0s), "frames_per_point_per_gpu": frames, "max_iter": cfg.max_iter,
+            "stop_rule": "belief W=M + syndrome verify", "llr": "int8" if args.llr_mode else "fp32",
+            "seed": args.seed, "parallelism": f"dp{n_gpus} (frame-range shards, NCCL allreduce of counters)",
+            "l2": "flushed (256 MiB write) before every step; ber_sim reads no input from HBM"}
+
+
+# ------------------------------------------------------------------ product arm
+def main():
+    args = parse()
+    import inputs
+    cfg = inputs.CONFIGS[args.config]
+    ebn0s = [float(x) for x in args.ebn0.split(",")] if args.ebn0 else list(cfg.ebn0_db)
+    if args.impl == "reference":
+        return run_reference(args, cfg, ebn0s)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2305_05286_b200 as cbp
+    from paper_2305_05286_b200 import pipeline
+    from paper_2305_05286_b200.dist import allreduce_counts
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    frames = args.frames or cfg.frames
+    base, Z = inputs.config_base(cfg.name)
+    code = cbp.Code(base, Z, device=local)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)   # 256 MiB > L2
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(counts_per_point, launch_ms=None):
+        for p, eb in enumerate(ebn0s):
+            c = counts_per_point[p]
+            c.zero_()
+            if launch_ms is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            # this rank's frame range of the global workload (weak scaling: frames per GPU fixed)
+            code.ber_sim(eb, args.seed, rank * frames, frames, cfg.max_iter, llr_mode=args.llr_mode, counts=c,
+                         stream=stream)
+            if launch_ms is not None:
+                e1.record(stream)
+                launch_ms.append((p, e0, e1))
+            allreduce_counts(c)
+
+    counts = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in ebn0s]
+    for _ in range(args.warmup):
+        step(counts)
+    torch.cuda.synchronize()
+
+    launches = []
+    step_ms = []
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.fill_(1.0)                                   # L2 flush outside the step events
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            step(counts, launches)
+            s1.record(stream)
+            step_ms.append((s0, s1))
+        torch.cuda.synchronize()
+        barrier()
+    t_ms = sum(a.elapsed_time(b) for a, b in step_ms)
+    t_max = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    T = t_max.item() / 1e3
+    tot = torch.stack(counts).cpu().numpy()                   # counts of the last step, all ranks summed
+    frames_all = int(tot[:, 0].sum()) * args.steps
+    fps = frames_all / T
+    gbps = fps * code.K / 1e9
+
+    # roofline of the dominant kernel (the fused cbp_kernel launch, one per Eb/N0 point)
+    per_launch_ms = [a.elapsed_time(b) for _, a, b in launches]
+    ev_local = []
+    for p in range(len(ebn0s)):
+        ev_local.append(int(tot[p, 5]) // max(world, 1))       # edge visits per launch (this rank's share)
+    dur = np.array(per_launch_ms).reshape(args.steps, len(ebn0s)).mean(axis=0) / 1e3
+    ops = np.array(ev_local, dtype=np.float64) * I_EDGE
+    achieved = float(ops.sum() / dur.sum())                    # ops/s averaged over the launches of a step
+    li = code.launch_info()
+    clocks = clk.summary()
+    f_sm = measured_peaks().get("sm_max_mhz", 1965.0)
+    peak = li["num_sms"] * 128 * f_sm * 1e6
+    roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Top/s",
+                "frac": achieved / peak, "traffic": None,
+                "note": f"I_edge={I_EDGE} ops/edge-visit x exact edge visits / mean launch time; peak = "
+                        f"{li['num_sms']} SM x 128 lanes x {f_sm:.0f} MHz (sm_max, MEASURED_PEAKS.json)"}
+
+    # end-to-end: host LLRs -> cbp_decode (pipelined H2D / decode / D2H) -> host outputs
+    e2e = None
+    if not args.no_e2e:
+        Fe = args.e2e_frames
+        ld = (code.N + 3) // 4 * 4
+        host = torch.empty((Fe, ld), dtype=torch.float32, pin_memory=True)
+        eb_mid = ebn0s[len(ebn0s) // 2]
+        for b in range(0, Fe, 1 << 17):
+            n = min(1 << 17, Fe - b)
+            llr, _ = code.channel(eb_mid, args.seed + 1, rank * Fe + b, n, want_cw=False)
+            host[b:b + n].copy_(llr)
+        hout = pipeline.alloc_host_outputs(code, Fe)
+        for _ in range(2):
+            pipeline.decode_host(code, host, cfg.max_iter, out=hout)
+        barrier()
+        t0 = time.perf_counter()
+        reps = max(1, args.steps)
+        for _ in range(reps):
+            pipeline.decode_host(code, host, cfg.max_iter, out=hout)
+        te = time.perf_counter() - t0
+        tmax = torch.tensor([te], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        te = tmax.item()
+        e2e = {"value": reps * Fe * world * code.K / te / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": Fe * ld * 4 * world, "d2h_bytes_per_step": Fe * (code.words * 4 + 5) * world,
+               "what": f"cbp_decode via pipeline.decode_host on {Fe} host-resident frames/GPU at {eb_mid} dB "
+                       f"(pinned host LLRs, H2D + decode + D2H of bits/iters/flags timed, host wall clock)"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        try:
+            import oracle
+            o = oracle.OracleCode(base, Z)
+            t0 = time.perf_counter()
+            c = np.zeros(8, np.int64)
+            for p, eb in enumerate(ebn0s):
+                c += o.ber_sim(eb, args.seed, 0, args.cpu_frames, cfg.max_iter, llr_mode=args.llr_mode)
+            tc = time.perf_counter() - t0
+            cpu = {"value": c[0] * o.K / tc / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+                   "sample": f"{args.cpu_frames} frames x {len(ebn0s)} Eb/N0 points of the same workload, "
+                             f"single-threaded C++ oracle, {tc:.1f} s", "frames_per_s": c[0] / tc}
+        except Exception as ex:   # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        results = {}
+        for p, eb in enumerate(ebn0s):
+            t = tot[p]
+            results[str(eb)] = {"frames": int(t[0]), "ber": t[1] / max(1, t[0] * code.K), "fer": t[2] / max(1, t[0]),
+                                "avg_iters": t[4] / max(1, t[0]), "edge_visits": int(t[5]),
+                                "not_converged": int(t[6]), "undetected_fires": int(t[7])}
+        line = {
+            "metric": METRIC, "value": gbps, "unit": UNIT, "frames_per_s": fps, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_block(cfg, ebn0s, frames, args, world),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": args.steps * len(ebn0s), "launch": li, "results": results,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

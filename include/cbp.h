@@ -1,0 +1,163 @@
+/*
+ * cbp.h -- C ABI of the B200-native check-belief propagation (CBP) decoder.
+ *
+ * Method: Guan & Liang, "Check-Belief Propagation Decoding of LDPC Codes"
+ * (arXiv 2305.05286), §IV-C Steps 1-3 (l.400-487), with the readings
+ * R1-R21 of DESIGN.md §2 and the fp32 arithmetic contract of DESIGN.md §3.
+ * Implemented by paper_2305_05286_b200/libcbp.so (sm_100a kernels + host code).
+ *
+ * Conventions
+ *  - Every function returns a cbp_status; nothing else crosses the ABI (no
+ *    exceptions).  On a non-OK status cbp_last_error() returns a thread-local
+ *    message.  Decoding failure is a RESULT (flags bit0 = 0), not an error.
+ *  - "device pointer" = memory on the code's device, allocated and owned by
+ *    the caller; "host pointer" = caller-owned host memory.  The library never
+ *    frees caller memory.  All work is enqueued on the caller's CUDA stream
+ *    (a cudaStream_t passed as void*, NULL = legacy default stream) and is
+ *    asynchronous: asynchronous device faults surface at the caller's next
+ *    synchronisation (reported then by the CUDA runtime, not by this ABI).
+ *  - A cbp_code is immutable after creation and may be used concurrently from
+ *    several host threads and streams.
+ *  - Bits are packed LSB first: bit v of a frame is bit (v % 32) of word v / 32.
+ *  - Results depend only on (code, inputs, options) -- never on grid size,
+ *    stream or GPU count.  cbp_ber_sim / cbp_channel depend only on
+ *    (seed, global frame index): frames shard across GPUs by frame range.
+ */
+#ifndef CBP_H
+#define CBP_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CBP_OK = 0,
+    CBP_E_INVALID = 1,      /* bad argument (null pointer, size, range)        */
+    CBP_E_UNSUPPORTED = 2,  /* valid but not supported (e.g. no encoder structure) */
+    CBP_E_NOMEM = 3,        /* host or device allocation failed                */
+    CBP_E_CUDA = 4,         /* CUDA runtime error at enqueue time              */
+    CBP_E_INTERNAL = 5
+} cbp_status;
+
+/* Thread-local text of the last non-OK status of this thread ("" if none). */
+const char* cbp_last_error(void);
+/* Library version string. */
+const char* cbp_version(void);
+
+/* ------------------------------------------------------------------ codes */
+
+/* Seeded QC base-matrix constructor (BASELINE.json
+ * configs).  Host only.  base_out: host int16[mb*nb], row-major; -1 = zero
+ * block, s in [0,Z) = identity cyclically shifted by s (check row r of block
+ * (i,j) connects to variable j*Z + (r+s)%Z).  Identical to the shared input
+ * generator inputs/qc_construct.c (same source). */
+typedef struct {
+    int32_t mb, nb, Z;      /* base rows, base columns, lifting size            */
+    int32_t mb_core;        /* rows of the dual-diagonal core (mb if no extension) */
+    int32_t wmode;          /* info column weight rule: 0 const, 1 uniform, 2 heavy-tailed */
+    int32_t w_lo, w_hi;
+} cbp_construct_spec;
+cbp_status cbp_construct_base(const cbp_construct_spec* spec, uint64_t seed, int16_t* base_out);
+
+/* Opaque code handle: the expanded code graph G = (V, C, E) of PAPER.md l.92
+ * (N = nb*Z variables, M = mb*Z checks, K = N - M info bits) as per-base-entry
+ * schedule tables resident on `device`.
+ *   base  : host int16[mb*nb] (copied; caller keeps ownership)
+ *   Z     : 1 <= Z <= 1024; shifts must lie in [-1, Z)
+ *   every base row and column must be non-empty.
+ * Encoding (cbp_channel, cbp_ber_sim) additionally needs the dual-diagonal
+ * parity structure of SURVEY Appendix B; otherwise those return
+ * CBP_E_UNSUPPORTED while decoding still works. */
+typedef struct cbp_code cbp_code;
+cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t Z, int32_t device, cbp_code** out);
+void       cbp_code_destroy(cbp_code* code);
+/* any output pointer may be NULL */
+cbp_status cbp_code_dims(const cbp_code* code, int32_t* N, int32_t* K, int32_t* M, int64_t* E);
+
+/* ----------------------------------------------------------------- decode */
+
+/* Stop rules (readings R4-R6). */
+typedef enum {
+    CBP_STOP_BELIEF_M = 0,  /* M consecutive clean check updates (Omega>0, no flips), then syndrome verify (default) */
+    CBP_STOP_BELIEF_N = 1,  /* the literal "N consecutive" window, then syndrome verify */
+    CBP_STOP_SYNDROME = 2,  /* syndrome of the hard bits after every full sweep        */
+    CBP_STOP_NONE = 3       /* always run max_iter sweeps                              */
+} cbp_stop_rule;
+
+typedef struct {
+    int32_t max_iter;       /* sweeps over all M checks, 1..65535                    */
+    int32_t stop_rule;      /* cbp_stop_rule                                         */
+    int32_t reserved[2];    /* must be 0                                             */
+} cbp_opts;
+
+/* Decode `frames` channel-LLR vectors (PAPER.md equ_s4e15: L_v = ln Pr(y|0)/Pr(y|1)).
+ *   d_llr    : device float[frames][ld], ld >= N, (ld*4) % 16 == 0, 16-byte aligned
+ *   d_bits   : device uint32[frames][ld_words], ld_words >= ceil(N/32): hard decisions
+ *              of the V2C phase (reading R14)
+ *   d_iters  : device int32[frames]: 1-based sweep in which the stop fired, max_iter if none
+ *   d_flags  : device uint8[frames]: bit0 converged, bit1 output syndrome zero,
+ *              bit2 belief criterion fired with a nonzero syndrome at least once
+ *   d_omega  : optional device float[frames][M]: final check-beliefs Omega_c = +-phi(S_c)
+ *              (equ_s4e1/equ_s4e3), NULL to skip
+ *   d_ev     : optional device int64[frames]: edge visits (= B2V = V2C = C2B updates)
+ * frames == 0 is a no-op.  Non-finite LLRs give unspecified bits but stay memory-safe. */
+cbp_status cbp_decode(const cbp_code* code, const float* d_llr, int64_t ld, int64_t frames, const cbp_opts* opts,
+                      uint32_t* d_bits, int64_t ld_words, int32_t* d_iters, uint8_t* d_flags, float* d_omega,
+                      int64_t* d_ev, void* stream);
+
+/* Same with int8-quantised LLRs: L_v = scale * q_v (BASELINE config 5: q = sat(rint(4L), +-127),
+ * scale = 0.25).  d_q: device int8[frames][ld], ld >= N, ld % 16 == 0, 16-byte aligned. */
+cbp_status cbp_decode_i8(const cbp_code* code, const int8_t* d_q, int64_t ld, float scale, int64_t frames,
+                         const cbp_opts* opts, uint32_t* d_bits, int64_t ld_words, int32_t* d_iters,
+                         uint8_t* d_flags, float* d_omega, int64_t* d_ev, void* stream);
+
+/* ---------------------------------------------------------------- channel */
+
+/* BPSK/AWGN channel of DESIGN.md §4 on device for global frames
+ * [frame_begin, frame_begin + frames): uniform info bits (Philox4x32-10 keyed by
+ * seed), systematic encoding, y = (1-2c) + sigma n, L = 2y/sigma^2 with
+ * sigma^2 = 1/(2 (K/N) 10^(ebn0_db/10)); llr_mode 0 fp32, 1 int8 stream (L = q/4).
+ *   d_llr : device float[frames][ld] (ld >= N) or NULL
+ *   d_cw  : device uint32[frames][ld_words] transmitted codewords or NULL */
+cbp_status cbp_channel(const cbp_code* code, double ebn0_db, uint64_t seed, int64_t frame_begin, int64_t frames,
+                       int32_t llr_mode, float* d_llr, int64_t ld, uint32_t* d_cw, int64_t ld_words, void* stream);
+
+/* ------------------------------------------------------------------ BER sim */
+
+/* Counters accumulated (+=) by cbp_ber_sim; device memory, caller zeroes it. */
+typedef struct {
+    int64_t frames;
+    int64_t bit_errors;       /* over the K systematic info bits       */
+    int64_t frame_errors;     /* frames with >= 1 info bit error        */
+    int64_t cw_frame_errors;  /* frames with >= 1 codeword bit error    */
+    int64_t iter_sum;         /* sum of per-frame iteration counts      */
+    int64_t edge_visits;      /* sum of per-frame edge visits           */
+    int64_t not_converged;    /* frames with flags bit0 = 0             */
+    int64_t undetected_fires; /* failed syndrome verifications          */
+} cbp_counts;
+
+/* Fused channel + CBP decode + error counting for one Eb/N0 point (no LLR
+ * traffic through HBM).  Equivalent to cbp_channel -> cbp_decode -> compare. */
+cbp_status cbp_ber_sim(const cbp_code* code, double ebn0_db, uint64_t seed, int64_t frame_begin, int64_t frames,
+                       const cbp_opts* opts, int32_t llr_mode, cbp_counts* d_counts, void* stream);
+
+/* ----------------------------------------------------------- introspection */
+
+/* Launch geometry the library picks for this code (for reports): threads per
+ * CTA, CTAs per SM, frames per CTA, dynamic smem bytes, state in smem (1) or global (0). */
+typedef struct {
+    int32_t threads, ctas_per_sm, frames_per_cta, smem_bytes, state_in_smem, num_sms;
+} cbp_launch_info;
+cbp_status cbp_get_launch_info(const cbp_code* code, cbp_launch_info* out);
+
+/* Element-wise evaluation of the fp32 arithmetic contract on the device
+ * for the bit-equality pins: fn 0 phi32(x), 1 ln32(x),
+ * 2 / 3 sin / cos(2 pi m 2^-24) with m = the low 24 bits of x's bit pattern.
+ * d_x, d_y: device float[n] on `device`. */
+cbp_status cbp_eval_contract(int32_t fn, const float* d_x, float* d_y, int64_t n, int32_t device, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

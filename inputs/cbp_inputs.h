@@ -36,7 +36,7 @@ typedef struct {
     int32_t wmode;     /* CBP_W_*                                              */
     int32_t w_lo;
     int32_t w_hi;
-} cbp_construct_spec;
+} cbp_inputs_spec;
 
 /*
  * Draw a base matrix.  base_out must hold mb*nb int16.  Returns 0 on success,
@@ -45,12 +45,12 @@ typedef struct {
  * sampling, integer arithmetic only; the heavy-tailed rule uses one IEEE
  * double division).
  */
-int cbp_inputs_construct_base(const cbp_construct_spec* spec, uint64_t seed,
+int cbp_inputs_construct_base(const cbp_inputs_spec* spec, uint64_t seed,
                               int16_t* base_out, const char** err);
 
 /* Named specs of BASELINE.json configs: "C1", "C2", "C3a", "C3b", "C4",
  * plus "T24" (N=24 code for the brute-force ML pin).  Returns 0 if found. */
-int cbp_inputs_named_spec(const char* name, cbp_construct_spec* out);
+int cbp_inputs_named_spec(const char* name, cbp_inputs_spec* out);
 
 #ifdef __cplusplus
 }

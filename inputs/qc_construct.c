@@ -37,7 +37,7 @@ static uint32_t uniform_below(uint64_t* s, uint32_t n)
     return (uint32_t)(x % n);
 }
 
-int cbp_inputs_construct_base(const cbp_construct_spec* sp, uint64_t seed,
+int cbp_inputs_construct_base(const cbp_inputs_spec* sp, uint64_t seed,
                               int16_t* base, const char** err)
 {
     const char* dummy;
@@ -105,10 +105,10 @@ int cbp_inputs_construct_base(const cbp_construct_spec* sp, uint64_t seed,
     return 0;
 }
 
-int cbp_inputs_named_spec(const char* name, cbp_construct_spec* o)
+int cbp_inputs_named_spec(const char* name, cbp_inputs_spec* o)
 {
     /* BASELINE.json configs */
-    static const struct { const char* n; cbp_construct_spec s; } T[] = {
+    static const struct { const char* n; cbp_inputs_spec s; } T[] = {
         {"C1",  {6, 12, 8, 6, CBP_W_CONST, 3, 3}},
         {"C2",  {12, 24, 27, 12, CBP_W_UNIFORM, 3, 4}},
         {"C3a", {12, 24, 81, 12, CBP_W_UNIFORM, 3, 6}},

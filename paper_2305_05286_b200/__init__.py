@@ -1,0 +1,12 @@
+"""B200-native check-belief propagation (CBP) decoding of QC-LDPC codes.
+
+Guan & Liang, "Check-Belief Propagation Decoding of LDPC Codes" (arXiv
+2305.05286).  The hot path runs in sm_100a kernels behind the C ABI of
+include/cbp.h (libcbp.so); this package is the thin Python binding plus the
+multi-GPU counter reduction (dist.py).
+"""
+from .cbp import (CBP_STOP_BELIEF_M, CBP_STOP_BELIEF_N, CBP_STOP_NONE, CBP_STOP_SYNDROME, COUNT_NAMES, CbpError,
+                  Code, construct_base, lib, unpack_bits)
+
+__all__ = ["Code", "construct_base", "lib", "unpack_bits", "CbpError", "COUNT_NAMES", "CBP_STOP_BELIEF_M",
+           "CBP_STOP_BELIEF_N", "CBP_STOP_SYNDROME", "CBP_STOP_NONE"]

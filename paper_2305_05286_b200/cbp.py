@@ -1,0 +1,223 @@
+"""Thin ctypes binding of libcbp.so (include/cbp.h).
+
+Argument marshalling only: every step of the hot path runs in the sm_100a
+kernels behind the C ABI.  PyTorch is used for device memory and streams.
+There is no CPU fallback: if libcbp.so is missing or no CUDA device is
+present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import torch
+
+_HERE = Path(__file__).resolve().parent
+_SO = _HERE / "libcbp.so"
+_LIB = None
+
+CBP_STOP_BELIEF_M, CBP_STOP_BELIEF_N, CBP_STOP_SYNDROME, CBP_STOP_NONE = 0, 1, 2, 3
+COUNT_NAMES = ("frames", "bit_errors", "frame_errors", "cw_frame_errors", "iter_sum", "edge_visits",
+               "not_converged", "undetected_fires")
+
+_p, _i32, _i64, _u64, _f32, _f64 = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
+                                     ctypes.c_float, ctypes.c_double)
+
+
+class CbpError(RuntimeError):
+    pass
+
+
+class _Spec(ctypes.Structure):
+    _fields_ = [(n, _i32) for n in ("mb", "nb", "Z", "mb_core", "wmode", "w_lo", "w_hi")]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("max_iter", _i32), ("stop_rule", _i32), ("reserved", _i32 * 2)]
+
+
+class LaunchInfo(ctypes.Structure):
+    _fields_ = [(n, _i32) for n in ("threads", "ctas_per_sm", "frames_per_cta", "smem_bytes", "state_in_smem",
+                                    "num_sms")]
+
+
+SIGNATURES = {
+    "cbp_last_error": ([], ctypes.c_char_p),
+    "cbp_version": ([], ctypes.c_char_p),
+    "cbp_construct_base": ([_p, _u64, _p], _i32),
+    "cbp_code_create": ([_p, _i32, _i32, _i32, _i32, _p], _i32),
+    "cbp_code_destroy": ([_p], None),
+    "cbp_code_dims": ([_p, _p, _p, _p, _p], _i32),
+    "cbp_decode": ([_p, _p, _i64, _i64, _p, _p, _i64, _p, _p, _p, _p, _p], _i32),
+    "cbp_decode_i8": ([_p, _p, _i64, _f32, _i64, _p, _p, _i64, _p, _p, _p, _p, _p], _i32),
+    "cbp_channel": ([_p, _f64, _u64, _i64, _i64, _i32, _p, _i64, _p, _i64, _p], _i32),
+    "cbp_ber_sim": ([_p, _f64, _u64, _i64, _i64, _p, _i32, _p, _p], _i32),
+    "cbp_get_launch_info": ([_p, _p], _i32),
+    "cbp_eval_contract": ([_i32, _p, _p, _i64, _i32, _p], _i32),
+}
+
+
+def lib():
+    """Load libcbp.so (fails loudly if it was not built)."""
+    global _LIB
+    if _LIB is None:
+        if not _SO.exists():
+            raise CbpError(f"{_SO} not found: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(str(_SO))
+        for name, (args, res) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _LIB = L
+    return _LIB
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise CbpError(f"{what} failed (status {rc}): {lib().cbp_last_error().decode()}")
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _dptr(t: torch.Tensor | None, dtype, device, name):
+    if t is None:
+        return None
+    if not t.is_cuda or t.device != device:
+        raise CbpError(f"{name} must be a CUDA tensor on {device}")
+    if t.dtype != dtype:
+        raise CbpError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise CbpError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def construct_base(spec, seed: int):
+    """cbp_construct_base: spec = (mb, nb, Z, mb_core, wmode, w_lo, w_hi) -> int16 [mb, nb] (torch, CPU)."""
+    s = _Spec(*[int(x) for x in spec])
+    out = torch.empty((s.mb, s.nb), dtype=torch.int16)
+    _check(lib().cbp_construct_base(ctypes.byref(s), seed, out.data_ptr()), "cbp_construct_base")
+    return out
+
+
+class Code:
+    """cbp_code_create / cbp_code_destroy: a QC code resident on one CUDA device."""
+
+    def __init__(self, base, Z: int, device=None):
+        base_t = torch.as_tensor(base, dtype=torch.int16).contiguous().cpu()
+        self.mb, self.nb = base_t.shape
+        self.Z = int(Z)
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
+                                   torch.device(device).index or 0)
+        h = ctypes.c_void_p()
+        _check(lib().cbp_code_create(base_t.data_ptr(), self.mb, self.nb, self.Z, self.device.index,
+                                     ctypes.byref(h)), "cbp_code_create")
+        self._h = h
+        N, K, M, E = _i32(), _i32(), _i32(), _i64()
+        _check(lib().cbp_code_dims(h, ctypes.byref(N), ctypes.byref(K), ctypes.byref(M), ctypes.byref(E)),
+               "cbp_code_dims")
+        self.N, self.K, self.M, self.E = N.value, K.value, M.value, E.value
+        self.words = (self.N + 31) // 32
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _LIB is not None:
+            _LIB.cbp_code_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def launch_info(self) -> dict:
+        li = LaunchInfo()
+        _check(lib().cbp_get_launch_info(self._h, ctypes.byref(li)), "cbp_get_launch_info")
+        return {n: getattr(li, n) for n, _ in LaunchInfo._fields_}
+
+    # -------------------------------------------------------------- decode
+    def alloc_outputs(self, frames: int, omega: bool = False, ev: bool = False) -> dict:
+        d = self.device
+        out = {"bits": torch.empty((frames, self.words), dtype=torch.int32, device=d),
+               "iters": torch.empty(frames, dtype=torch.int32, device=d),
+               "flags": torch.empty(frames, dtype=torch.uint8, device=d)}
+        if omega:
+            out["omega"] = torch.empty((frames, self.M), dtype=torch.float32, device=d)
+        if ev:
+            out["ev"] = torch.empty(frames, dtype=torch.int64, device=d)
+        return out
+
+    def decode(self, llr: torch.Tensor, max_iter: int, stop_rule: int = CBP_STOP_BELIEF_M, out: dict | None = None,
+               omega: bool = False, ev: bool = False, stream=None) -> dict:
+        """cbp_decode: llr float32 [frames, ld] on the code's device (ld >= N, ld % 4 == 0)."""
+        frames, ld = llr.shape
+        out = out if out is not None else self.alloc_outputs(frames, omega, ev)
+        o = _Opts(max_iter, stop_rule, (_i32 * 2)(0, 0))
+        d = self.device
+        rc = lib().cbp_decode(self._h, _dptr(llr, torch.float32, d, "llr"), ld, frames, ctypes.byref(o),
+                              _dptr(out["bits"], torch.int32, d, "bits"), out["bits"].shape[1],
+                              _dptr(out["iters"], torch.int32, d, "iters"), _dptr(out["flags"], torch.uint8, d, "flags"),
+                              _dptr(out.get("omega"), torch.float32, d, "omega"),
+                              _dptr(out.get("ev"), torch.int64, d, "ev"), _stream(stream))
+        _check(rc, "cbp_decode")
+        return out
+
+    def decode_i8(self, q: torch.Tensor, scale: float, max_iter: int, stop_rule: int = CBP_STOP_BELIEF_M,
+                  out: dict | None = None, omega: bool = False, ev: bool = False, stream=None) -> dict:
+        """cbp_decode_i8: q int8 [frames, ld] (ld % 16 == 0), L = scale * q."""
+        frames, ld = q.shape
+        out = out if out is not None else self.alloc_outputs(frames, omega, ev)
+        o = _Opts(max_iter, stop_rule, (_i32 * 2)(0, 0))
+        d = self.device
+        rc = lib().cbp_decode_i8(self._h, _dptr(q, torch.int8, d, "q"), ld, scale, frames, ctypes.byref(o),
+                                 _dptr(out["bits"], torch.int32, d, "bits"), out["bits"].shape[1],
+                                 _dptr(out["iters"], torch.int32, d, "iters"),
+                                 _dptr(out["flags"], torch.uint8, d, "flags"),
+                                 _dptr(out.get("omega"), torch.float32, d, "omega"),
+                                 _dptr(out.get("ev"), torch.int64, d, "ev"), _stream(stream))
+        _check(rc, "cbp_decode_i8")
+        return out
+
+    # -------------------------------------------------------------- channel / ber
+    def channel(self, ebn0_db: float, seed: int, frame_begin: int, frames: int, llr_mode: int = 0,
+                ld: int | None = None, want_llr: bool = True, want_cw: bool = True, stream=None):
+        """cbp_channel: returns (llr float32 [frames, ld] or None, codewords int32 [frames, words] or None)."""
+        d = self.device
+        ld = ld or (self.N + 3) // 4 * 4
+        llr = torch.empty((frames, ld), dtype=torch.float32, device=d) if want_llr else None
+        cw = torch.empty((frames, self.words), dtype=torch.int32, device=d) if want_cw else None
+        rc = lib().cbp_channel(self._h, float(ebn0_db), seed, frame_begin, frames, llr_mode,
+                               _dptr(llr, torch.float32, d, "llr"), ld, _dptr(cw, torch.int32, d, "cw"), self.words,
+                               _stream(stream))
+        _check(rc, "cbp_channel")
+        return llr, cw
+
+    def ber_sim(self, ebn0_db: float, seed: int, frame_begin: int, frames: int, max_iter: int,
+                stop_rule: int = CBP_STOP_BELIEF_M, llr_mode: int = 0, counts: torch.Tensor | None = None,
+                stream=None) -> torch.Tensor:
+        """cbp_ber_sim: accumulates into `counts` (int64 [8] on device; zeroed if not given)."""
+        if counts is None:
+            counts = torch.zeros(8, dtype=torch.int64, device=self.device)
+        o = _Opts(max_iter, stop_rule, (_i32 * 2)(0, 0))
+        rc = lib().cbp_ber_sim(self._h, float(ebn0_db), seed, frame_begin, frames, ctypes.byref(o), llr_mode,
+                               _dptr(counts, torch.int64, self.device, "counts"), _stream(stream))
+        _check(rc, "cbp_ber_sim")
+        return counts
+
+
+def eval_contract(fn: int, x: torch.Tensor, stream=None) -> torch.Tensor:
+    """cbp_eval_contract: device evaluation of phi32 (0), ln32 (1), sin (2) / cos (3) of 2 pi m 2^-24."""
+    y = torch.empty_like(x)
+    _check(lib().cbp_eval_contract(fn, _dptr(x, torch.float32, x.device, "x"), y.data_ptr(), x.numel(),
+                                   x.device.index, _stream(stream)), "cbp_eval_contract")
+    return y
+
+
+def unpack_bits(words: torch.Tensor, n: int) -> torch.Tensor:
+    """int32/uint32 words [.., W] (bit v%32 of word v/32) -> uint8 bits [.., n] (on the same device)."""
+    w = words.to(torch.int64) & 0xFFFFFFFF
+    shifts = torch.arange(32, device=words.device, dtype=torch.int64)
+    b = (w.unsqueeze(-1) >> shifts) & 1
+    return b.reshape(*words.shape[:-1], -1)[..., :n].to(torch.uint8)

@@ -1,0 +1,436 @@
+// cbp_api.cpp -- host side of the C ABI (include/cbp.h): validation, schedule
+// tables of the expanded code graph, launch geometry, launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "cbp.h"
+#include "cbp_inputs.h"
+#include "cbp_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+cbp_status fail(cbp_status s, const std::string& msg)
+{
+    g_err = msg;
+    return s;
+}
+
+cbp_status cuda_fail(cudaError_t e, const char* what)
+{
+    return fail(CBP_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// RAII switch of the current device
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) return;
+        ok = (prev == dev) || cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard()
+    {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+struct cbp_code {
+    int device = 0;
+    int32_t mb = 0, nb = 0, Z = 0, N = 0, K = 0, M = 0, kb = 0, core = 0, mid = 0, nent = 0, max_dc = 0;
+    int64_t E = 0;
+    bool can_encode = false;
+    int4* d_ent = nullptr;
+    int32_t* d_row_ptr = nullptr;
+    int16_t* d_pshift = nullptr;
+    cbp::Geometry geo{};
+    int ctas_per_sm = 1, num_sms = 1;
+};
+
+extern "C" {
+
+const char* cbp_last_error(void) { return g_err.c_str(); }
+
+const char* cbp_version(void) { return "cbp-b200 0.1 (sm_100a)"; }
+
+cbp_status cbp_construct_base(const cbp_construct_spec* spec, uint64_t seed, int16_t* base_out)
+{
+    if (!spec || !base_out) return fail(CBP_E_INVALID, "cbp_construct_base: null argument");
+    cbp_inputs_spec s{spec->mb, spec->nb, spec->Z, spec->mb_core, spec->wmode, spec->w_lo, spec->w_hi};
+    const char* err = nullptr;
+    if (cbp_inputs_construct_base(&s, seed, base_out, &err) != 0)
+        return fail(CBP_E_INVALID, std::string("cbp_construct_base: ") + (err ? err : "invalid spec"));
+    return CBP_OK;
+}
+
+void cbp_code_destroy(cbp_code* c)
+{
+    if (!c) return;
+    DeviceGuard g(c->device);
+    cudaFree(c->d_ent);
+    cudaFree(c->d_row_ptr);
+    cudaFree(c->d_pshift);
+    delete c;
+}
+
+cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t Z, int32_t device, cbp_code** out)
+{
+    if (!base || !out) return fail(CBP_E_INVALID, "cbp_code_create: null argument");
+    *out = nullptr;
+    if (mb < 1 || nb <= mb) return fail(CBP_E_INVALID, "cbp_code_create: need 1 <= mb < nb");
+    if (Z < 1 || Z > 1024) return fail(CBP_E_INVALID, "cbp_code_create: need 1 <= Z <= 1024");
+    if (static_cast<int64_t>(nb) * Z > 65535 || static_cast<int64_t>(mb) * Z > 65535)
+        return fail(CBP_E_UNSUPPORTED, "cbp_code_create: N and M must be < 65536");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return fail(CBP_E_INVALID, "cbp_code_create: no such CUDA device");
+
+    std::vector<int32_t> colw(nb, 0), roww(mb, 0);
+    for (int i = 0; i < mb; ++i)
+        for (int j = 0; j < nb; ++j) {
+            const int s = base[i * nb + j];
+            if (s < -1 || s >= Z) return fail(CBP_E_INVALID, "cbp_code_create: shift out of [-1, Z)");
+            if (s >= 0) { ++colw[j]; ++roww[i]; }
+        }
+    for (int j = 0; j < nb; ++j)
+        if (!colw[j]) return fail(CBP_E_INVALID, "cbp_code_create: empty base column");
+    for (int i = 0; i < mb; ++i)
+        if (!roww[i]) return fail(CBP_E_INVALID, "cbp_code_create: empty base row");
+    const int max_dc = *std::max_element(roww.begin(), roww.end());
+    if (max_dc > 32) return fail(CBP_E_UNSUPPORTED, "cbp_code_create: base row degree > 32");
+
+    // entries row-major; per column the list of its nonzero rows (ascending)
+    std::vector<int> ent_row, ent_col, ent_s, row_ptr(mb + 1, 0);
+    std::vector<std::vector<int>> col_ent(nb);
+    for (int i = 0; i < mb; ++i) {
+        for (int j = 0; j < nb; ++j) {
+            const int s = base[i * nb + j];
+            if (s < 0) continue;
+            col_ent[j].push_back(static_cast<int>(ent_row.size()));
+            ent_row.push_back(i);
+            ent_col.push_back(j);
+            ent_s.push_back(s);
+        }
+        row_ptr[i + 1] = static_cast<int>(ent_row.size());
+    }
+    const int nent = static_cast<int>(ent_row.size());
+    std::vector<int4> ent(nent);
+    for (int j = 0; j < nb; ++j) {
+        const auto& L = col_ent[j];
+        for (size_t k = 0; k < L.size(); ++k) {
+            const int b = L[k];
+            const int p = L[(k + L.size() - 1) % L.size()];       // previous nonzero row of column j, cyclic
+            const int ds = ((ent_s[b] - ent_s[p]) % Z + Z) % Z;
+            const int first = (k == 0) ? 1 : 0;                   // R1: no latest check before this visit
+            const int self = (p == b) ? 1 : 0;                    // R3: degree-1 column
+            ent[b].x = (j * Z) | ((ent_row[p] * Z) << 16);
+            ent[b].y = ent_s[b] | (ds << 11) | (first << 22) | (self << 23);
+            ent[b].z = b * Z;
+            ent[b].w = p * Z;
+        }
+    }
+
+    cbp_code* c = new cbp_code();
+    c->device = device;
+    c->mb = mb; c->nb = nb; c->Z = Z;
+    c->N = nb * Z; c->M = mb * Z; c->K = c->N - c->M; c->kb = nb - mb;
+    c->E = static_cast<int64_t>(nent) * Z;
+    c->nent = nent;
+    c->max_dc = max_dc;
+
+    // encoder structure: dual-diagonal core + degree-1 extension
+    {
+        const int kb = c->kb;
+        int core = 0;
+        while (kb + core < nb && colw[kb + core] >= 2) ++core;
+        bool ok = core >= 3;
+        const int mid = core / 2;
+        auto at = [&](int i, int j) { return static_cast<int>(base[i * nb + j]); };
+        if (ok) {
+            for (int i = 0; i < mb && ok; ++i) {
+                const bool want = (i == 0 || i == mid || i == core - 1);
+                ok = want == (at(i, kb) >= 0);
+            }
+            ok = ok && at(mid, kb) == 0 && at(0, kb) == at(core - 1, kb);
+            for (int t = 1; t < core && ok; ++t)
+                for (int i = 0; i < mb && ok; ++i) {
+                    const bool want = (i == t - 1 || i == t);
+                    ok = want ? at(i, kb + t) == 0 : at(i, kb + t) < 0;
+                }
+            ok = ok && (nb - kb - core) == (mb - core);
+            for (int k = 0; kb + core + k < nb && ok; ++k)
+                for (int i = 0; i < mb && ok; ++i) {
+                    const bool want = (i == core + k);
+                    ok = want ? at(i, kb + core + k) == 0 : at(i, kb + core + k) < 0;
+                }
+        }
+        c->can_encode = ok;
+        c->core = ok ? core : 0;
+        c->mid = ok ? mid : 0;
+    }
+    std::vector<int16_t> pshift(mb, -1);
+    for (int i = 0; i < mb; ++i) pshift[i] = base[i * nb + c->kb];
+
+    DeviceGuard g(device);
+    if (!g.ok) { delete c; return fail(CBP_E_CUDA, "cbp_code_create: cudaSetDevice failed"); }
+    cudaError_t e;
+    if ((e = cudaMalloc(&c->d_ent, sizeof(int4) * nent)) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_row_ptr, sizeof(int32_t) * (mb + 1))) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_pshift, sizeof(int16_t) * mb)) != cudaSuccess) {
+        cbp_code_destroy(c);
+        return fail(CBP_E_NOMEM, std::string("cbp_code_create: ") + cudaGetErrorString(e));
+    }
+    if ((e = cudaMemcpy(c->d_ent, ent.data(), sizeof(int4) * nent, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(c->d_row_ptr, row_ptr.data(), sizeof(int32_t) * (mb + 1), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(c->d_pshift, pshift.data(), sizeof(int16_t) * mb, cudaMemcpyHostToDevice)) != cudaSuccess) {
+        cbp_code_destroy(c);
+        return cuda_fail(e, "cbp_code_create: cudaMemcpy");
+    }
+
+    // ---- launch geometry
+    cbp::Geometry& G = c->geo;
+    const int nwords = (c->N + 31) / 32;
+    if (Z <= 16) {
+        int zp = 1;
+        while (zp < Z) zp <<= 1;
+        G.Zp = zp; G.F = 32 / zp; G.threads = 32; G.multi = 0;
+    } else if (Z <= 32) {
+        G.Zp = 32; G.F = 1; G.threads = 32; G.multi = 0;
+    } else {
+        G.Zp = (Z + 31) / 32 * 32; G.F = 1; G.threads = G.Zp; G.multi = 1;
+    }
+    const int64_t raw = 2LL * c->N + c->E + c->M + nwords;
+    G.slot_words = static_cast<int32_t>(G.F > 1 ? (raw + 31) / 32 * 32 + G.Zp : (raw + 3) / 4 * 4);
+    G.table_words = (4 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4;
+    int smem_optin = 0, nsm = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    const int64_t full = 4LL * (G.table_words + 96 + static_cast<int64_t>(G.F) * G.slot_words);
+    G.state_in_smem = full <= smem_optin ? 1 : 0;
+    G.smem_bytes = static_cast<int32_t>(G.state_in_smem ? full : 4LL * (G.table_words + 96));
+    c->num_sms = nsm > 0 ? nsm : 1;
+    int occ = 0;
+    if (cbp::occupancy_ctas_per_sm(G, &occ) != 0 || occ < 1) {
+        cudaGetLastError();
+        cbp_code_destroy(c);
+        return fail(CBP_E_UNSUPPORTED, "cbp_code_create: kernel does not fit on this device");
+    }
+    c->ctas_per_sm = G.state_in_smem ? occ : 1;
+    *out = c;
+    return CBP_OK;
+}
+
+cbp_status cbp_code_dims(const cbp_code* c, int32_t* N, int32_t* K, int32_t* M, int64_t* E)
+{
+    if (!c) return fail(CBP_E_INVALID, "cbp_code_dims: null code");
+    if (N) *N = c->N;
+    if (K) *K = c->K;
+    if (M) *M = c->M;
+    if (E) *E = c->E;
+    return CBP_OK;
+}
+
+cbp_status cbp_get_launch_info(const cbp_code* c, cbp_launch_info* o)
+{
+    if (!c || !o) return fail(CBP_E_INVALID, "cbp_get_launch_info: null argument");
+    o->threads = c->geo.threads;
+    o->ctas_per_sm = c->ctas_per_sm;
+    o->frames_per_cta = c->geo.F;
+    o->smem_bytes = c->geo.smem_bytes;
+    o->state_in_smem = c->geo.state_in_smem;
+    o->num_sms = c->num_sms;
+    return CBP_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+cbp::KernelArgs base_args(const cbp_code* c)
+{
+    cbp::KernelArgs a{};
+    cbp::DevCode& d = a.code;
+    d.N = c->N; d.K = c->K; d.M = c->M; d.Z = c->Z; d.mb = c->mb; d.nb = c->nb; d.kb = c->kb; d.core = c->core;
+    d.nent = c->nent; d.E = static_cast<int32_t>(c->E); d.nwords = (c->N + 31) / 32; d.kwords = (c->K + 31) / 32;
+    d.max_dc = c->max_dc; d.can_encode = c->can_encode; d.mid = c->mid;
+    d.ent = c->d_ent; d.row_ptr = c->d_row_ptr; d.pshift = c->d_pshift;
+    a.Zp = c->geo.Zp; a.F = c->geo.F; a.slot_words = c->geo.slot_words; a.table_words = c->geo.table_words;
+    a.max_iter = 1; a.stop_rule = 0;
+    return a;
+}
+
+cbp_status check_opts(const cbp_opts* o)
+{
+    if (!o) return fail(CBP_E_INVALID, "null opts");
+    if (o->max_iter < 1 || o->max_iter > 65535) return fail(CBP_E_INVALID, "opts.max_iter must be in [1, 65535]");
+    if (o->stop_rule < 0 || o->stop_rule > 3) return fail(CBP_E_INVALID, "opts.stop_rule must be in [0, 3]");
+    if (o->reserved[0] || o->reserved[1]) return fail(CBP_E_INVALID, "opts.reserved must be 0");
+    return CBP_OK;
+}
+
+// allocate the work queue (+ global state), launch, release -- all stream-ordered
+cbp_status run(const cbp_code* c, cbp::KernelArgs& a, int64_t frames, void* stream, const char* who)
+{
+    DeviceGuard g(c->device);
+    if (!g.ok) return fail(CBP_E_CUDA, std::string(who) + ": cudaSetDevice failed");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t ctas_needed = (frames + c->geo.F - 1) / c->geo.F;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(c->num_sms) * c->ctas_per_sm, ctas_needed)));
+    cudaError_t e;
+    unsigned long long* q = nullptr;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&q), sizeof(unsigned long long), st)) != cudaSuccess)
+        return fail(CBP_E_NOMEM, std::string(who) + ": " + cudaGetErrorString(e));
+    float* gs = nullptr;
+    if (!c->geo.state_in_smem) {
+        const size_t bytes = sizeof(float) * static_cast<size_t>(grid) * c->geo.F * c->geo.slot_words;
+        if ((e = cudaMallocAsync(reinterpret_cast<void**>(&gs), bytes, st)) != cudaSuccess) {
+            cudaFreeAsync(q, st);
+            return fail(CBP_E_NOMEM, std::string(who) + ": " + cudaGetErrorString(e));
+        }
+    }
+    a.queue = q;
+    a.gstate = gs;
+    e = cudaMemsetAsync(q, 0, sizeof(unsigned long long), st);
+    int le = (e == cudaSuccess) ? cbp::launch_cbp(a, c->geo, grid, stream) : static_cast<int>(e);
+    cudaFreeAsync(q, st);
+    if (gs) cudaFreeAsync(gs, st);
+    if (le != 0) return cuda_fail(static_cast<cudaError_t>(le), who);
+    return CBP_OK;
+}
+
+void channel_params(const cbp_code* c, double ebn0_db, float* sigma, float* scale)
+{
+    // sigma^2 = 1 / (2 R 10^(Eb/N0 / 10)), R = K/N; L = 2 y / sigma^2 (reading R17)
+    const double R = static_cast<double>(c->K) / static_cast<double>(c->N);
+    const double sigma2 = 1.0 / (2.0 * R * std::pow(10.0, ebn0_db / 10.0));
+    *sigma = static_cast<float>(std::sqrt(sigma2));
+    *scale = static_cast<float>(2.0 / sigma2);
+}
+
+cbp_status decode_common(const cbp_code* c, const void* in, int32_t mode, int64_t ld, float scale, int64_t frames,
+                         const cbp_opts* opts, uint32_t* d_bits, int64_t ld_words, int32_t* d_iters, uint8_t* d_flags,
+                         float* d_omega, int64_t* d_ev, void* stream, const char* who)
+{
+    if (!c) return fail(CBP_E_INVALID, std::string(who) + ": null code");
+    cbp_status s = check_opts(opts);
+    if (s != CBP_OK) return s;
+    if (frames < 0) return fail(CBP_E_INVALID, std::string(who) + ": frames < 0");
+    if (frames == 0) return CBP_OK;
+    if (!in || !d_bits || !d_iters || !d_flags) return fail(CBP_E_INVALID, std::string(who) + ": null buffer");
+    const int64_t esz = (mode == cbp::MODE_DECODE_I8) ? 1 : 4;
+    if (ld < c->N || (ld * esz) % 16 != 0) return fail(CBP_E_INVALID, std::string(who) + ": need ld >= N and ld*elem % 16 == 0");
+    if (reinterpret_cast<uintptr_t>(in) % 16 != 0) return fail(CBP_E_INVALID, std::string(who) + ": input not 16-byte aligned");
+    if (ld_words < (c->N + 31) / 32) return fail(CBP_E_INVALID, std::string(who) + ": ld_words < ceil(N/32)");
+    if (mode == cbp::MODE_DECODE_I8 && !(std::isfinite(scale) && scale > 0.0f))
+        return fail(CBP_E_INVALID, std::string(who) + ": scale must be finite and > 0");
+    cbp::KernelArgs a = base_args(c);
+    a.mode = mode;
+    a.max_iter = opts->max_iter;
+    a.stop_rule = opts->stop_rule;
+    a.llr = static_cast<const float*>(in);
+    a.q = static_cast<const int8_t*>(in);
+    a.ld = ld;
+    a.qscale = scale;
+    a.frames = frames;
+    a.bits = d_bits;
+    a.ld_words = ld_words;
+    a.iters = d_iters;
+    a.flags = d_flags;
+    a.omega = d_omega;
+    a.ev = d_ev;
+    return run(c, a, frames, stream, who);
+}
+
+}  // namespace
+
+extern "C" {
+
+cbp_status cbp_decode(const cbp_code* c, const float* d_llr, int64_t ld, int64_t frames, const cbp_opts* opts,
+                      uint32_t* d_bits, int64_t ld_words, int32_t* d_iters, uint8_t* d_flags, float* d_omega,
+                      int64_t* d_ev, void* stream)
+{
+    return decode_common(c, d_llr, cbp::MODE_DECODE_F32, ld, 1.0f, frames, opts, d_bits, ld_words, d_iters, d_flags,
+                         d_omega, d_ev, stream, "cbp_decode");
+}
+
+cbp_status cbp_decode_i8(const cbp_code* c, const int8_t* d_q, int64_t ld, float scale, int64_t frames,
+                         const cbp_opts* opts, uint32_t* d_bits, int64_t ld_words, int32_t* d_iters, uint8_t* d_flags,
+                         float* d_omega, int64_t* d_ev, void* stream)
+{
+    return decode_common(c, d_q, cbp::MODE_DECODE_I8, ld, scale, frames, opts, d_bits, ld_words, d_iters, d_flags,
+                         d_omega, d_ev, stream, "cbp_decode_i8");
+}
+
+cbp_status cbp_channel(const cbp_code* c, double ebn0_db, uint64_t seed, int64_t frame_begin, int64_t frames,
+                       int32_t llr_mode, float* d_llr, int64_t ld, uint32_t* d_cw, int64_t ld_words, void* stream)
+{
+    if (!c) return fail(CBP_E_INVALID, "cbp_channel: null code");
+    if (!c->can_encode) return fail(CBP_E_UNSUPPORTED, "cbp_channel: base has no dual-diagonal encoder structure");
+    if (frames < 0 || frame_begin < 0) return fail(CBP_E_INVALID, "cbp_channel: negative frame range");
+    if (llr_mode != 0 && llr_mode != 1) return fail(CBP_E_INVALID, "cbp_channel: llr_mode must be 0 or 1");
+    if (!std::isfinite(ebn0_db)) return fail(CBP_E_INVALID, "cbp_channel: ebn0_db not finite");
+    if (frames == 0) return CBP_OK;
+    if (!d_llr && !d_cw) return fail(CBP_E_INVALID, "cbp_channel: both outputs NULL");
+    if (d_llr && ld < c->N) return fail(CBP_E_INVALID, "cbp_channel: ld < N");
+    if (d_cw && ld_words < (c->N + 31) / 32) return fail(CBP_E_INVALID, "cbp_channel: ld_words < ceil(N/32)");
+    cbp::KernelArgs a = base_args(c);
+    a.mode = cbp::MODE_CHANNEL;
+    a.frames = frames;
+    a.frame_begin = frame_begin;
+    a.seed = seed;
+    a.llr_mode = llr_mode;
+    channel_params(c, ebn0_db, &a.sigma, &a.scale);
+    a.llr_out = d_llr;
+    a.ld = ld;
+    a.cw_out = d_cw;
+    a.ld_words = ld_words;
+    return run(c, a, frames, stream, "cbp_channel");
+}
+
+cbp_status cbp_ber_sim(const cbp_code* c, double ebn0_db, uint64_t seed, int64_t frame_begin, int64_t frames,
+                       const cbp_opts* opts, int32_t llr_mode, cbp_counts* d_counts, void* stream)
+{
+    if (!c) return fail(CBP_E_INVALID, "cbp_ber_sim: null code");
+    if (!c->can_encode) return fail(CBP_E_UNSUPPORTED, "cbp_ber_sim: base has no dual-diagonal encoder structure");
+    cbp_status s = check_opts(opts);
+    if (s != CBP_OK) return s;
+    if (frames < 0 || frame_begin < 0) return fail(CBP_E_INVALID, "cbp_ber_sim: negative frame range");
+    if (llr_mode != 0 && llr_mode != 1) return fail(CBP_E_INVALID, "cbp_ber_sim: llr_mode must be 0 or 1");
+    if (!std::isfinite(ebn0_db)) return fail(CBP_E_INVALID, "cbp_ber_sim: ebn0_db not finite");
+    if (!d_counts) return fail(CBP_E_INVALID, "cbp_ber_sim: null counts");
+    if (frames == 0) return CBP_OK;
+    cbp::KernelArgs a = base_args(c);
+    a.mode = cbp::MODE_BER_SIM;
+    a.max_iter = opts->max_iter;
+    a.stop_rule = opts->stop_rule;
+    a.frames = frames;
+    a.frame_begin = frame_begin;
+    a.seed = seed;
+    a.llr_mode = llr_mode;
+    channel_params(c, ebn0_db, &a.sigma, &a.scale);
+    a.counts = reinterpret_cast<unsigned long long*>(d_counts);
+    return run(c, a, frames, stream, "cbp_ber_sim");
+}
+
+cbp_status cbp_eval_contract(int32_t fn, const float* d_x, float* d_y, int64_t n, int32_t device, void* stream)
+{
+    if (fn < 0 || fn > 3) return fail(CBP_E_INVALID, "cbp_eval_contract: fn must be 0..3");
+    if (n < 0 || (n > 0 && (!d_x || !d_y))) return fail(CBP_E_INVALID, "cbp_eval_contract: bad buffers");
+    DeviceGuard g(device);
+    if (!g.ok) return fail(CBP_E_CUDA, "cbp_eval_contract: cudaSetDevice failed");
+    const int e = cbp::launch_contract_eval(fn, d_x, d_y, n, stream);
+    if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cbp_eval_contract");
+    return CBP_OK;
+}
+
+}  // extern "C"

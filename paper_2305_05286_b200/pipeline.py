@@ -1,0 +1,46 @@
+"""Host-buffer decoding: chunked, double-buffered H2D -> cbp_decode -> D2H on
+two CUDA streams so PCIe transfers overlap the decode kernel (the end-to-end
+call a user with LLRs in host memory makes)."""
+from __future__ import annotations
+
+import torch
+
+from .cbp import CBP_STOP_BELIEF_M, Code
+
+
+def alloc_host_outputs(code: Code, frames: int) -> dict:
+    return {"bits": torch.empty((frames, code.words), dtype=torch.int32, pin_memory=True),
+            "iters": torch.empty(frames, dtype=torch.int32, pin_memory=True),
+            "flags": torch.empty(frames, dtype=torch.uint8, pin_memory=True)}
+
+
+def decode_host(code: Code, llr_host: torch.Tensor, max_iter: int, stop_rule: int = CBP_STOP_BELIEF_M,
+                out: dict | None = None, chunk: int = 1 << 17, streams=None) -> dict:
+    """Decode float32 LLRs [frames, ld] held in (pinned) host memory; returns pinned host outputs.
+
+    The copies and launches are enqueued on two streams; the call returns after
+    synchronising them, so the outputs are ready."""
+    frames, ld = llr_host.shape
+    out = out if out is not None else alloc_host_outputs(code, frames)
+    if frames == 0:
+        return out
+    dev = code.device
+    streams = streams or [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+    n = min(chunk, frames)
+    bufs = [(torch.empty((n, ld), dtype=torch.float32, device=dev), code.alloc_outputs(n)) for _ in streams]
+    cur = torch.cuda.current_stream(dev)
+    for s in streams:
+        s.wait_stream(cur)
+    for k, b in enumerate(range(0, frames, n)):
+        e = min(b + n, frames)
+        s = streams[k % len(streams)]
+        dl, dout = bufs[k % len(streams)]
+        with torch.cuda.stream(s):
+            dl[: e - b].copy_(llr_host[b:e], non_blocking=True)
+            o = {key: v[: e - b] for key, v in dout.items()}
+            code.decode(dl[: e - b], max_iter, stop_rule, out=o, stream=s)
+            for key in ("bits", "iters", "flags"):
+                out[key][b:e].copy_(o[key], non_blocking=True)
+    for s in streams:
+        s.synchronize()
+    return out

@@ -1,0 +1,208 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element on identical seeded inputs.  Bar: bits, iteration
+counts, flags, edge visits and BER/FER counters bit-exact; check-beliefs
+(Omega) within 1e-5 absolute (observed: exact)."""
+import numpy as np
+import pytest
+import torch
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+cbp = pytest.importorskip("paper_2305_05286_b200")
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.fixture(scope="module")
+def codes():
+    _need_gpu()
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            base, Z = inputs.config_base(name)
+            cache[name] = (cbp.Code(base, Z), oracle.OracleCode(base, Z))
+        return cache[name]
+    return get
+
+
+def gpu_decode(g, llr_np, max_iter, rule=0, ld=None):
+    F, N = llr_np.shape
+    ld = ld or (N + 3) // 4 * 4
+    x = torch.zeros((F, ld), dtype=torch.float32)
+    x[:, :N] = torch.from_numpy(llr_np)
+    out = g.decode(x.cuda(), max_iter, rule, omega=True, ev=True)
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def assert_same(go, oo, N, omega=True):
+    W = oo["bits"].shape[1]
+    gb = go["bits"].view(np.uint32)[:, :W]
+    bad = np.nonzero(~(gb == oo["bits"]).all(axis=1) | (go["iters"] != oo["iters"]) |
+                     (go["flags"] != oo["flags"]) | (go["ev"] != oo["edge_visits"]))[0]
+    assert len(bad) == 0, (f"{len(bad)} frames differ, first {bad[:5]}: gpu iters {go['iters'][bad[:5]]} "
+                           f"oracle {oo['iters'][bad[:5]]}; flags {go['flags'][bad[:5]]} vs {oo['flags'][bad[:5]]}")
+    if omega:
+        np.testing.assert_allclose(go["omega"], oo["omega"], rtol=0, atol=1e-5)
+
+
+# ---------------------------------------------------------------- contract bits
+def test_contract_bit_equal_on_device():
+    _need_gpu()
+    rng = np.random.default_rng(0)
+    lo, hi = np.log(1e-14), np.log(40.0)
+    x = np.concatenate([np.exp(rng.uniform(lo, hi, 1 << 22)), [0.0, 1.0, 30.0, 1e-40, 1e30, np.inf]]).astype(np.float32)
+    # dense exhaustive slice around the regime switch x = 1 and the clamp 30
+    for centre in (1.0, 30.0, oracle.PHI_LO):
+        b = np.float32(centre).view(np.uint32).astype(np.int64)
+        x = np.concatenate([x, (np.arange(b - 100000, b + 100000)).astype(np.uint32).view(np.float32)])
+    y_gpu = cbp.cbp.eval_contract(0, torch.from_numpy(x).cuda()).cpu().numpy()
+    y_ora = oracle.phi32_array(x)
+    assert (y_gpu.view(np.uint32) == y_ora.view(np.uint32)).all()
+    u = (np.arange(1, 1 << 24, 7, dtype=np.float64) * 2.0 ** -24).astype(np.float32)
+    assert (cbp.cbp.eval_contract(1, torch.from_numpy(u).cuda()).cpu().numpy().view(np.uint32) ==
+            oracle.ln32_array(u).view(np.uint32)).all()
+    m = np.arange(0, 1 << 24, 13, dtype=np.uint32)
+    s_gpu = cbp.cbp.eval_contract(2, torch.from_numpy(m.view(np.float32)).cuda()).cpu().numpy()
+    c_gpu = cbp.cbp.eval_contract(3, torch.from_numpy(m.view(np.float32)).cuda()).cpu().numpy()
+    for k in range(0, len(m), 997):
+        s, c = oracle.sincos_quarter32(int(m[k]))
+        assert np.float32(s) == s_gpu[k] and np.float32(c) == c_gpu[k]
+
+
+# ---------------------------------------------------------------- decode parity
+def test_decode_parity_c1_all_10k_frames(codes):
+    """BASELINE config 1: every one of the 10,000 frames at 2.0 dB."""
+    g, o = codes("C1")
+    llr, _ = o.channel(2.0, seed=1, frame_begin=0, frames=10_000)
+    oo = o.decode(llr, 20, want_omega=True)
+    assert_same(gpu_decode(g, llr, 20), oo, o.N)
+
+
+@pytest.mark.parametrize("name,ebn0,frames", [("C2", 1.0, 400), ("C2", 2.0, 1000), ("C2", 3.0, 1000),
+                                              ("C3a", 2.0, 200), ("C3a", 1.5, 100), ("C3b", 3.5, 200),
+                                              ("T24", 4.0, 2000)])
+def test_decode_parity_configs(codes, name, ebn0, frames):
+    g, o = codes(name)
+    mi = inputs.CONFIGS[name].max_iter
+    llr, _ = o.channel(ebn0, seed=3, frame_begin=0, frames=frames)
+    assert_same(gpu_decode(g, llr, mi), o.decode(llr, mi, want_omega=True), o.N)
+
+
+@pytest.mark.parametrize("rule", [oracle.STOP_BELIEF_M, oracle.STOP_BELIEF_N, oracle.STOP_SYNDROME, oracle.STOP_NONE])
+@pytest.mark.parametrize("max_iter", [1, 2, 7])
+def test_decode_parity_stop_rules(codes, rule, max_iter):
+    g, o = codes("C2")
+    llr, _ = o.channel(2.0, seed=4, frame_begin=50, frames=200)
+    assert_same(gpu_decode(g, llr, max_iter, rule), o.decode(llr, max_iter, rule, want_omega=True), o.N)
+
+
+def test_decode_parity_degree_one_and_mid_row_stops(codes):
+    """C4-like degree-1 extension rows (reading R3) and many belief fires that
+    fail verification (mid-row stop + rollback path, reading R5)."""
+    _need_gpu()
+    base = inputs.construct_base((8, 14, 8, 4, 0, 3, 3), 1)
+    g, o = cbp.Code(base, 8), oracle.OracleCode(base, 8)
+    for eb in (1.0, 3.0, 5.0):
+        llr, _ = o.channel(eb, seed=5, frame_begin=0, frames=600)
+        for rule in (0, 1, 2, 3):
+            oo = o.decode(llr, 25, rule, want_omega=True)
+            assert_same(gpu_decode(g, llr, 25, rule), oo, o.N)
+    assert oo["fires"].sum() >= 0
+
+
+def test_decode_parity_random_llrs_and_extremes(codes):
+    g, o = codes("C2")
+    rng = np.random.default_rng(7)
+    llr = inputs.random_llr(o.N, 300, 3.0, seed=7)
+    llr[0] = 0.0                                          # tie rule
+    llr[1] = 1e30                                         # huge, beyond the phi clamp
+    llr[2] = -1e-30
+    llr[3, ::2] = np.float32(-0.0)
+    llr[4] = rng.choice([-50.0, 50.0], o.N)
+    assert_same(gpu_decode(g, llr, 30), o.decode(llr, 30, want_omega=True), o.N)
+
+
+def test_decode_padding_and_empty(codes):
+    g, o = codes("C1")
+    llr, _ = o.channel(2.0, seed=2, frame_begin=0, frames=64)
+    go = gpu_decode(g, llr, 20, ld=128)                   # ld > N
+    assert_same(go, o.decode(llr, 20, want_omega=True), o.N)
+    out = g.alloc_outputs(4)
+    out["bits"] = torch.full((4, 7), -1, dtype=torch.int32, device="cuda")   # ld_words > ceil(N/32)
+    g.decode(torch.from_numpy(np.ascontiguousarray(llr[:4])).cuda(), 20, out=out)
+    b = out["bits"].cpu().numpy()
+    assert (b[:, 3:] == 0).all()
+    e = g.decode(torch.empty((0, 96), dtype=torch.float32, device="cuda"), 20)
+    assert e["iters"].numel() == 0
+
+
+def test_decode_i8_parity(codes):
+    g, o = codes("C2")
+    l8, _ = o.channel(2.5, seed=8, frame_begin=0, frames=500, llr_mode=1)
+    q = np.zeros((500, 656), np.int8)
+    q[:, :o.N] = np.rint(l8 * 4).astype(np.int8)
+    out = g.decode_i8(torch.from_numpy(q).cuda(), 0.25, 30, omega=True, ev=True)
+    torch.cuda.synchronize()
+    go = {k: v.cpu().numpy() for k, v in out.items()}
+    assert_same(go, o.decode(l8, 30, want_omega=True), o.N)
+
+
+# ---------------------------------------------------------------- channel + ber_sim
+@pytest.mark.parametrize("name,llr_mode", [("C1", 0), ("C2", 0), ("C2", 1), ("C3a", 0), ("C3b", 0)])
+def test_channel_parity(codes, name, llr_mode):
+    g, o = codes(name)
+    for fb in (0, (1 << 32) - 3):                          # frame index across the 32-bit boundary
+        l_o, cw_o = o.channel(1.5, seed=0xDEADBEEF12345678, frame_begin=fb, frames=40, llr_mode=llr_mode)
+        l_g, cw_g = g.channel(1.5, seed=0xDEADBEEF12345678, frame_begin=fb, frames=40, llr_mode=llr_mode)
+        assert (l_g[:, :o.N].cpu().numpy().view(np.uint32) == l_o.view(np.uint32)).all()
+        assert (cw_g.cpu().numpy().view(np.uint32) == cw_o).all()
+
+
+@pytest.mark.parametrize("name,ebn0,frames,llr_mode", [("C1", 2.0, 10_000, 0), ("C2", 1.5, 1500, 0),
+                                                       ("C2", 2.5, 1500, 1), ("C3a", 2.5, 200, 0),
+                                                       ("C3b", 4.0, 200, 0)])
+def test_ber_sim_parity(codes, name, ebn0, frames, llr_mode):
+    g, o = codes(name)
+    mi = inputs.CONFIGS[name].max_iter
+    want = o.ber_sim(ebn0, 21, 1000, frames, mi, llr_mode=llr_mode)
+    got = g.ber_sim(ebn0, 21, 1000, frames, mi, llr_mode=llr_mode).cpu().numpy()
+    assert list(got) == list(want), dict(zip(oracle.COUNT_NAMES, zip(got, want)))
+
+
+def test_ber_sim_full_size_sampled(codes):
+    """BASELINE config 2 at full size (10^6 frames, 2.0 dB) in the bench launch
+    configuration: counters equal channel -> decode -> compare on the GPU, shard
+    invariant, and a seeded sample of frames (plus error frames) equal the oracle."""
+    g, o = codes("C2")
+    F, seed, eb = 1_000_000, 1, 2.0
+    full = g.ber_sim(eb, seed, 0, F, 30).cpu().numpy()
+    halves = (g.ber_sim(eb, seed, 0, 400_000, 30) + g.ber_sim(eb, seed, 400_000, F - 400_000, 30)).cpu().numpy()
+    assert (full == halves).all()
+    # channel -> decode on the GPU reproduces the fused counters
+    tot = np.zeros(8, np.int64)
+    err_frames = []
+    for b in range(0, F, 250_000):
+        llr, cw = g.channel(eb, seed, b, 250_000)
+        out = g.decode(llr, 30, ev=True)
+        d = cbp.unpack_bits(out["bits"], o.N) != cbp.unpack_bits(cw, o.N)
+        info = d[:, :o.K].sum(1)
+        tot += np.array([250_000, info.sum().item(), (info > 0).sum().item(), d.any(1).sum().item(),
+                         out["iters"].sum().item(), out["ev"].sum().item(),
+                         ((out["flags"] & 1) == 0).sum().item(), 0], np.int64)
+        err_frames += (b + torch.nonzero((info > 0) | ((out["flags"] & 1) == 0)).flatten().cpu().numpy()).tolist()
+    assert (tot[:7] == full[:7]).all()
+    rng = np.random.default_rng(3)
+    sample = sorted(set(rng.integers(0, F, 150).tolist() + err_frames[:100]))
+    for fidx in sample:
+        llr_o, _ = o.channel(eb, seed, fidx, 1)
+        llr_g, _ = g.channel(eb, seed, fidx, 1)
+        assert (llr_g[:, :o.N].cpu().numpy() == llr_o).all()
+        assert_same(gpu_decode(g, llr_o, 30), o.decode(llr_o, 30, want_omega=True), o.N)
