@@ -212,12 +212,22 @@ cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t 
     const int64_t raw = 2LL * c->N + c->E + c->M + nwords;
     G.slot_words = static_cast<int32_t>(G.F > 1 ? (raw + 31) / 32 * 32 + G.Zp : (raw + 3) / 4 * 4);
     G.table_words = (4 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4;
+    G.team_threads = G.threads;
     int smem_optin = 0, nsm = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-    const int64_t full = 4LL * (G.table_words + 96 + static_cast<int64_t>(G.F) * G.slot_words);
-    G.state_in_smem = full <= smem_optin ? 1 : 0;
-    G.smem_bytes = static_cast<int32_t>(G.state_in_smem ? full : 4LL * (G.table_words + 96));
+    // teams per CTA: as many independent teams as shared memory, 512 threads and
+    // 15 named barriers allow (they share the staged tables)
+    const int64_t per_team = 4LL * (cbp::kCtlTeamWords + static_cast<int64_t>(G.F) * G.slot_words);
+    const int64_t fixed = 4LL * G.table_words;
+    int nt = static_cast<int>((smem_optin - fixed) / per_team);
+    nt = std::min(nt, std::max(1, 512 / G.team_threads));
+    if (G.multi) nt = std::min(nt, 15);
+    G.state_in_smem = nt >= 1 ? 1 : 0;
+    G.teams = std::max(nt, 1);
+    G.threads = G.teams * G.team_threads;
+    G.smem_bytes = static_cast<int32_t>(G.state_in_smem ? fixed + G.teams * per_team
+                                                        : fixed + 4LL * cbp::kCtlTeamWords * G.teams);
     c->num_sms = nsm > 0 ? nsm : 1;
     int occ = 0;
     if (cbp::occupancy_ctas_per_sm(G, &occ) != 0 || occ < 1) {
@@ -245,7 +255,7 @@ cbp_status cbp_get_launch_info(const cbp_code* c, cbp_launch_info* o)
     if (!c || !o) return fail(CBP_E_INVALID, "cbp_get_launch_info: null argument");
     o->threads = c->geo.threads;
     o->ctas_per_sm = c->ctas_per_sm;
-    o->frames_per_cta = c->geo.F;
+    o->frames_per_cta = c->geo.F * c->geo.teams;
     o->smem_bytes = c->geo.smem_bytes;
     o->state_in_smem = c->geo.state_in_smem;
     o->num_sms = c->num_sms;
@@ -265,6 +275,7 @@ cbp::KernelArgs base_args(const cbp_code* c)
     d.max_dc = c->max_dc; d.can_encode = c->can_encode; d.mid = c->mid;
     d.ent = c->d_ent; d.row_ptr = c->d_row_ptr; d.pshift = c->d_pshift;
     a.Zp = c->geo.Zp; a.F = c->geo.F; a.slot_words = c->geo.slot_words; a.table_words = c->geo.table_words;
+    a.team_threads = c->geo.team_threads;
     a.max_iter = 1; a.stop_rule = 0;
     return a;
 }
@@ -284,7 +295,8 @@ cbp_status run(const cbp_code* c, cbp::KernelArgs& a, int64_t frames, void* stre
     DeviceGuard g(c->device);
     if (!g.ok) return fail(CBP_E_CUDA, std::string(who) + ": cudaSetDevice failed");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int64_t ctas_needed = (frames + c->geo.F - 1) / c->geo.F;
+    const int64_t per_cta = static_cast<int64_t>(c->geo.F) * c->geo.teams;
+    const int64_t ctas_needed = (frames + per_cta - 1) / per_cta;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(c->num_sms) * c->ctas_per_sm, ctas_needed)));
     cudaError_t e;
     unsigned long long* q = nullptr;
@@ -292,7 +304,7 @@ cbp_status run(const cbp_code* c, cbp::KernelArgs& a, int64_t frames, void* stre
         return fail(CBP_E_NOMEM, std::string(who) + ": " + cudaGetErrorString(e));
     float* gs = nullptr;
     if (!c->geo.state_in_smem) {
-        const size_t bytes = sizeof(float) * static_cast<size_t>(grid) * c->geo.F * c->geo.slot_words;
+        const size_t bytes = sizeof(float) * static_cast<size_t>(grid) * per_cta * c->geo.slot_words;
         if ((e = cudaMallocAsync(reinterpret_cast<void**>(&gs), bytes, st)) != cudaSuccess) {
             cudaFreeAsync(q, st);
             return fail(CBP_E_NOMEM, std::string(who) + ": " + cudaGetErrorString(e));

@@ -52,12 +52,15 @@ struct KernelArgs {
     unsigned long long* counts;   // MODE_BER_SIM: 8 x int64
     unsigned long long* queue;    // frame work counter (zeroed)
     // geometry
-    int32_t Zp, F, slot_words, table_words;
+    int32_t Zp, F, slot_words, table_words, team_threads;
     float* gstate;         // per-CTA global state (state_in_smem == 0)
 };
 
+constexpr int kCtlTeamWords = 72;   // shared control words per team: 2 x 32 ballot words + broadcast
+
 struct Geometry {
     int32_t threads, F, Zp, slot_words, table_words, smem_bytes, state_in_smem, multi;
+    int32_t team_threads, teams;   // threads per team, teams per CTA
 };
 
 // launch (cbp_kernels.cu); returns cudaError_t as int

@@ -22,7 +22,6 @@
 namespace cbp {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kCtlWords = 96;
 
 struct SlotPtrs {
     float* Q;       // [N] latest V2C message Q_{v->c*}
@@ -33,29 +32,56 @@ struct SlotPtrs {
 };
 
 // ---------------------------------------------------------------- team helpers
+// A CTA holds several independent teams.  !MULTI: a team is one warp holding F
+// frame slots of Zp lanes; MULTI: a team is TW warps holding one frame.  Teams
+// synchronise with their own named barrier (id 1 + team index).
+__device__ __forceinline__ void named_bar_sync(int id, int n)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ bool named_bar_or(int id, int n, bool pred)
+{
+    unsigned out;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.u32 p, %1, 0;\n\t"
+        "bar.red.or.pred q, %2, %3, p;\n\t"
+        "selp.u32 %0, 1, 0, q;\n\t}"
+        : "=r"(out)
+        : "r"(static_cast<unsigned>(pred)), "r"(id), "r"(n)
+        : "memory");
+    return out != 0u;
+}
+
 template <bool MULTI>
 struct Team {
+    int tidx;             // team index in the CTA
+    int nthreads;         // threads per team
+    int tl;               // thread index within the team
     int slot, r, lane_base;
     bool lane_on;
     unsigned slot_mask;   // lanes of this slot within the warp (!MULTI)
 
     __device__ __forceinline__ void sync() const
     {
-        if (MULTI) __syncthreads();
+        if (MULTI) named_bar_sync(1 + tidx, nthreads);
         else __syncwarp();
     }
-    // OR of pred over the lanes of this slot (a synchronisation point)
-    __device__ __forceinline__ bool slot_any(bool pred) const
+    // OR over the team (a synchronisation point)
+    __device__ __forceinline__ bool team_any(bool pred) const
     {
-        if (MULTI) return __syncthreads_or(pred) != 0;
-        return (__ballot_sync(kFull, pred) & slot_mask) != 0u;
-    }
-    // OR over the whole CTA
-    __device__ __forceinline__ bool cta_any(bool pred) const
-    {
-        if (MULTI) return __syncthreads_or(pred) != 0;
+        if (MULTI) return named_bar_or(1 + tidx, nthreads, pred);
         return __any_sync(kFull, pred) != 0;
     }
+    // OR over the lanes of this slot (a synchronisation point)
+    __device__ __forceinline__ bool slot_any(bool pred) const
+    {
+        if (MULTI) return team_any(pred);
+        return (__ballot_sync(kFull, pred) & slot_mask) != 0u;
+    }
+    // kept for readability at call sites that mean "any slot of this team"
+    __device__ __forceinline__ bool cta_any(bool pred) const { return team_any(pred); }
 };
 
 // ---------------------------------------------------------------- per-row edge chain
@@ -310,28 +336,31 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
     for (int k = threadIdx.x; k < C.nent; k += blockDim.x) ent[k] = C.ent[k];
     for (int k = threadIdx.x; k <= mb; k += blockDim.x) row_ptr[k] = C.row_ptr[k];
     for (int k = threadIdx.x; k < mb; k += blockDim.x) pshift[k] = C.pshift[k];
-    uint32_t* ctl = smem + a.table_words;
-    long long* ctl64 = reinterpret_cast<long long*>(ctl + 64);
-
     Team<MULTI> tm;
+    tm.nthreads = a.team_threads;
+    tm.tidx = threadIdx.x / a.team_threads;
+    tm.tl = threadIdx.x - tm.tidx * a.team_threads;
     if (MULTI) {
         tm.slot = 0;
-        tm.r = threadIdx.x;
+        tm.r = tm.tl;
         tm.lane_base = 0;
         tm.slot_mask = kFull;
     } else {
-        tm.slot = threadIdx.x / a.Zp;
-        tm.r = threadIdx.x % a.Zp;
+        tm.slot = tm.tl / a.Zp;
+        tm.r = tm.tl % a.Zp;
         tm.lane_base = tm.slot * a.Zp;
         tm.slot_mask = (a.Zp == 32) ? kFull : (((1u << a.Zp) - 1u) << tm.lane_base);
     }
     tm.lane_on = tm.r < Z && tm.slot < a.F;
     const int r = tm.r;
+    uint32_t* ctl = smem + a.table_words + tm.tidx * kCtlTeamWords;
+    long long* ctl64 = reinterpret_cast<long long*>(ctl + 64);
 
-    float* sbase = SMEM ? reinterpret_cast<float*>(ctl + kCtlWords)
-                        : a.gstate + static_cast<size_t>(blockIdx.x) * a.F * a.slot_words;
+    const int nteams = blockDim.x / a.team_threads;
+    float* sbase = SMEM ? reinterpret_cast<float*>(smem + a.table_words + nteams * kCtlTeamWords)
+                        : a.gstate + static_cast<size_t>(blockIdx.x) * nteams * a.F * a.slot_words;
     SlotPtrs s;
-    s.Q = sbase + static_cast<size_t>(tm.slot < a.F ? tm.slot : 0) * a.slot_words;
+    s.Q = sbase + static_cast<size_t>(tm.tidx * a.F + (tm.slot < a.F ? tm.slot : 0)) * a.slot_words;
     s.P = s.Q + C.N;
     s.R = s.P + C.N;
     s.S = s.R + C.E;
@@ -355,10 +384,10 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
         long long f = -1;
         if (need && r == 0) f = static_cast<long long>(atomicAdd(a.queue, 1ull));
         if (MULTI) {
-            if (threadIdx.x == 0) ctl64[0] = f;
-            __syncthreads();
+            if (tm.tl == 0) ctl64[0] = f;
+            tm.sync();
             f = ctl64[0];
-            __syncthreads();
+            tm.sync();
         } else {
             f = __shfl_sync(kFull, f, tm.lane_base);
         }
@@ -413,10 +442,10 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
                 if (MULTI) {
                     const int buf = (i & 1) * 32;
                     const unsigned m = __ballot_sync(kFull, tm.lane_on && !ro.ok);
-                    if ((threadIdx.x & 31) == 0) ctl[buf + (threadIdx.x >> 5)] = m;
-                    __syncthreads();
+                    if ((tm.tl & 31) == 0) ctl[buf + (tm.tl >> 5)] = m;
+                    tm.sync();
                     if (belief) {
-                        const int nw = blockDim.x >> 5;
+                        const int nw = tm.nthreads >> 5;
                         for (int w = 0; w < nw; ++w) {
                             const unsigned mw = ctl[buf + w];
                             if (mw) {
@@ -625,16 +654,16 @@ static int occ_t(const Geometry& g, int* out)
 int launch_cbp(const KernelArgs& a, const Geometry& g, int grid, void* stream)
 {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (!g.multi) return g.state_in_smem ? launch_t<false, true, 32>(a, g, grid, st) : launch_t<false, false, 32>(a, g, grid, st);
-    if (g.threads <= 384)
-        return g.state_in_smem ? launch_t<true, true, 384>(a, g, grid, st) : launch_t<true, false, 384>(a, g, grid, st);
+    if (!g.multi) return g.state_in_smem ? launch_t<false, true, 512>(a, g, grid, st) : launch_t<false, false, 512>(a, g, grid, st);
+    if (g.threads <= 512)
+        return g.state_in_smem ? launch_t<true, true, 512>(a, g, grid, st) : launch_t<true, false, 512>(a, g, grid, st);
     return g.state_in_smem ? launch_t<true, true, 1024>(a, g, grid, st) : launch_t<true, false, 1024>(a, g, grid, st);
 }
 
 int occupancy_ctas_per_sm(const Geometry& g, int* out)
 {
-    if (!g.multi) return g.state_in_smem ? occ_t<false, true, 32>(g, out) : occ_t<false, false, 32>(g, out);
-    if (g.threads <= 384) return g.state_in_smem ? occ_t<true, true, 384>(g, out) : occ_t<true, false, 384>(g, out);
+    if (!g.multi) return g.state_in_smem ? occ_t<false, true, 512>(g, out) : occ_t<false, false, 512>(g, out);
+    if (g.threads <= 512) return g.state_in_smem ? occ_t<true, true, 512>(g, out) : occ_t<true, false, 512>(g, out);
     return g.state_in_smem ? occ_t<true, true, 1024>(g, out) : occ_t<true, false, 1024>(g, out);
 }
 

@@ -81,10 +81,15 @@ __device__ __forceinline__ float phi_large(float x)
 }
 
 // phi(x) = -log(tanh(x/2)) (equ_s2e5) with input/output clamp
+// Both regimes are evaluated and selected (no divergent branch), so the U
+// independent phi chains of an edge chunk interleave in straight-line code.
+// phi_large is evaluated on max(x, 1) to stay inside its reduction range.
 __device__ __forceinline__ float phi32(float x)
 {
     x = fminf(fmaxf(x, kPhiLo), kPhiHi);
-    const float r = (x < 1.0f) ? phi_small(x) : phi_large(x);
+    const float a = phi_small(x);
+    const float b = phi_large(fmaxf(x, 1.0f));
+    const float r = (x < 1.0f) ? a : b;
     return fminf(fmaxf(r, kPhiLo), kPhiHi);
 }
 
