@@ -54,6 +54,8 @@ def _lib():
             "oracle_ln32": ([_f32], _f32),
             "oracle_sincos_quarter32": ([ctypes.c_uint32, _p, _p], None),
             "oracle_phi32_n": ([_p, _p, _i64], None),
+            "oracle_phi32_v1": ([_f32], _f32),
+            "oracle_phi32_table": ([_p], None),
             "oracle_ln32_n": ([_p, _p, _i64], None),
         }
         for name, (args, res) in sig.items():
@@ -202,6 +204,16 @@ def ln32_array(x: np.ndarray) -> np.ndarray:
     y = np.empty_like(x)
     _lib().oracle_ln32_n(_ptr(x), _ptr(y), x.size)
     return y
+
+
+def phi32_v1(x: float) -> float:
+    return float(_lib().oracle_phi32_v1(x))
+
+
+def phi32_table() -> np.ndarray:
+    t = np.zeros((929, 4), np.float32)
+    _lib().oracle_phi32_table(_ptr(t))
+    return t
 
 
 def ln32(x: float) -> float:

@@ -93,6 +93,8 @@ int oracle_ml_decode(const or_code* c, const float* llr, uint32_t* cw);
 
 /* contract functions re-exported for the pin tests */
 float oracle_phi32(float x);
+float oracle_phi32_v1(float x);
+void  oracle_phi32_table(float* out);    /* 929 x 4 floats */
 float oracle_ln32(float x);
 void  oracle_sincos_quarter32(uint32_t m24, float* s, float* c);
 /* element-wise over arrays (pin tests) */

@@ -48,17 +48,15 @@ float oracle_ln32(float x)
 }
 
 /*
- * phi(x) = -log(tanh(x/2))  (equ_s2e5), clamped in and out to
- * [PHI_LO, PHI_HI] (reading R9).
+ * Reference formula phi_v1(x) = -log(tanh(x/2))  (equ_s2e5),
+ * unclamped, for x in [2^-43, 31] ("v1"):
  *   regime A, x < 1 :  phi = x^2 G(x^2) - ln(x/2)
  *                      (G(y) = ln((sqrt(y)/2) coth(sqrt(y)/2)) / y)
  *   regime B, x >= 1:  t = e^{-x} = 2^{-n} e^{-r};  phi = 2 t H(t^2)
  *                      (H(w) = atanh(sqrt(w)) / sqrt(w))
  */
-float oracle_phi32(float x)
+static float phi_v1_unclamped(float x)
 {
-    x = fmaxf(x, OR_PHI_LO);
-    x = fminf(x, OR_PHI_HI);
     float r;
     if (x < PHI_XA) {
         const float h = 0.5f * x;
@@ -94,9 +92,105 @@ float oracle_phi32(float x)
         const float u = t * hh;
         r = u + u;
     }
+    return r;
+}
+
+/* v1 with the input/output clamp of reading R9 (kept for the pins) */
+float oracle_phi32_v1(float x)
+{
+    x = fmaxf(x, OR_PHI_LO);
+    x = fminf(x, OR_PHI_HI);
+    float r = phi_v1_unclamped(x);
     r = fmaxf(r, OR_PHI_LO);
     r = fminf(r, OR_PHI_HI);
     return r;
+}
+
+/*
+ * phi contract v2: piecewise cubic in a local variable u in [0,1)
+ * over 929 segments --
+ *   seg 0..703   x < 2:  16 segments per binade 2^e, e = -43..0:
+ *                        seg = (bits(x) >> 19) - 1344,  u = 19 low mantissa bits / 2^19,
+ *                        x(u) = 2^e (1 + (j + u)/16), j = seg % 16
+ *   seg 704..928 x >= 2: t = fmaf(x, 8, -16), i = (int)t, u = t - i, seg = 704 + i,
+ *                        x(u) = 2 + (i + u)/8
+ * Coefficients: cubic interpolation of phi_v1 at u = 0, 1/4, 3/4, 1 (exact floats
+ * x(u)), Newton divided differences in IEEE double in the order written below,
+ * each coefficient rounded to binary32.
+ */
+#define OR_PHI_SEGS 929
+static float phi_tab[OR_PHI_SEGS][4];
+static int phi_tab_ready;
+
+static void phi_segment(float f0, float f1, float f2, float f3, float* c)
+{
+    const double F0 = f0, F1 = f1, F2 = f2, F3 = f3;
+    const double d01 = (F1 - F0) * 4.0;
+    const double d12 = (F2 - F1) * 2.0;
+    const double d23 = (F3 - F2) * 4.0;
+    const double d012 = ((d12 - d01) * 4.0) / 3.0;
+    const double d123 = ((d23 - d12) * 4.0) / 3.0;
+    const double d0123 = d123 - d012;
+    const double t1 = d012 * 0.25;
+    const double t2 = d01 - t1;
+    const double t3 = d0123 * 0.1875;
+    c[0] = (float)F0;
+    c[1] = (float)(t2 + t3);
+    c[2] = (float)(d012 - d0123);
+    c[3] = (float)d0123;
+}
+
+static void phi_build_table(void)
+{
+    static const int Q4[4] = {0, 1, 3, 4};                 /* u = Q4/4 */
+    for (int seg = 0; seg < OR_PHI_SEGS; ++seg) {
+        float f[4];
+        for (int k = 0; k < 4; ++k) {
+            float x;
+            if (seg < 704) {
+                const int e = -43 + seg / 16, j = seg % 16;
+                x = ldexpf((float)(64 + 4 * j + Q4[k]), e - 6);     /* 2^e (1 + (j + u)/16), exact */
+            } else {
+                const int i = seg - 704;
+                x = (float)(64 + 4 * i + Q4[k]) * 0.03125f;         /* 2 + (i + u)/8, exact */
+            }
+            f[k] = phi_v1_unclamped(x);
+        }
+        phi_segment(f[0], f[1], f[2], f[3], phi_tab[seg]);
+    }
+    phi_tab_ready = 1;
+}
+
+void oracle_phi32_table(float* out)
+{
+    if (!phi_tab_ready) phi_build_table();
+    memcpy(out, phi_tab, sizeof(phi_tab));
+}
+
+float oracle_phi32(float x)
+{
+    if (!phi_tab_ready) phi_build_table();
+    x = fmaxf(x, OR_PHI_LO);
+    x = fminf(x, OR_PHI_HI);
+    int seg;
+    float u;
+    if (x < 2.0f) {
+        const uint32_t b = bits_of(x);
+        seg = (int)(b >> 19) - 1344;
+        u = f_from_bits(((b & 0x7ffffu) << 4) | 0x3f800000u) - 1.0f;   /* exact */
+    } else {
+        const float t = fmaf(x, 8.0f, -16.0f);                     /* exact */
+        const int i = (int)t;
+        u = t - (float)i;                                          /* exact */
+        seg = 704 + i;
+    }
+    const float* c = phi_tab[seg];
+    float p = fmaf(c[3], u, c[2]);
+    p = fmaf(p, u, c[1]);
+    p = fmaf(p, u, c[0]);
+    p = fmaxf(p, OR_PHI_LO);
+    p = fminf(p, OR_PHI_HI);
+    return p;
 }
 
 /*
