@@ -153,9 +153,14 @@ cbp_status cbp_get_launch_info(const cbp_code* code, cbp_launch_info* out);
 
 /* Element-wise evaluation of the fp32 arithmetic contract on the device
  * for the bit-equality pins: fn 0 phi32(x), 1 ln32(x),
- * 2 / 3 sin / cos(2 pi m 2^-24) with m = the low 24 bits of x's bit pattern.
+ * 2 / 3 sin / cos(2 pi m 2^-24) with m = the low 24 bits of x's bit pattern,
+ * 4 the clamped reference formula phi_v1(x) the v2 table interpolates.
  * d_x, d_y: device float[n] on `device`. */
 cbp_status cbp_eval_contract(int32_t fn, const float* d_x, float* d_y, int64_t n, int32_t device, void* stream);
+
+/* Copy the phi contract v2 table of `device` (929 segments x {c0, c1, c2, c3},
+ * DESIGN.md §3, built on the device at first use) into d_out (device float[3716]). */
+cbp_status cbp_phi_table(int32_t device, float* d_out, void* stream);
 
 #ifdef __cplusplus
 }

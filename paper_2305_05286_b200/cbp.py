@@ -54,6 +54,7 @@ SIGNATURES = {
     "cbp_ber_sim": ([_p, _f64, _u64, _i64, _i64, _p, _i32, _p, _p], _i32),
     "cbp_get_launch_info": ([_p, _p], _i32),
     "cbp_eval_contract": ([_i32, _p, _p, _i64, _i32, _p], _i32),
+    "cbp_phi_table": ([_i32, _p, _p], _i32),
 }
 
 
@@ -213,6 +214,13 @@ def eval_contract(fn: int, x: torch.Tensor, stream=None) -> torch.Tensor:
     _check(lib().cbp_eval_contract(fn, _dptr(x, torch.float32, x.device, "x"), y.data_ptr(), x.numel(),
                                    x.device.index, _stream(stream)), "cbp_eval_contract")
     return y
+
+
+def phi_table(device: int = 0, stream=None) -> torch.Tensor:
+    """cbp_phi_table: the device's phi contract v2 table, float32 [929, 4] (on the device)."""
+    out = torch.empty((929, 4), dtype=torch.float32, device=torch.device("cuda", device))
+    _check(lib().cbp_phi_table(device, out.data_ptr(), _stream(stream)), "cbp_phi_table")
+    return out
 
 
 def unpack_bits(words: torch.Tensor, n: int) -> torch.Tensor:

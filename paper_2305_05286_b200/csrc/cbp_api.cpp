@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "cbp.h"
@@ -43,6 +44,32 @@ struct DeviceGuard {
     }
 };
 
+// phi contract v2 table, built once per device by phi_table_kernel
+std::mutex g_tab_mu;
+float4* g_tab[128] = {};
+
+const float4* phi_table(int device, std::string* err)
+{
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    if (device < 0 || device >= 128) { *err = "device index out of range"; return nullptr; }
+    if (g_tab[device]) return g_tab[device];
+    DeviceGuard g(device);
+    float4* p = nullptr;
+    cudaStream_t st = nullptr;
+    cudaError_t e = cudaMalloc(&p, sizeof(float4) * cbp::kPhiTableSegs);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = static_cast<cudaError_t>(cbp::launch_phi_table(p, st));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (st) cudaStreamDestroy(st);
+    if (e != cudaSuccess) {
+        if (p) cudaFree(p);
+        *err = std::string("phi table: ") + cudaGetErrorString(e);
+        return nullptr;
+    }
+    g_tab[device] = p;
+    return p;
+}
+
 }  // namespace
 
 struct cbp_code {
@@ -53,6 +80,7 @@ struct cbp_code {
     int4* d_ent = nullptr;
     int32_t* d_row_ptr = nullptr;
     int16_t* d_pshift = nullptr;
+    const float4* phi_tab = nullptr;   // per-device table, not owned
     cbp::Geometry geo{};
     int ctas_per_sm = 1, num_sms = 1;
 };
@@ -124,7 +152,9 @@ cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t 
         row_ptr[i + 1] = static_cast<int>(ent_row.size());
     }
     const int nent = static_cast<int>(ent_row.size());
-    std::vector<int4> ent(nent);
+    // two int4 per entry b (layout documented in cbp_kernels.cu):
+    //   A = {8 jZ, 4 row(p) Z, 4 bZ, 4 pZ},  B = {8 s, 4 ds, first, jZ}
+    std::vector<int4> ent(2 * static_cast<size_t>(nent));
     for (int j = 0; j < nb; ++j) {
         const auto& L = col_ent[j];
         for (size_t k = 0; k < L.size(); ++k) {
@@ -132,11 +162,8 @@ cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t 
             const int p = L[(k + L.size() - 1) % L.size()];       // previous nonzero row of column j, cyclic
             const int ds = ((ent_s[b] - ent_s[p]) % Z + Z) % Z;
             const int first = (k == 0) ? 1 : 0;                   // R1: no latest check before this visit
-            const int self = (p == b) ? 1 : 0;                    // R3: degree-1 column
-            ent[b].x = (j * Z) | ((ent_row[p] * Z) << 16);
-            ent[b].y = ent_s[b] | (ds << 11) | (first << 22) | (self << 23);
-            ent[b].z = b * Z;
-            ent[b].w = p * Z;
+            ent[2 * b] = make_int4(8 * j * Z, 4 * ent_row[p] * Z, 4 * b * Z, 4 * p * Z);
+            ent[2 * b + 1] = make_int4(8 * ent_s[b], 4 * ds, first, j * Z);
         }
     }
 
@@ -183,14 +210,19 @@ cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t 
 
     DeviceGuard g(device);
     if (!g.ok) { delete c; return fail(CBP_E_CUDA, "cbp_code_create: cudaSetDevice failed"); }
+    {
+        std::string terr;
+        c->phi_tab = phi_table(device, &terr);
+        if (!c->phi_tab) { delete c; return fail(CBP_E_CUDA, "cbp_code_create: " + terr); }
+    }
     cudaError_t e;
-    if ((e = cudaMalloc(&c->d_ent, sizeof(int4) * nent)) != cudaSuccess ||
+    if ((e = cudaMalloc(&c->d_ent, sizeof(int4) * 2 * nent)) != cudaSuccess ||
         (e = cudaMalloc(&c->d_row_ptr, sizeof(int32_t) * (mb + 1))) != cudaSuccess ||
         (e = cudaMalloc(&c->d_pshift, sizeof(int16_t) * mb)) != cudaSuccess) {
         cbp_code_destroy(c);
         return fail(CBP_E_NOMEM, std::string("cbp_code_create: ") + cudaGetErrorString(e));
     }
-    if ((e = cudaMemcpy(c->d_ent, ent.data(), sizeof(int4) * nent, cudaMemcpyHostToDevice)) != cudaSuccess ||
+    if ((e = cudaMemcpy(c->d_ent, ent.data(), sizeof(int4) * 2 * nent, cudaMemcpyHostToDevice)) != cudaSuccess ||
         (e = cudaMemcpy(c->d_row_ptr, row_ptr.data(), sizeof(int32_t) * (mb + 1), cudaMemcpyHostToDevice)) != cudaSuccess ||
         (e = cudaMemcpy(c->d_pshift, pshift.data(), sizeof(int16_t) * mb, cudaMemcpyHostToDevice)) != cudaSuccess) {
         cbp_code_destroy(c);
@@ -211,7 +243,7 @@ cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t 
     }
     const int64_t raw = 2LL * c->N + c->E + c->M + nwords;
     G.slot_words = static_cast<int32_t>(G.F > 1 ? (raw + 31) / 32 * 32 + G.Zp : (raw + 3) / 4 * 4);
-    G.table_words = (4 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4;
+    G.table_words = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4;
     G.team_threads = G.threads;
     int smem_optin = 0, nsm = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
@@ -273,7 +305,7 @@ cbp::KernelArgs base_args(const cbp_code* c)
     d.N = c->N; d.K = c->K; d.M = c->M; d.Z = c->Z; d.mb = c->mb; d.nb = c->nb; d.kb = c->kb; d.core = c->core;
     d.nent = c->nent; d.E = static_cast<int32_t>(c->E); d.nwords = (c->N + 31) / 32; d.kwords = (c->K + 31) / 32;
     d.max_dc = c->max_dc; d.can_encode = c->can_encode; d.mid = c->mid;
-    d.ent = c->d_ent; d.row_ptr = c->d_row_ptr; d.pshift = c->d_pshift;
+    d.ent = c->d_ent; d.row_ptr = c->d_row_ptr; d.pshift = c->d_pshift; d.phi_tab = c->phi_tab;
     a.Zp = c->geo.Zp; a.F = c->geo.F; a.slot_words = c->geo.slot_words; a.table_words = c->geo.table_words;
     a.team_threads = c->geo.team_threads;
     a.max_iter = 1; a.stop_rule = 0;
@@ -436,12 +468,28 @@ cbp_status cbp_ber_sim(const cbp_code* c, double ebn0_db, uint64_t seed, int64_t
 
 cbp_status cbp_eval_contract(int32_t fn, const float* d_x, float* d_y, int64_t n, int32_t device, void* stream)
 {
-    if (fn < 0 || fn > 3) return fail(CBP_E_INVALID, "cbp_eval_contract: fn must be 0..3");
+    if (fn < 0 || fn > 4) return fail(CBP_E_INVALID, "cbp_eval_contract: fn must be 0..4");
     if (n < 0 || (n > 0 && (!d_x || !d_y))) return fail(CBP_E_INVALID, "cbp_eval_contract: bad buffers");
     DeviceGuard g(device);
     if (!g.ok) return fail(CBP_E_CUDA, "cbp_eval_contract: cudaSetDevice failed");
-    const int e = cbp::launch_contract_eval(fn, d_x, d_y, n, stream);
+    std::string terr;
+    const float4* tab = phi_table(device, &terr);
+    if (!tab) return fail(CBP_E_CUDA, "cbp_eval_contract: " + terr);
+    const int e = cbp::launch_contract_eval(fn, d_x, d_y, n, tab, stream);
     if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cbp_eval_contract");
+    return CBP_OK;
+}
+
+cbp_status cbp_phi_table(int32_t device, float* d_out, void* stream)
+{
+    if (!d_out) return fail(CBP_E_INVALID, "cbp_phi_table: null output");
+    std::string terr;
+    const float4* tab = phi_table(device, &terr);
+    if (!tab) return fail(CBP_E_CUDA, "cbp_phi_table: " + terr);
+    DeviceGuard g(device);
+    const cudaError_t e = cudaMemcpyAsync(d_out, tab, sizeof(float4) * cbp::kPhiTableSegs, cudaMemcpyDeviceToDevice,
+                                          static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "cbp_phi_table");
     return CBP_OK;
 }
 

@@ -22,6 +22,7 @@ struct DevCode {
     const int4* ent;       // [nent]
     const int32_t* row_ptr;// [mb+1]
     const int16_t* pshift; // [mb]: shift of column kb in row i (-1 if none)
+    const float4* phi_tab; // [929] phi contract v2 coefficients
 };
 
 enum Mode : int32_t { MODE_DECODE_F32 = 0, MODE_DECODE_I8 = 1, MODE_BER_SIM = 2, MODE_CHANNEL = 3 };
@@ -66,6 +67,8 @@ struct Geometry {
 // launch (cbp_kernels.cu); returns cudaError_t as int
 int launch_cbp(const KernelArgs& a, const Geometry& g, int grid, void* stream);
 int occupancy_ctas_per_sm(const Geometry& g, int* out);
-int launch_contract_eval(int fn, const float* x, float* y, int64_t n, void* stream);
+int launch_contract_eval(int fn, const float* x, float* y, int64_t n, const float4* tab, void* stream);
+int launch_phi_table(float4* out, void* stream);
+constexpr int kPhiTableSegs = 929;
 
 }  // namespace cbp

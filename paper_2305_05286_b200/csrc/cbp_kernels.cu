@@ -1,13 +1,14 @@
 // cbp_kernels.cu -- sm_100a kernels of check-belief propagation decoding.
 //
 // One persistent kernel serves cbp_decode, cbp_decode_i8, cbp_channel and
-// cbp_ber_sim.  Mapping: a CTA is a "team" of F frame slots;
-// each slot owns Z lanes, lane r processes lifted check i*Z + r of the current
-// base row i.  The Z lifted checks of one base row touch disjoint variables
-// (each block is a permutation), so processing them in parallel is bit-identical
-// to the paper's sequential check order (reading R12).  Per-frame state
-// (Q, Phi|hard bit, R, S|sign of Omega) lives in shared memory; the code's
-// schedule tables are staged once per CTA.
+// cbp_ber_sim.  A CTA holds several independent teams; a team
+// owns F frame slots of Zp lanes, and lane r of a slot processes lifted check
+// i*Z + r of the current base row i.  The Z lifted checks of one base row touch
+// disjoint variables (each block is a permutation), so processing them in
+// parallel is bit-identical to the paper's sequential check order (reading
+// R12).  Per-frame state lives in shared memory:
+//   QP[N] float2 (Q_v, Phi_v | hard bit in the sign), R[E], S[M] (sign = Omega<0)
+// The phi table (contract v2) and the code's schedule tables are staged once per CTA.
 //
 // Paper steps (§IV-C): init = Step 1 (l.402-422, equ_s4e15-17);
 // process_row = Step 2(1) B2V/V2C/C2B (equ_s4e18-22) and 2(2) (equ_s4e23);
@@ -22,19 +23,43 @@
 namespace cbp {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr uint32_t kSign = 0x80000000u;
 
+// Per-slot state.  Byte-addressed bases plus typed views for the cold paths.
 struct SlotPtrs {
-    float* Q;       // [N] latest V2C message Q_{v->c*}
-    float* P;       // [N] Phi_v = phi(|Q_v|) with the sign bit = hard decision x_v
-    float* R;       // [E] C2V messages, slot b*Z + r = edge of (check i*Z+r, entry b)
-    float* S;       // [M] phi-domain check-belief sum, sign bit = (Omega_c < 0)
+    char* qp;       // float2 [N]: (Q_{v->c*}, Phi_v = phi(|Q_v|) with sign bit = hard decision x_v)
+    char* R;        // float [E]: C2V message of edge (check i*Z+r, entry b) at byte 4*(b*Z + r)
+    char* S;        // float [M]: phi-domain check-belief sum S_c, sign bit = (Omega_c < 0)
     uint32_t* cw;   // [nwords] transmitted codeword (ber_sim) / scratch
+    __device__ __forceinline__ float2* QP() const { return reinterpret_cast<float2*>(qp); }
+    __device__ __forceinline__ float* Rf() const { return reinterpret_cast<float*>(R); }
+    __device__ __forceinline__ float* Sf() const { return reinterpret_cast<float*>(S); }
 };
 
+__device__ __forceinline__ float2 ld2(const char* b, int off) { return *reinterpret_cast<const float2*>(b + off); }
+__device__ __forceinline__ float ld1(const char* b, int off) { return *reinterpret_cast<const float*>(b + off); }
+__device__ __forceinline__ void st2(char* b, int off, float2 v) { *reinterpret_cast<float2*>(b + off) = v; }
+__device__ __forceinline__ void st1(char* b, int off, float v) { *reinterpret_cast<float*>(b + off) = v; }
+
+// Schedule table entry b (two int4, built in cbp_api.cpp):
+//   A = {8 j Z, 4 row(prev(b)) Z, 4 b Z, 4 prev(b) Z}    byte bases: variable block (QP),
+//        S block of the previous check of the same variables, own R block, R block of prev(b)
+//   B = {8 s, 4 ds, first, j Z}   ds = (s - s_prev) mod Z; first: no latest check in sweep 1 (R1)
+// prev(b) = previous nonzero row of b's column, cyclically (the static "latest check" of
+// every variable of the block after sweep 1); prev(b) == b for a degree-1
+// column (R3).  Variable of lane r: j Z + (r + s) mod Z; its previous check's row (r + ds) mod Z.
+
+__device__ __forceinline__ int lane_var(const int4* ent, int e, int r, int Z)
+{
+    const int4 B = ent[2 * e + 1];
+    int t = r + (B.x >> 3);
+    t = (t >= Z) ? t - Z : t;
+    return B.w + t;
+}
+
 // ---------------------------------------------------------------- team helpers
-// A CTA holds several independent teams.  !MULTI: a team is one warp holding F
-// frame slots of Zp lanes; MULTI: a team is TW warps holding one frame.  Teams
-// synchronise with their own named barrier (id 1 + team index).
+// !MULTI: a team is one warp holding F frame slots of Zp lanes; MULTI: a team is
+// TW warps holding one frame.  Teams synchronise with their own named barrier.
 __device__ __forceinline__ void named_bar_sync(int id, int n)
 {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -80,127 +105,127 @@ struct Team {
         if (MULTI) return team_any(pred);
         return (__ballot_sync(kFull, pred) & slot_mask) != 0u;
     }
-    // kept for readability at call sites that mean "any slot of this team"
-    __device__ __forceinline__ bool cta_any(bool pred) const { return team_any(pred); }
 };
 
 // ---------------------------------------------------------------- per-row edge chain
-struct RowOut {
-    float Snew, Sold;
-    uint32_t oldbits, newbits;
-    bool ok;
+struct Lane {
+    int r, r4, r8, Z, Z4, Z8;
 };
 
-// U consecutive edges of lane r's check (entries e0+k0 .. e0+k0+U-1, U <= remaining).
-// Loads first, then U independent B2V phi chains, commits/V2C, U independent C2B
-// phi chains, and the ordered S accumulation (reading R12).
-template <int U>
-__device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, int e0, int k0, int r, int Z, bool sweep1,
-                                           const SlotPtrs& s, float& Ssum, uint32_t& negf, uint32_t& flip,
-                                           uint32_t& oldbits, uint32_t& newbits)
+struct RowAcc {
+    float Ssum;
+    uint32_t negw;     // bit 31: XOR of the signs of Q^new over the check (sign of Omega)
+    uint32_t flipw;    // bit 31: some posterior sign flipped (equ_s4e24)
+    uint32_t oldbits;  // previous hard bits of the check's variables (rollback of a mid-row stop)
+};
+
+// U consecutive edges of lane r's check.  Loads first, then U independent B2V
+// phi chains, commits / V2C, U independent C2B phi chains and the ordered S
+// accumulation (reading R12).  SWEEP1 handles first visits (reading R1).
+template <int U, bool SWEEP1>
+__device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int k0,
+                                           const Lane& L, const SlotPtrs& s, RowAcc& acc)
 {
-    int v[U], wsl[U];
+    int aqp[U], aw[U], ar[U];
     float q[U], p[U], scj[U], rold[U], Rn[U];
-    bool fst[U], slf[U];
+    bool fst[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const int4 e = ent[e0 + k0 + u];
-        const int vb = e.x & 0xffff, psb = static_cast<int>(static_cast<uint32_t>(e.x) >> 16);
-        const int sh = e.y & 0x7ff, ds = (e.y >> 11) & 0x7ff;
-        fst[u] = sweep1 && ((e.y >> 22) & 1);
-        slf[u] = (e.y >> 23) & 1;
-        int t = r + sh;
-        t = (t >= Z) ? t - Z : t;
-        int rp = r + ds;
-        rp = (rp >= Z) ? rp - Z : rp;
-        v[u] = vb + t;
-        wsl[u] = e.w + rp;
-        q[u] = s.Q[v[u]];
-        p[u] = s.P[v[u]];
-        scj[u] = s.S[psb + rp];
-        rold[u] = s.R[e.z + r];
+        const int4 A = ent[2 * (e0 + k0 + u)];
+        const int4 B = ent[2 * (e0 + k0 + u) + 1];
+        int t8 = L.r8 + B.x;
+        t8 = (t8 >= L.Z8) ? t8 - L.Z8 : t8;
+        int rp4 = L.r4 + B.y;
+        rp4 = (rp4 >= L.Z4) ? rp4 - L.Z4 : rp4;
+        aqp[u] = A.x + t8;
+        aw[u] = A.w + rp4;
+        ar[u] = A.z + L.r4;
+        fst[u] = SWEEP1 && B.z != 0;
+        const float2 qp = ld2(s.qp, aqp[u]);
+        q[u] = qp.x;
+        p[u] = qp.y;
+        scj[u] = ld1(s.S, A.y + rp4);
+        rold[u] = ld1(s.R, ar[u]);
     }
     // B2V (equ_s4e18): R^new_{cj->v} = sgn(Omega_cj) sgn(Q) phi(|phi(|Omega_cj|) - phi(|Q|)|), phi(|Omega|) = S (R11)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const float D = fabsf(__fsub_rn(fabsf(scj[u]), fabsf(p[u])));
-        const float mag = phi32(D);
-        const bool sg = ((__float_as_uint(scj[u]) >> 31) != 0u) != (q[u] < 0.0f);
-        Rn[u] = fst[u] ? 0.0f : (sg ? -mag : mag);
+        const float mag = phi32(fabsf(__fsub_rn(fabsf(scj[u]), fabsf(p[u]))), ptab);
+        const uint32_t sg = (__float_as_uint(scj[u]) ^ __float_as_uint(q[u])) & kSign;
+        Rn[u] = __uint_as_float(__float_as_uint(mag) | sg);
+        if (SWEEP1 && fst[u]) Rn[u] = 0.0f;
     }
     float qn[U];
-    uint32_t bit[U];
+    uint32_t lb[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        if (!fst[u]) s.R[wsl[u]] = Rn[u];                 // equ_s4e22 commit of R_{cj->v} (R2), before the read (R3)
-        const float ro = slf[u] ? Rn[u] : rold[u];
-        const float lam = __fadd_rn(q[u], Rn[u]);         // equ_s4e20
-        qn[u] = __fsub_rn(lam, ro);                       // equ_s4e19 (R15)
-        bit[u] = lam < 0.0f ? 1u : 0u;                    // equ_s2e7
-        const uint32_t ob = __float_as_uint(p[u]) >> 31;
-        flip |= bit[u] ^ ob;                              // equ_s4e24 (R7)
-        oldbits |= ob << (k0 + u);
-        newbits |= bit[u] << (k0 + u);
+        if (!(SWEEP1 && fst[u])) st1(s.R, aw[u], Rn[u]);   // equ_s4e22 commit of R_{cj->v} (R2), before the read (R3)
+        const float ro = (aw[u] == ar[u]) ? Rn[u] : rold[u];
+        const float lam = __fadd_rn(q[u], Rn[u]);            // equ_s4e20 (Lambda is never -0)
+        qn[u] = __fsub_rn(lam, ro);                          // equ_s4e19 (R15)
+        lb[u] = __float_as_uint(lam) & kSign;                // hard decision, equ_s2e7
+        acc.flipw |= __float_as_uint(lam) ^ __float_as_uint(p[u]);   // equ_s4e24 (R7), bit 31
+        acc.oldbits |= (__float_as_uint(p[u]) >> 31) << (k0 + u);
     }
     float ph[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) ph[u] = phi32(fabsf(qn[u]));   // C2B (equ_s4e21, App. equ_ae4)
+    for (int u = 0; u < U; ++u) ph[u] = phi32(fabsf(qn[u]), ptab);   // C2B (equ_s4e21, App. equ_ae4)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        Ssum = __fadd_rn(Ssum, ph[u]);
-        negf ^= qn[u] < 0.0f ? 1u : 0u;
-        s.Q[v[u]] = qn[u];
-        s.P[v[u]] = bit[u] ? -ph[u] : ph[u];
+        acc.Ssum = __fadd_rn(acc.Ssum, ph[u]);
+        acc.negw ^= __float_as_uint(qn[u]);                  // Q^new is never -0
+        st2(s.qp, aqp[u], make_float2(qn[u], __uint_as_float(__float_as_uint(ph[u]) | lb[u])));
     }
 }
 
-__device__ __forceinline__ RowOut process_row(const int4* __restrict__ ent, int e0, int dc, int r, int Z, int sidx,
-                                              bool sweep1, const SlotPtrs& s)
+struct RowOut {
+    float Snew, Sold;
+    uint32_t oldbits;
+    bool ok;
+};
+
+template <bool SWEEP1>
+__device__ __forceinline__ RowOut process_row(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
+                                              int dc, int sidx4, const Lane& L, const SlotPtrs& s)
 {
-    float Ssum = 0.0f;
-    uint32_t negf = 0, flip = 0, oldbits = 0, newbits = 0;
-    const float Sold = s.S[sidx];
+    RowAcc acc{0.0f, 0u, 0u, 0u};
+    const float Sold = ld1(s.S, sidx4);
     int k0 = 0;
-    for (; k0 + 4 <= dc; k0 += 4) edge_chunk<4>(ent, e0, k0, r, Z, sweep1, s, Ssum, negf, flip, oldbits, newbits);
-    for (; k0 < dc; ++k0) edge_chunk<1>(ent, e0, k0, r, Z, sweep1, s, Ssum, negf, flip, oldbits, newbits);
-    const float Snew = negf ? -Ssum : Ssum;
-    s.S[sidx] = Snew;                                     // equ_s4e23
+    for (; k0 + 4 <= dc; k0 += 4) edge_chunk<4, SWEEP1>(ent, ptab, e0, k0, L, s, acc);
+    for (; k0 < dc; ++k0) edge_chunk<1, SWEEP1>(ent, ptab, e0, k0, L, s, acc);
+    const float Snew = __uint_as_float(__float_as_uint(acc.Ssum) | (acc.negw & kSign));
+    st1(s.S, sidx4, Snew);                                   // equ_s4e23
     RowOut o;
     o.Snew = Snew;
     o.Sold = Sold;
-    o.oldbits = oldbits;
-    o.newbits = newbits;
-    o.ok = (negf == 0u) && (flip == 0u);                  // equ_s4e2 and equ_s4e24 for this check
+    o.oldbits = acc.oldbits;
+    o.ok = ((acc.negw | acc.flipw) & kSign) == 0u;           // equ_s4e2 and equ_s4e24 for this check
     return o;
 }
 
-// rewrite the hard-decision bits (sign of P) of lane r's variables in row (e0, dc)
-__device__ __forceinline__ void put_row_bits(const int4* __restrict__ ent, int e0, int dc, int r, int Z, uint32_t bits,
-                                             const SlotPtrs& s)
+// write hard bits (sign of Phi) of lane r's variables in row (e0, dc); returns the previous ones
+__device__ __forceinline__ uint32_t swap_row_bits(const int4* __restrict__ ent, int e0, int dc, int r, int Z,
+                                                  uint32_t bits, const SlotPtrs& s)
 {
+    uint32_t prev = 0;
     for (int k = 0; k < dc; ++k) {
-        const int4 e = ent[e0 + k];
-        int t = r + (e.y & 0x7ff);
-        t = (t >= Z) ? t - Z : t;
-        const int v = (e.x & 0xffff) + t;
-        const float a = fabsf(s.P[v]);
-        s.P[v] = ((bits >> k) & 1u) ? -a : a;
+        const int v = lane_var(ent, e0 + k, r, Z);
+        const uint32_t w = __float_as_uint(s.QP()[v].y);
+        prev |= (w >> 31) << k;
+        s.QP()[v].y = __uint_as_float((w & ~kSign) | (((bits >> k) & 1u) << 31));
     }
+    return prev;
 }
 
-// parity of lane r's checks over all rows, from the hard bits (sign of P)
+// parity of lane r's checks over all rows, from the hard bits (sign of Phi)
 __device__ __forceinline__ bool lane_syndrome(const int4* __restrict__ ent, const int32_t* row_ptr, int mb, int r,
                                               int Z, const SlotPtrs& s)
 {
     uint32_t nz = 0;
     for (int i = 0; i < mb; ++i) {
         uint32_t par = 0;
-        for (int k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
-            const int4 e = ent[k];
-            int t = r + (e.y & 0x7ff);
-            t = (t >= Z) ? t - Z : t;
-            par ^= __float_as_uint(s.P[(e.x & 0xffff) + t]) >> 31;
-        }
+        for (int k = row_ptr[i]; k < row_ptr[i + 1]; ++k)
+            par ^= __float_as_uint(s.QP()[lane_var(ent, k, r, Z)].y) >> 31;
         nz |= par;
     }
     return nz != 0u;
@@ -212,12 +237,8 @@ __device__ __forceinline__ uint32_t info_parity(const int4* __restrict__ ent, co
 {
     uint32_t par = 0;
     for (int k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
-        const int4 e = ent[k];
-        const int vb = e.x & 0xffff;
-        if (vb >= K) continue;
-        int t = r + (e.y & 0x7ff);
-        t = (t >= Z) ? t - Z : t;
-        const int v = vb + t;
+        if (ent[2 * k + 1].w >= K) continue;
+        const int v = lane_var(ent, k, r, Z);
         par ^= (cw[v >> 5] >> (v & 31)) & 1u;
     }
     return par;
@@ -231,6 +252,7 @@ __device__ void channel_frame(const KernelArgs& a, const Team<MULTI>& tm, bool f
     const DevCode& C = a.code;
     const int Z = C.Z, r = tm.r;
     const bool on = fresh && tm.lane_on;
+    float2* QP = s.QP();
     const uint32_t flo = static_cast<uint32_t>(gframe), fhi = static_cast<uint32_t>(static_cast<uint64_t>(gframe) >> 32);
     const uint32_t k0 = static_cast<uint32_t>(a.seed), k1 = static_cast<uint32_t>(a.seed >> 32);
     // (a2) info words: word w = Philox(w/4, f_lo, f_hi, 0)[w%4]
@@ -251,12 +273,12 @@ __device__ void channel_frame(const KernelArgs& a, const Team<MULTI>& tm, bool f
         }
     }
     tm.sync();
-    // (a3) systematic part and p0 = XOR of the core rows' lambda
+    // (a3) systematic part and p0 = XOR of the core rows' lambda (QP.x holds the symbol 1 - 2c)
     if (on) {
-        for (int v = r; v < C.K; v += Z) s.Q[v] = ((s.cw[v >> 5] >> (v & 31)) & 1u) ? -1.0f : 1.0f;
+        for (int v = r; v < C.K; v += Z) QP[v].x = ((s.cw[v >> 5] >> (v & 31)) & 1u) ? -1.0f : 1.0f;
         uint32_t p0 = 0;
         for (int i = 0; i < C.core; ++i) p0 ^= info_parity(ent, row_ptr, i, r, Z, C.K, s.cw);
-        s.Q[C.kb * Z + r] = p0 ? -1.0f : 1.0f;
+        QP[C.kb * Z + r].x = p0 ? -1.0f : 1.0f;
     }
     tm.sync();
     // p_t = lambda_{t-1} ^ p_{t-1} ^ P^{s0} p0 (row t-1), extension p = lambda
@@ -269,14 +291,14 @@ __device__ void channel_frame(const KernelArgs& a, const Team<MULTI>& tm, bool f
             if (s0 >= 0) {
                 int rr = r + s0;
                 rr = (rr >= Z) ? rr - Z : rr;
-                pt ^= s.Q[C.kb * Z + rr] < 0.0f ? 1u : 0u;
+                pt ^= QP[C.kb * Z + rr].x < 0.0f ? 1u : 0u;
             }
-            s.Q[(C.kb + t) * Z + r] = pt ? -1.0f : 1.0f;
+            QP[(C.kb + t) * Z + r].x = pt ? -1.0f : 1.0f;
             pprev = pt;
         }
         for (int k = 0; k < C.mb - C.core; ++k) {
             const uint32_t pe = info_parity(ent, row_ptr, C.core + k, r, Z, C.K, s.cw);
-            s.Q[(C.kb + C.core + k) * Z + r] = pe ? -1.0f : 1.0f;
+            QP[(C.kb + C.core + k) * Z + r].x = pe ? -1.0f : 1.0f;
         }
     }
     tm.sync();
@@ -286,7 +308,7 @@ __device__ void channel_frame(const KernelArgs& a, const Team<MULTI>& tm, bool f
             uint32_t word = 0;
             for (int b = 0; b < 32; ++b) {
                 const int v = 32 * w + b;
-                if (v < C.N && s.Q[v] < 0.0f) word |= 1u << b;
+                if (v < C.N && QP[v].x < 0.0f) word |= 1u << b;
             }
             s.cw[w] = word;
         }
@@ -304,19 +326,18 @@ __device__ void channel_frame(const KernelArgs& a, const Team<MULTI>& tm, bool f
             for (int m = 0; m < 4; ++m) {
                 const int v = 4 * b + m;
                 if (v >= C.N) break;
-                const float y = __fadd_rn(s.Q[v], __fmul_rn(a.sigma, n[m]));
-                float L = __fmul_rn(a.scale, y);
+                const float y = __fadd_rn(QP[v].x, __fmul_rn(a.sigma, n[m]));
+                float Lv = __fmul_rn(a.scale, y);
                 if (a.llr_mode == 1) {
-                    float qq = rintf(__fmul_rn(L, 4.0f));
+                    float qq = rintf(__fmul_rn(Lv, 4.0f));
                     qq = fminf(fmaxf(qq, -127.0f), 127.0f);
-                    L = __fmul_rn(qq, 0.25f);
+                    Lv = __fmul_rn(qq, 0.25f);
                 }
-                s.Q[v] = L;
-                s.P[v] = L < 0.0f ? -0.0f : 0.0f;
+                QP[v] = make_float2(Lv, Lv < 0.0f ? -0.0f : 0.0f);
             }
         }
-        for (int e = r; e < C.E; e += Z) s.R[e] = 0.0f;
-        for (int c = r; c < C.M; c += Z) s.S[c] = 0.0f;
+        for (int e = r; e < C.E; e += Z) s.Rf()[e] = 0.0f;
+        for (int c = r; c < C.M; c += Z) s.Sf()[c] = 0.0f;
     }
     tm.sync();
 }
@@ -329,11 +350,13 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
     const DevCode& C = a.code;
     const int Z = C.Z, mb = C.mb;
 
-    // ---- stage the schedule tables (a1)
-    int4* ent = reinterpret_cast<int4*>(smem);
-    int32_t* row_ptr = reinterpret_cast<int32_t*>(smem + 4 * C.nent);
+    // ---- stage the phi table and the schedule tables (a1)
+    float4* ptab = reinterpret_cast<float4*>(smem);
+    int4* ent = reinterpret_cast<int4*>(smem + 4 * kPhiSegs);
+    int32_t* row_ptr = reinterpret_cast<int32_t*>(smem + 4 * kPhiSegs + 8 * C.nent);
     int16_t* pshift = reinterpret_cast<int16_t*>(row_ptr + mb + 1);
-    for (int k = threadIdx.x; k < C.nent; k += blockDim.x) ent[k] = C.ent[k];
+    for (int k = threadIdx.x; k < kPhiSegs; k += blockDim.x) ptab[k] = C.phi_tab[k];
+    for (int k = threadIdx.x; k < 2 * C.nent; k += blockDim.x) ent[k] = C.ent[k];
     for (int k = threadIdx.x; k <= mb; k += blockDim.x) row_ptr[k] = C.row_ptr[k];
     for (int k = threadIdx.x; k < mb; k += blockDim.x) pshift[k] = C.pshift[k];
     Team<MULTI> tm;
@@ -353,6 +376,7 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
     }
     tm.lane_on = tm.r < Z && tm.slot < a.F;
     const int r = tm.r;
+    const Lane lane{r, 4 * r, 8 * r, Z, 4 * Z, 8 * Z};
     uint32_t* ctl = smem + a.table_words + tm.tidx * kCtlTeamWords;
     long long* ctl64 = reinterpret_cast<long long*>(ctl + 64);
 
@@ -360,11 +384,11 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
     float* sbase = SMEM ? reinterpret_cast<float*>(smem + a.table_words + nteams * kCtlTeamWords)
                         : a.gstate + static_cast<size_t>(blockIdx.x) * nteams * a.F * a.slot_words;
     SlotPtrs s;
-    s.Q = sbase + static_cast<size_t>(tm.tidx * a.F + (tm.slot < a.F ? tm.slot : 0)) * a.slot_words;
-    s.P = s.Q + C.N;
-    s.R = s.P + C.N;
-    s.S = s.R + C.E;
-    s.cw = reinterpret_cast<uint32_t*>(s.S + C.M);
+    float* slot0 = sbase + static_cast<size_t>(tm.tidx * a.F + (tm.slot < a.F ? tm.slot : 0)) * a.slot_words;
+    s.qp = reinterpret_cast<char*>(slot0);
+    s.R = reinterpret_cast<char*>(slot0 + 2 * C.N);
+    s.S = reinterpret_cast<char*>(slot0 + 2 * C.N + C.E);
+    s.cw = reinterpret_cast<uint32_t*>(slot0 + 2 * C.N + C.E + C.M);
     __syncthreads();
 
     const bool belief = a.stop_rule <= 1;
@@ -407,36 +431,38 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
         }
         // ---- Step 1: initialisation (a4/a5)
         if (a.mode == MODE_BER_SIM || a.mode == MODE_CHANNEL) {
-            if (tm.cta_any(fresh))
+            if (tm.team_any(fresh))
                 channel_frame<MULTI>(a, tm, fresh, a.frame_begin + fidx, ent, row_ptr, pshift, s);
         } else {
             if (fresh && tm.lane_on) {
                 const size_t base = static_cast<size_t>(fidx) * a.ld;
                 for (int v = r; v < C.N; v += Z) {
-                    const float L = (a.mode == MODE_DECODE_I8) ? __fmul_rn(static_cast<float>(a.q[base + v]), a.qscale)
-                                                               : a.llr[base + v];
-                    s.Q[v] = L;                                   // equ_s4e15
-                    s.P[v] = L < 0.0f ? -0.0f : 0.0f;             // hard bit from L (R7)
+                    const float Lv = (a.mode == MODE_DECODE_I8) ? __fmul_rn(static_cast<float>(a.q[base + v]), a.qscale)
+                                                                : a.llr[base + v];
+                    s.QP()[v] = make_float2(Lv, Lv < 0.0f ? -0.0f : 0.0f);   // equ_s4e15, hard bit from L (R7)
                 }
-                for (int e = r; e < C.E; e += Z) s.R[e] = 0.0f;   // equ_s4e17
-                for (int c = r; c < C.M; c += Z) s.S[c] = 0.0f;   // equ_s4e16: Omega = inf <=> S = 0
+                for (int e = r; e < C.E; e += Z) s.Rf()[e] = 0.0f;   // equ_s4e17
+                for (int c = r; c < C.M; c += Z) s.Sf()[c] = 0.0f;   // equ_s4e16: Omega = inf <=> S = 0
             }
             tm.sync();
         }
-        if (!tm.cta_any(active)) break;
+        if (!tm.team_any(active)) break;
 
         bool done = false;
         if (decoding) {
             // ---- Step 2: one sweep over the base rows (checks in ascending order)
             for (int i = 0; i < mb; ++i) {
                 const bool live = active && !conv;
-                if (!tm.cta_any(live)) break;
+                if (!tm.team_any(live)) break;
                 const int e0 = row_ptr[i], dc = row_ptr[i + 1] - e0;
                 RowOut ro;
                 ro.ok = true;
-                ro.oldbits = ro.newbits = 0;
+                ro.oldbits = 0;
                 ro.Snew = ro.Sold = 0.0f;
-                if (live && tm.lane_on) ro = process_row(ent, e0, dc, r, Z, i * Z + r, sweep == 1, s);
+                if (live && tm.lane_on) {
+                    if (sweep == 1) ro = process_row<true>(ent, ptab, e0, dc, 4 * (i * Z + r), lane, s);
+                    else ro = process_row<false>(ent, ptab, e0, dc, 4 * (i * Z + r), lane, s);
+                }
                 // ---- Step 2(3): stopping criterion, counted per check update (R4, R5)
                 int first_bad = Z, last_bad = -1;
                 if (MULTI) {
@@ -470,13 +496,14 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
                     if (!fire) consec = (last_bad < 0) ? consec + Z : (Z - 1 - last_bad);
                 }
                 if (live && !fire) ev += static_cast<int64_t>(dc) * Z;
-                if (tm.cta_any(fire)) {
+                if (tm.team_any(fire)) {
                     // the sequential decoder stops right after check i*Z + rstar: lanes r > rstar
                     // show their pre-row hard bits and S while the syndrome is verified (R5)
                     const bool back = fire && tm.lane_on && r > rstar;
+                    uint32_t newbits = 0;
                     if (back) {
-                        put_row_bits(ent, e0, dc, r, Z, ro.oldbits, s);
-                        s.S[i * Z + r] = ro.Sold;
+                        newbits = swap_row_bits(ent, e0, dc, r, Z, ro.oldbits, s);
+                        st1(s.S, 4 * (i * Z + r), ro.Sold);
                     }
                     tm.sync();
                     const bool nz = tm.slot_any(fire && tm.lane_on && lane_syndrome(ent, row_ptr, mb, r, Z, s));
@@ -489,8 +516,8 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
                             ev += static_cast<int64_t>(dc) * Z;
                             consec = Z - 1 - max(static_cast<int64_t>(last_bad), rstar);
                             if (back) {
-                                put_row_bits(ent, e0, dc, r, Z, ro.newbits, s);
-                                s.S[i * Z + r] = ro.Snew;
+                                swap_row_bits(ent, e0, dc, r, Z, newbits, s);
+                                st1(s.S, 4 * (i * Z + r), ro.Snew);
                             }
                         }
                     }
@@ -499,7 +526,7 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
             }
             // ---- end of sweep
             const bool want_syn = active && !conv && a.stop_rule == 2;
-            if (tm.cta_any(want_syn)) {
+            if (tm.team_any(want_syn)) {
                 tm.sync();
                 const bool nz = tm.slot_any(want_syn && tm.lane_on && lane_syndrome(ent, row_ptr, mb, r, Z, s));
                 if (want_syn && !nz) conv = true;
@@ -511,16 +538,17 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
         }
 
         // ---- Step 3: outputs of finished frames (a8)
-        if (tm.cta_any(done)) {
+        if (tm.team_any(done)) {
             tm.sync();
             bool synd_zero = conv;
             const bool need_syn = done && !conv && decoding;
-            if (tm.cta_any(need_syn)) {
+            if (tm.team_any(need_syn)) {
                 const bool nz = tm.slot_any(need_syn && tm.lane_on && lane_syndrome(ent, row_ptr, mb, r, Z, s));
                 if (need_syn) synd_zero = !nz;
             }
             const int iters = conv ? sweep : a.max_iter;
             const uint8_t flags = static_cast<uint8_t>((conv ? 1 : 0) | (synd_zero ? 2 : 0) | (fires > 0 ? 4 : 0));
+            const float2* QP = s.QP();
             if (a.mode == MODE_DECODE_F32 || a.mode == MODE_DECODE_I8) {
                 if (done && tm.lane_on) {
                     uint32_t* out = a.bits + static_cast<size_t>(fidx) * a.ld_words;
@@ -529,15 +557,15 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
                         if (w < C.nwords)
                             for (int b = 0; b < 32; ++b) {
                                 const int v = 32 * w + b;
-                                if (v < C.N) word |= (__float_as_uint(s.P[v]) >> 31) << b;
+                                if (v < C.N) word |= (__float_as_uint(QP[v].y) >> 31) << b;
                             }
                         out[w] = word;
                     }
                     if (a.omega) {
                         float* om = a.omega + static_cast<size_t>(fidx) * C.M;
                         for (int c = r; c < C.M; c += Z) {
-                            const float Sv = s.S[c];
-                            const float m = phi32(fabsf(Sv));
+                            const float Sv = s.Sf()[c];
+                            const float m = phi32(fabsf(Sv), ptab);
                             om[c] = (__float_as_uint(Sv) >> 31) ? -m : m;
                         }
                     }
@@ -554,7 +582,7 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
                         uint32_t word = 0;
                         for (int b = 0; b < 32; ++b) {
                             const int v = 32 * w + b;
-                            if (v < C.N) word |= (__float_as_uint(s.P[v]) >> 31) << b;
+                            if (v < C.N) word |= (__float_as_uint(QP[v].y) >> 31) << b;
                         }
                         const uint32_t d = word ^ s.cw[w];
                         uint32_t im = 0;
@@ -580,7 +608,7 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
                 if (done && tm.lane_on) {
                     if (a.llr_out) {
                         float* out = a.llr_out + static_cast<size_t>(fidx) * a.ld;
-                        for (int v = r; v < C.N; v += Z) out[v] = s.Q[v];
+                        for (int v = r; v < C.N; v += Z) out[v] = QP[v].x;
                     }
                     if (a.cw_out) {
                         uint32_t* out = a.cw_out + static_cast<size_t>(fidx) * a.ld_words;
@@ -604,14 +632,18 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
 }
 
 // element-wise evaluation of the contract functions (pin of device vs oracle bits)
-__global__ void contract_eval_kernel(int fn, const float* __restrict__ x, float* __restrict__ y, int64_t n)
+__global__ void contract_eval_kernel(int fn, const float* __restrict__ x, float* __restrict__ y, int64_t n,
+                                     const float4* __restrict__ tab)
 {
     for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
          k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const float v = x[k];
         float out;
         if (fn == 0) {
-            out = phi32(v);
+            out = phi32(v, tab);
+        } else if (fn == 4) {
+            out = phi_v1_unclamped(fminf(fmaxf(v, kPhiLo), kPhiHi));
+            out = fminf(fmaxf(out, kPhiLo), kPhiHi);
         } else if (fn == 1) {
             out = ln32(v);
         } else {
@@ -623,11 +655,24 @@ __global__ void contract_eval_kernel(int fn, const float* __restrict__ x, float*
     }
 }
 
-int launch_contract_eval(int fn, const float* x, float* y, int64_t n, void* stream)
+int launch_contract_eval(int fn, const float* x, float* y, int64_t n, const float4* tab, void* stream)
 {
     if (n <= 0) return 0;
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
-    contract_eval_kernel<<<static_cast<int>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(fn, x, y, n);
+    contract_eval_kernel<<<static_cast<int>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(fn, x, y, n, tab);
+    return static_cast<int>(cudaGetLastError());
+}
+
+// phi contract v2 table, one thread per segment (fp32 v1 values, fp64 Newton differences)
+__global__ void phi_table_kernel(float4* __restrict__ out)
+{
+    const int seg = blockIdx.x * blockDim.x + threadIdx.x;
+    if (seg < kPhiSegs) out[seg] = phi_segment_coeffs(seg);
+}
+
+int launch_phi_table(float4* out, void* stream)
+{
+    phi_table_kernel<<<(kPhiSegs + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(out);
     return static_cast<int>(cudaGetLastError());
 }
 

@@ -80,17 +80,64 @@ __device__ __forceinline__ float phi_large(float x)
     return __fadd_rn(u, u);
 }
 
-// phi(x) = -log(tanh(x/2)) (equ_s2e5) with input/output clamp
-// Both regimes are evaluated and selected (no divergent branch), so the U
-// independent phi chains of an edge chunk interleave in straight-line code.
-// phi_large is evaluated on max(x, 1) to stay inside its reduction range.
-__device__ __forceinline__ float phi32(float x)
+// phi v1 reference formula (unclamped): only used to build the v2 table
+__device__ __forceinline__ float phi_v1_unclamped(float x)
+{
+    return (x < 1.0f) ? phi_small(x) : phi_large(x);
+}
+
+// ---- phi contract v2: 929-segment cubic in u in [0, 1)
+constexpr int kPhiSegs = 929;
+
+// Coefficients of one segment: cubic through v1 at u = 0, 1/4, 3/4, 1 by
+// Newton divided differences in IEEE double, in the DESIGN.md order.
+__device__ __forceinline__ float4 phi_segment_coeffs(int seg)
+{
+    const int q4[4] = {0, 1, 3, 4};
+    double f[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        float x;
+        if (seg < 704) {
+            const int e = -43 + seg / 16, j = seg % 16;
+            x = __fmul_rn(static_cast<float>(64 + 4 * j + q4[k]), __uint_as_float(static_cast<uint32_t>(127 + e - 6) << 23));
+        } else {
+            x = __fmul_rn(static_cast<float>(64 + 4 * (seg - 704) + q4[k]), 0.03125f);
+        }
+        f[k] = static_cast<double>(phi_v1_unclamped(x));
+    }
+    const double d01 = __dmul_rn(__dsub_rn(f[1], f[0]), 4.0);
+    const double d12 = __dmul_rn(__dsub_rn(f[2], f[1]), 2.0);
+    const double d23 = __dmul_rn(__dsub_rn(f[3], f[2]), 4.0);
+    const double d012 = __ddiv_rn(__dmul_rn(__dsub_rn(d12, d01), 4.0), 3.0);
+    const double d123 = __ddiv_rn(__dmul_rn(__dsub_rn(d23, d12), 4.0), 3.0);
+    const double d0123 = __dsub_rn(d123, d012);
+    const double t2 = __dsub_rn(d01, __dmul_rn(d012, 0.25));
+    const double t3 = __dmul_rn(d0123, 0.1875);
+    return make_float4(__double2float_rn(f[0]), __double2float_rn(__dadd_rn(t2, t3)),
+                       __double2float_rn(__dsub_rn(d012, d0123)), __double2float_rn(d0123));
+}
+
+// phi(x) = -log(tanh(x/2)) (equ_s2e5) with the R9 clamps:
+// segment index and local u from the float's bits (x < 2) or from 8(x - 2)
+// (x >= 2), one 16-byte table load, three FMA.
+__device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab)
 {
     x = fminf(fmaxf(x, kPhiLo), kPhiHi);
-    const float a = phi_small(x);
-    const float b = phi_large(fmaxf(x, 1.0f));
-    const float r = (x < 1.0f) ? a : b;
-    return fminf(fmaxf(r, kPhiLo), kPhiHi);
+    const uint32_t b = __float_as_uint(x);
+    const int seg_lo = static_cast<int>(b >> 19) - 1344;
+    const float u_lo = __fsub_rn(__uint_as_float(((b & 0x7ffffu) << 4) | 0x3f800000u), 1.0f);
+    const float t = __fmaf_rn(x, 8.0f, -16.0f);
+    const int i = static_cast<int>(t);
+    const float u_hi = __fsub_rn(t, static_cast<float>(i));
+    const bool hi = x >= 2.0f;
+    const int seg = hi ? 704 + i : seg_lo;
+    const float u = hi ? u_hi : u_lo;
+    const float4 c = tab[seg];
+    float p = __fmaf_rn(c.w, u, c.z);
+    p = __fmaf_rn(p, u, c.y);
+    p = __fmaf_rn(p, u, c.x);
+    return fminf(fmaxf(p, kPhiLo), kPhiHi);
 }
 
 // sin / cos of 2 pi m 2^-24 with exact integer quadrant reduction (Box-Muller)

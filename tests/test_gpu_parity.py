@@ -77,6 +77,21 @@ def test_contract_bit_equal_on_device():
         assert np.float32(s) == s_gpu[k] and np.float32(c) == c_gpu[k]
 
 
+def test_phi_table_built_on_device_equals_oracle_table():
+    """The v2 table is generated on the GPU (fp32 v1 values + fp64 Newton
+    differences) and independently by the oracle on the host: identical bits."""
+    _need_gpu()
+    g = cbp.cbp.phi_table(0).cpu().numpy()
+    o = oracle.phi32_table()
+    assert (g.view(np.uint32) == o.view(np.uint32)).all()
+    rng = np.random.default_rng(1)
+    x = np.exp(rng.uniform(np.log(1e-14), np.log(40.0), 1 << 20)).astype(np.float32)
+    v1 = cbp.cbp.eval_contract(4, torch.from_numpy(x).cuda()).cpu().numpy()
+    sample = x[:20000]
+    assert (v1[:20000].view(np.uint32) == np.array([oracle.phi32_v1(float(t)) for t in sample],
+                                                    np.float32).view(np.uint32)).all()
+
+
 # ---------------------------------------------------------------- decode parity
 def test_decode_parity_c1_all_10k_frames(codes):
     """BASELINE config 1: every one of the 10,000 frames at 2.0 dB."""
