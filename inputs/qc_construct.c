@@ -74,16 +74,22 @@ int cbp_inputs_construct_base(const cbp_inputs_spec* sp, uint64_t seed,
             if (w < sp->w_lo) w = sp->w_lo;
         }
         for (int i = 0; i < mb; ++i) { key[i] = splitmix64(&st); picked[i] = 0; }
-        /* w selections of the minimum (row_deg, key) among unpicked rows */
+        /* w selections of the minimum (row_deg, key) among unpicked rows.  With a
+         * degree-1 extension (core < mb) the first two go to core rows and the rest
+         * to extension rows, so every info bit is protected by the core (otherwise
+         * an info column lying only on extension rows is a weight-4 codeword). */
+        const int ncore_pick = (core < mb) ? (w < 2 ? w : 2) : w;
         for (int n = 0; n < w; ++n) {
+            const int lo = (core < mb && n >= ncore_pick) ? core : 0;
+            const int hi = (core < mb && n < ncore_pick) ? core : mb;
             int best = -1;
-            for (int i = 0; i < mb; ++i) {
+            for (int i = lo; i < hi; ++i) {
                 if (picked[i]) continue;
                 if (best < 0 || row_deg[i] < row_deg[best] ||
                     (row_deg[i] == row_deg[best] && key[i] < key[best]))
                     best = i;
             }
-            picked[best] = 1;
+            if (best >= 0) picked[best] = 1;
         }
         for (int i = 0; i < mb; ++i) {
             if (!picked[i]) continue;
