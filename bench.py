@@ -25,7 +25,16 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "CBP info Gbit/s and frames/s per GPU and 8×B200 at Eb/N0, % of roofline"
 UNIT = "info Gbit/s"
-I_EDGE = 68            # algorithmic fp32/int ops per edge visit of the contract
+I_EDGE = 38            # algorithmic fp32/int ops per edge visit of the arithmetic contract v2
+
+
+def kernel_traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture (profiles/)."""
+    caps = sorted((ROOT / "profiles").glob("r*_kernel_traffic.json"))
+    if not caps:
+        return None, None
+    d = json.loads(caps[-1].read_text())
+    return d["dram_bytes_read"] + d["dram_bytes_write"], d
 
 
 def parse():
@@ -220,15 +229,19 @@ def main():
         ev_local.append(int(tot[p, 5]) // max(world, 1))       # edge visits per launch (this rank's share)
     dur = np.array(per_launch_ms).reshape(args.steps, len(ebn0s)).mean(axis=0) / 1e3
     ops = np.array(ev_local, dtype=np.float64) * I_EDGE
+    traffic, traffic_src = kernel_traffic()
     achieved = float(ops.sum() / dur.sum())                    # ops/s averaged over the launches of a step
     li = code.launch_info()
     clocks = clk.summary()
     f_sm = measured_peaks().get("sm_max_mhz", 1965.0)
     peak = li["num_sms"] * 128 * f_sm * 1e6
     roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Top/s",
-                "frac": achieved / peak, "traffic": None,
-                "note": f"I_edge={I_EDGE} ops/edge-visit x exact edge visits / mean launch time; peak = "
-                        f"{li['num_sms']} SM x 128 lanes x {f_sm:.0f} MHz (sm_max, MEASURED_PEAKS.json)"}
+                "frac": achieved / peak, "traffic": traffic,
+                "note": f"I_edge={I_EDGE} contract ops/edge-visit x exact edge visits / mean launch time; peak = "
+                        f"{li['num_sms']} SM x 128 lanes x {f_sm:.0f} MHz (sm_max, MEASURED_PEAKS.json); traffic = "
+                        f"DRAM bytes/launch from {traffic_src.get('source', 'n/a') if traffic_src else 'n/a'} "
+                        f"(algorithmic HBM bytes of ber_sim: 0 in, 64 out); shared-memory wavefronts/SM-cycle "
+                        f"{traffic_src.get('smem_wavefronts_per_sm_cycle') if traffic_src else None}"}
 
     # end-to-end: host LLRs -> cbp_decode (pipelined H2D / decode / D2H) -> host outputs
     e2e = None
