@@ -56,6 +56,7 @@ def _lib():
             "oracle_phi32_n": ([_p, _p, _i64], None),
             "oracle_phi32_v1": ([_f32], _f32),
             "oracle_phi32_table": ([_p], None),
+            "oracle_phi32_clamp_check": ([_p, _p, _p], None),
             "oracle_ln32_n": ([_p, _p, _i64], None),
         }
         for name, (args, res) in sig.items():
@@ -208,6 +209,13 @@ def ln32_array(x: np.ndarray) -> np.ndarray:
 
 def phi32_v1(x: float) -> float:
     return float(_lib().oracle_phi32_v1(x))
+
+
+def phi32_clamp_check():
+    """(#below PHI_LO, #above PHI_HI, max) of the unclamped v2 cubic over every float in [PHI_LO, 30]."""
+    b, a, m = _i64(), _i64(), _f32()
+    _lib().oracle_phi32_clamp_check(ctypes.byref(b), ctypes.byref(a), ctypes.byref(m))
+    return b.value, a.value, m.value
 
 
 def phi32_table() -> np.ndarray:

@@ -95,6 +95,7 @@ int oracle_ml_decode(const or_code* c, const float* llr, uint32_t* cw);
 float oracle_phi32(float x);
 float oracle_phi32_v1(float x);
 void  oracle_phi32_table(float* out);    /* 929 x 4 floats */
+void  oracle_phi32_clamp_check(int64_t* below, int64_t* above, float* maxp);
 float oracle_ln32(float x);
 void  oracle_sincos_quarter32(uint32_t m24, float* s, float* c);
 /* element-wise over arrays (pin tests) */

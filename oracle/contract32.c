@@ -161,6 +161,41 @@ static void phi_build_table(void)
     phi_tab_ready = 1;
 }
 
+/* Exhaustive check over every binary32 x in [PHI_LO, PHI_HI] of the v2 cubic
+ * WITHOUT the output clamp: counts results below PHI_LO / above PHI_HI and the
+ * maximum (pin: the output clamp of the contract never binds). */
+void oracle_phi32_clamp_check(int64_t* below, int64_t* above, float* maxp)
+{
+    if (!phi_tab_ready) phi_build_table();
+    const uint32_t a = bits_of(OR_PHI_LO), z = bits_of(OR_PHI_HI);
+    int64_t nb = 0, na = 0;
+    float mx = 0.0f;
+    for (uint32_t w = a; w <= z; ++w) {
+        const float x = f_from_bits(w);
+        int seg;
+        float u;
+        if (x < 2.0f) {
+            seg = (int)(w >> 19) - 1344;
+            u = f_from_bits(((w & 0x7ffffu) << 4) | 0x3f800000u) - 1.0f;
+        } else {
+            const float t = fmaf(x, 8.0f, -16.0f);
+            const int i = (int)t;
+            u = t - (float)i;
+            seg = 704 + i;
+        }
+        const float* c = phi_tab[seg];
+        float p = fmaf(c[3], u, c[2]);
+        p = fmaf(p, u, c[1]);
+        p = fmaf(p, u, c[0]);
+        nb += p < OR_PHI_LO;
+        na += p > OR_PHI_HI;
+        if (p > mx) mx = p;
+    }
+    *below = nb;
+    *above = na;
+    *maxp = mx;
+}
+
 void oracle_phi32_table(float* out)
 {
     if (!phi_tab_ready) phi_build_table();

@@ -8,12 +8,14 @@ present, the calls raise.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import torch
 
 _HERE = Path(__file__).resolve().parent
-_SO = _HERE / "libcbp.so"
+# CBP_LIB selects an alternate build of the same library (A/B kernel experiments)
+_SO = Path(os.environ["CBP_LIB"]) if os.environ.get("CBP_LIB") else _HERE / "libcbp.so"
 _LIB = None
 
 CBP_STOP_BELIEF_M, CBP_STOP_BELIEF_N, CBP_STOP_SYNDROME, CBP_STOP_NONE = 0, 1, 2, 3

@@ -25,6 +25,11 @@ namespace cbp {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr uint32_t kSign = 0x80000000u;
 
+// independent edges of a check processed together (ILP); remainder one at a time
+#ifndef CBP_CHUNK
+#define CBP_CHUNK 3
+#endif
+
 // Per-slot state.  Byte-addressed bases plus typed views for the cold paths.
 struct SlotPtrs {
     char* qp;       // float2 [N]: (Q_{v->c*}, Phi_v = phi(|Q_v|) with sign bit = hard decision x_v)
@@ -121,13 +126,16 @@ struct RowAcc {
 
 // U consecutive edges of lane r's check.  Loads first, then U independent B2V
 // phi chains, commits / V2C, U independent C2B phi chains and the ordered S
-// accumulation (reading R12).  SWEEP1 handles first visits (reading R1).
-template <int U, bool SWEEP1>
+// accumulation (reading R12).  SWEEP1 handles first visits (reading R1); TRACK
+// records the previous hard bits (only rows where the belief window can fire).
+// R_{ci->v} is read after the commit of R_{cj->v}: for a degree-1 column both are
+// the same slot, which realises "commit before read" (R3) through memory order.
+template <int U, bool SWEEP1, bool TRACK>
 __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int k0,
                                            const Lane& L, const SlotPtrs& s, RowAcc& acc)
 {
     int aqp[U], aw[U], ar[U];
-    float q[U], p[U], scj[U], rold[U], Rn[U];
+    float q[U], p[U], scj[U], Rn[U];
     bool fst[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -145,7 +153,6 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
         q[u] = qp.x;
         p[u] = qp.y;
         scj[u] = ld1(s.S, A.y + rp4);
-        rold[u] = ld1(s.R, ar[u]);
     }
     // B2V (equ_s4e18): R^new_{cj->v} = sgn(Omega_cj) sgn(Q) phi(|phi(|Omega_cj|) - phi(|Q|)|), phi(|Omega|) = S (R11)
 #pragma unroll
@@ -155,17 +162,19 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
         Rn[u] = __uint_as_float(__float_as_uint(mag) | sg);
         if (SWEEP1 && fst[u]) Rn[u] = 0.0f;
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (!(SWEEP1 && fst[u])) st1(s.R, aw[u], Rn[u]);   // equ_s4e22 commit of R_{cj->v} (R2), before the read (R3)
     float qn[U];
     uint32_t lb[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        if (!(SWEEP1 && fst[u])) st1(s.R, aw[u], Rn[u]);   // equ_s4e22 commit of R_{cj->v} (R2), before the read (R3)
-        const float ro = (aw[u] == ar[u]) ? Rn[u] : rold[u];
+        const float ro = ld1(s.R, ar[u]);                    // R_{ci->v}
         const float lam = __fadd_rn(q[u], Rn[u]);            // equ_s4e20 (Lambda is never -0)
         qn[u] = __fsub_rn(lam, ro);                          // equ_s4e19 (R15)
         lb[u] = __float_as_uint(lam) & kSign;                // hard decision, equ_s2e7
         acc.flipw |= __float_as_uint(lam) ^ __float_as_uint(p[u]);   // equ_s4e24 (R7), bit 31
-        acc.oldbits |= (__float_as_uint(p[u]) >> 31) << (k0 + u);
+        if (TRACK) acc.oldbits |= (__float_as_uint(p[u]) >> 31) << (k0 + u);
     }
     float ph[U];
 #pragma unroll
@@ -184,15 +193,15 @@ struct RowOut {
     bool ok;
 };
 
-template <bool SWEEP1>
+template <bool SWEEP1, bool TRACK>
 __device__ __forceinline__ RowOut process_row(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
                                               int dc, int sidx4, const Lane& L, const SlotPtrs& s)
 {
     RowAcc acc{0.0f, 0u, 0u, 0u};
     const float Sold = ld1(s.S, sidx4);
     int k0 = 0;
-    for (; k0 + 4 <= dc; k0 += 4) edge_chunk<4, SWEEP1>(ent, ptab, e0, k0, L, s, acc);
-    for (; k0 < dc; ++k0) edge_chunk<1, SWEEP1>(ent, ptab, e0, k0, L, s, acc);
+    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) edge_chunk<CBP_CHUNK, SWEEP1, TRACK>(ent, ptab, e0, k0, L, s, acc);
+    for (; k0 < dc; ++k0) edge_chunk<1, SWEEP1, TRACK>(ent, ptab, e0, k0, L, s, acc);
     const float Snew = __uint_as_float(__float_as_uint(acc.Ssum) | (acc.negw & kSign));
     st1(s.S, sidx4, Snew);                                   // equ_s4e23
     RowOut o;
@@ -344,7 +353,7 @@ __device__ void channel_frame(const KernelArgs& a, const Team<MULTI>& tm, bool f
 
 // ---------------------------------------------------------------- the kernel
 template <bool MULTI, bool SMEM, int MAXT>
-__global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
+__global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
 {
     extern __shared__ __align__(16) uint32_t smem[];
     const DevCode& C = a.code;
@@ -460,8 +469,17 @@ __global__ void __launch_bounds__(MAXT) cbp_kernel(const KernelArgs a)
                 ro.oldbits = 0;
                 ro.Snew = ro.Sold = 0.0f;
                 if (live && tm.lane_on) {
-                    if (sweep == 1) ro = process_row<true>(ent, ptab, e0, dc, 4 * (i * Z + r), lane, s);
-                    else ro = process_row<false>(ent, ptab, e0, dc, 4 * (i * Z + r), lane, s);
+                    // the window can only fill in this row if consec + Z >= W (R4); otherwise
+                    // no rollback information is needed
+                    const bool track = belief && consec + Z >= W;
+                    const int sidx4 = 4 * (i * Z + r);
+                    if (sweep == 1) {
+                        ro = track ? process_row<true, true>(ent, ptab, e0, dc, sidx4, lane, s)
+                                   : process_row<true, false>(ent, ptab, e0, dc, sidx4, lane, s);
+                    } else {
+                        ro = track ? process_row<false, true>(ent, ptab, e0, dc, sidx4, lane, s)
+                                   : process_row<false, false>(ent, ptab, e0, dc, sidx4, lane, s);
+                    }
                 }
                 // ---- Step 2(3): stopping criterion, counted per check update (R4, R5)
                 int first_bad = Z, last_bad = -1;

@@ -114,19 +114,30 @@ __device__ __forceinline__ float4 phi_segment_coeffs(int seg)
     const double d0123 = __dsub_rn(d123, d012);
     const double t2 = __dsub_rn(d01, __dmul_rn(d012, 0.25));
     const double t3 = __dmul_rn(d0123, 0.1875);
-    return make_float4(__double2float_rn(f[0]), __double2float_rn(__dadd_rn(t2, t3)),
-                       __double2float_rn(__dsub_rn(d012, d0123)), __double2float_rn(d0123));
+    float4 c = make_float4(__double2float_rn(f[0]), __double2float_rn(__dadd_rn(t2, t3)),
+                           __double2float_rn(__dsub_rn(d012, d0123)), __double2float_rn(d0123));
+    if (seg < 704) {
+        // device storage form: the local variable of x < 2 is taken as u' = u/16 (no shift),
+        // so c1, c2, c3 are stored times 16, 256, 4096 -- exact, and every product of the
+        // Horner evaluation is scaled by the same power of two: identical results.
+        c.y = __fmul_rn(c.y, 16.0f);
+        c.z = __fmul_rn(c.z, 256.0f);
+        c.w = __fmul_rn(c.w, 4096.0f);
+    }
+    return c;
 }
 
-// phi(x) = -log(tanh(x/2)) (equ_s2e5) with the R9 clamps:
+// phi(x) = -log(tanh(x/2)) (equ_s2e5) with the R9 input clamp:
 // segment index and local u from the float's bits (x < 2) or from 8(x - 2)
-// (x >= 2), one 16-byte table load, three FMA.
+// (x >= 2), one 16-byte table load, three FMA.  The contract's output clamp is
+// omitted: on every float of [PHI_LO, 30] the cubic already lies in [PHI_LO, 30]
+// (exhaustive check, tests/test_oracle_contract.py), so results are identical.
 __device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab)
 {
     x = fminf(fmaxf(x, kPhiLo), kPhiHi);
     const uint32_t b = __float_as_uint(x);
     const int seg_lo = static_cast<int>(b >> 19) - 1344;
-    const float u_lo = __fsub_rn(__uint_as_float(((b & 0x7ffffu) << 4) | 0x3f800000u), 1.0f);
+    const float u_lo = __fsub_rn(__uint_as_float((b & 0x7ffffu) | 0x3f800000u), 1.0f);   // u/16, see phi_segment_coeffs
     const float t = __fmaf_rn(x, 8.0f, -16.0f);
     const int i = static_cast<int>(t);
     const float u_hi = __fsub_rn(t, static_cast<float>(i));
@@ -136,8 +147,7 @@ __device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab)
     const float4 c = tab[seg];
     float p = __fmaf_rn(c.w, u, c.z);
     p = __fmaf_rn(p, u, c.y);
-    p = __fmaf_rn(p, u, c.x);
-    return fminf(fmaxf(p, kPhiLo), kPhiHi);
+    return __fmaf_rn(p, u, c.x);
 }
 
 // sin / cos of 2 pi m 2^-24 with exact integer quadrant reduction (Box-Muller)

@@ -147,3 +147,10 @@ def test_phi_v2_table_interpolates_v1_at_nodes():
                 assert p == pytest.approx(f, rel=4e-7), (seg, q)
         if seg < 704:
             assert np.float32(t[seg, 0]) == t[seg, 0]
+
+
+def test_phi_v2_output_clamp_never_binds():
+    """Exhaustive over every float in [PHI_LO, 30]: the unclamped v2 cubic stays in
+    [PHI_LO, 30], so an implementation may omit the output clamp (the GPU does)."""
+    below, above, mx = oracle.phi32_clamp_check()
+    assert below == 0 and above == 0 and mx <= 30.0

@@ -68,23 +68,27 @@ def build_oracle(force=False):
     return ORACLE_SO
 
 
-def build_cbp(force=False):
+def build_cbp(force=False, out=None, defines=()):
+    """libcbp.so; `out`/`defines` build an alternate variant (kernel A/B experiments,
+    loaded with CBP_LIB=<path>)."""
+    out = Path(out) if out else CBP_SO
     deps = CBP_SRC + CBP_HDR + INPUTS_SRC
-    if force or _stale(CBP_SO, deps):
-        tmp = ROOT / "build" / "cbp"
+    if force or _stale(out, deps):
+        tmp = ROOT / "build" / ("cbp" if out == CBP_SO else "cbp_" + out.stem)
         tmp.mkdir(parents=True, exist_ok=True)
         objs = []
         common = ["-I", ROOT / "include", "-I", ROOT / "inputs", "-I", ROOT / "paper_2305_05286_b200" / "csrc"]
         for src in CBP_SRC:
             obj = tmp / (src.stem + ".o")
             _run([NVCC, "-std=c++17", *ARCH, "-O3", "-lineinfo", *NVCC_CONTRACT, "-Xptxas", "-v",
-                  "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", *common, "-c", src, "-o", obj])
+                  "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-Xcompiler", "-ffp-contract=off",
+                  *[f"-D{d}" for d in defines], *common, "-c", src, "-o", obj])
             objs.append(obj)
         inp_obj = tmp / "qc_construct.o"
         _run(["gcc", "-std=c11", "-O2", "-fPIC", "-c", INPUTS_SRC[0], "-o", inp_obj])
         objs.append(inp_obj)
-        _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", CBP_SO])
-    return CBP_SO
+        _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", out])
+    return out
 
 
 def build_all(force=False):
