@@ -98,16 +98,18 @@ struct Team {
         if (MULTI) named_bar_sync(1 + tidx, nthreads);
         else __syncwarp();
     }
-    // OR over the team (a synchronisation point)
+    // OR of a slot-uniform predicate over the team's slots.  A MULTI team holds one
+    // frame and every thread derives the control state identically, so the predicate
+    // is already team-uniform (no barrier); a warp team votes over its F slots.
     __device__ __forceinline__ bool team_any(bool pred) const
     {
-        if (MULTI) return named_bar_or(1 + tidx, nthreads, pred);
+        if (MULTI) return pred;
         return __any_sync(kFull, pred) != 0;
     }
     // OR over the lanes of this slot (a synchronisation point)
     __device__ __forceinline__ bool slot_any(bool pred) const
     {
-        if (MULTI) return team_any(pred);
+        if (MULTI) return named_bar_or(1 + tidx, nthreads, pred);
         return (__ballot_sync(kFull, pred) & slot_mask) != 0u;
     }
 };
