@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--llr-mode", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-suite", action="store_true", help="skip the other-config measurements")
     ap.add_argument("--e2e-frames", type=int, default=200_000)
     ap.add_argument("--cpu-frames", type=int, default=400, help="oracle frames per Eb/N0 point (cpu_baseline)")
     return ap.parse_args()
@@ -272,6 +273,39 @@ def main():
                "what": f"cbp_decode via pipeline.decode_host on {Fe} host-resident frames/GPU at {eb_mid} dB "
                        f"(pinned host LLRs, H2D + decode + D2H of bits/iters/flags timed, host wall clock)"}
 
+    # the other BASELINE configs, one timed fused launch each (after a warm-up launch):
+    # C1 @ 2 dB; C3a / C3b (rates 1/2, 5/6); C4 (global-state path, syndrome stop);
+    # C5 = C3a @ 2.5 dB with the fp32 and the int8 LLR stream
+    others = {}
+    if not args.no_suite:
+        suite = [("C1", 2.0, 1_000_000, 0, 0), ("C3a", 2.5, 300_000, 0, 0), ("C5", 2.5, 300_000, 0, 1),
+                 ("C3b", 4.0, 300_000, 0, 0), ("C4", 1.5, 3_000, 2, 0)]
+        for name, eb, nf, rule, lm in suite:
+            ocfg = inputs.CONFIGS[name]
+            ob, oz = inputs.config_base(name)
+            oc = cbp.Code(ob, oz, device=local)
+            c = torch.zeros(8, dtype=torch.int64, device=dev)
+            oc.ber_sim(eb, args.seed, 0, min(nf, 20_000), ocfg.max_iter, rule, lm, counts=c, stream=stream)
+            c.zero_()
+            barrier()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            oc.ber_sim(eb, args.seed, rank * nf, nf, ocfg.max_iter, rule, lm, counts=c, stream=stream)
+            a1.record(stream)
+            allreduce_counts(c)
+            torch.cuda.synchronize()
+            ms = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            t = c.cpu().numpy()
+            others[f"{name}@{eb}dB" + ("/int8" if lm else "")] = {
+                "N": oc.N, "K": oc.K, "frames": int(t[0]), "ms": ms.item(),
+                "frames_per_s": t[0] / ms.item() * 1e3, "info_gbps": t[0] * oc.K / ms.item() / 1e6,
+                "edge_visits_per_s": t[5] / ms.item() * 1e3, "ber": t[1] / max(1, t[0] * oc.K),
+                "fer": t[2] / max(1, t[0]), "avg_iters": t[4] / max(1, t[0]),
+                "stop_rule": ["belief W=M", "belief W=N", "syndrome", "none"][rule],
+                "launch": oc.launch_info()}
+
     cpu = None
     if rank == 0 and not args.no_cpu:
         try:
@@ -302,6 +336,7 @@ def main():
             "config": config_block(cfg, ebn0s, frames, args, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": args.steps * len(ebn0s), "launch": li, "results": results,
+            "other_configs": others,
         }
         print(json.dumps(line))
     if world > 1:
