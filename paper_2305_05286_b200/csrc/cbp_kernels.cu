@@ -117,6 +117,7 @@ struct Team {
 // ---------------------------------------------------------------- per-row edge chain
 struct Lane {
     int r, r4, r8, Z, Z4, Z8;
+    int qp_bytes, R_bytes, S_bytes;   // slot array sizes (bounds checks of debug builds)
 };
 
 struct RowAcc {
@@ -147,6 +148,9 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
         t8 = (t8 >= L.Z8) ? t8 - L.Z8 : t8;
         int rp4 = L.r4 + B.y;
         rp4 = (rp4 >= L.Z4) ? rp4 - L.Z4 : rp4;
+        CBP_CHECK(t8 >= 0 && t8 < L.Z8 && rp4 >= 0 && rp4 < L.Z4);
+        CBP_CHECK(A.x + t8 + 8 <= L.qp_bytes && A.y + rp4 + 4 <= L.S_bytes && A.z + L.r4 + 4 <= L.R_bytes &&
+                  A.w + rp4 + 4 <= L.R_bytes);
         aqp[u] = A.x + t8;
         aw[u] = A.w + rp4;
         ar[u] = A.z + L.r4;
@@ -387,7 +391,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
     }
     tm.lane_on = tm.r < Z && tm.slot < a.F;
     const int r = tm.r;
-    const Lane lane{r, 4 * r, 8 * r, Z, 4 * Z, 8 * Z};
+    const Lane lane{r, 4 * r, 8 * r, Z, 4 * Z, 8 * Z, 8 * C.N, 4 * C.E, 4 * C.M};
     uint32_t* ctl = smem + a.table_words + tm.tidx * kCtlTeamWords;
     long long* ctl64 = reinterpret_cast<long long*>(ctl + 64);
 

@@ -6,7 +6,16 @@
 // IEEE div/sqrt and denormals kept.  Every FMA below is an explicit
 // __fmaf_rn (one correctly rounded FFMA), never formed by the compiler.
 #pragma once
+#include <cassert>
 #include <cstdint>
+
+// CBP_DEBUG_BOUNDS: device asserts on every table / shared-state index (debug builds
+// only; compute-sanitizer is not available on the GPU pool)
+#ifdef CBP_DEBUG_BOUNDS
+#define CBP_CHECK(c) assert(c)
+#else
+#define CBP_CHECK(c) ((void)0)
+#endif
 
 namespace cbp {
 
@@ -144,6 +153,7 @@ __device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab)
     const bool hi = x >= 2.0f;
     const int seg = hi ? 704 + i : seg_lo;
     const float u = hi ? u_hi : u_lo;
+    CBP_CHECK(seg >= 0 && seg < kPhiSegs);
     const float4 c = tab[seg];
     float p = __fmaf_rn(c.w, u, c.z);
     p = __fmaf_rn(p, u, c.y);
