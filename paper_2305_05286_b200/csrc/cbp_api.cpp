@@ -308,6 +308,8 @@ cbp::KernelArgs base_args(const cbp_code* c)
     d.ent = c->d_ent; d.row_ptr = c->d_row_ptr; d.pshift = c->d_pshift; d.phi_tab = c->phi_tab;
     a.Zp = c->geo.Zp; a.F = c->geo.F; a.slot_words = c->geo.slot_words; a.table_words = c->geo.table_words;
     a.team_threads = c->geo.team_threads;
+    a.phi_m19 = 0x7ffffu;
+    a.phi_one = 0x3f800000u;
     a.max_iter = 1; a.stop_rule = 0;
     return a;
 }

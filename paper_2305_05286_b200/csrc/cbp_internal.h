@@ -54,6 +54,7 @@ struct KernelArgs {
     unsigned long long* queue;    // frame work counter (zeroed)
     // geometry
     int32_t Zp, F, slot_words, table_words, team_threads;
+    uint32_t phi_m19, phi_one;     // 0x7ffff, 0x3f800000 (phi local variable, runtime operands)
     float* gstate;         // per-CTA global state (state_in_smem == 0)
 };
 

@@ -118,6 +118,7 @@ struct Team {
 struct Lane {
     int r, r4, r8, Z, Z4, Z8;
     int qp_bytes, R_bytes, S_bytes;   // slot array sizes (bounds checks of debug builds)
+    uint32_t m19, one;                // phi local-variable masks as runtime operands (one LOP3)
 };
 
 struct RowAcc {
@@ -163,7 +164,7 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
     // B2V (equ_s4e18): R^new_{cj->v} = sgn(Omega_cj) sgn(Q) phi(|phi(|Omega_cj|) - phi(|Q|)|), phi(|Omega|) = S (R11)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const float mag = phi32(fabsf(__fsub_rn(fabsf(scj[u]), fabsf(p[u]))), ptab);
+        const float mag = phi32(fabsf(__fsub_rn(fabsf(scj[u]), fabsf(p[u]))), ptab, L.m19, L.one);
         const uint32_t sg = (__float_as_uint(scj[u]) ^ __float_as_uint(q[u])) & kSign;
         Rn[u] = __uint_as_float(__float_as_uint(mag) | sg);
         if (SWEEP1 && fst[u]) Rn[u] = 0.0f;
@@ -184,7 +185,7 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
     }
     float ph[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) ph[u] = phi32(fabsf(qn[u]), ptab);   // C2B (equ_s4e21, App. equ_ae4)
+    for (int u = 0; u < U; ++u) ph[u] = phi32(fabsf(qn[u]), ptab, L.m19, L.one);   // C2B (equ_s4e21, App. equ_ae4)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         acc.Ssum = __fadd_rn(acc.Ssum, ph[u]);
@@ -292,7 +293,11 @@ __device__ void channel_frame(const KernelArgs& a, const Team<MULTI>& tm, bool f
     if (on) {
         for (int v = r; v < C.K; v += Z) QP[v].x = ((s.cw[v >> 5] >> (v & 31)) & 1u) ? -1.0f : 1.0f;
         uint32_t p0 = 0;
-        for (int i = 0; i < C.core; ++i) p0 ^= info_parity(ent, row_ptr, i, r, Z, C.K, s.cw);
+        for (int i = 0; i < C.core; ++i) {
+            const uint32_t lam = info_parity(ent, row_ptr, i, r, Z, C.K, s.cw);
+            s.Sf()[i * Z + r] = __uint_as_float(lam);      // lambda_i[r] kept for the next pass (S is free here)
+            p0 ^= lam;
+        }
         QP[C.kb * Z + r].x = p0 ? -1.0f : 1.0f;
     }
     tm.sync();
@@ -300,7 +305,7 @@ __device__ void channel_frame(const KernelArgs& a, const Team<MULTI>& tm, bool f
     if (on) {
         uint32_t pprev = 0;
         for (int t = 1; t < C.core; ++t) {
-            uint32_t pt = info_parity(ent, row_ptr, t - 1, r, Z, C.K, s.cw);
+            uint32_t pt = __float_as_uint(s.Sf()[(t - 1) * Z + r]);   // lambda_{t-1}[r]
             if (t >= 2) pt ^= pprev;
             const int s0 = pshift[t - 1];
             if (s0 >= 0) {
@@ -391,7 +396,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
     }
     tm.lane_on = tm.r < Z && tm.slot < a.F;
     const int r = tm.r;
-    const Lane lane{r, 4 * r, 8 * r, Z, 4 * Z, 8 * Z, 8 * C.N, 4 * C.E, 4 * C.M};
+    const Lane lane{r, 4 * r, 8 * r, Z, 4 * Z, 8 * Z, 8 * C.N, 4 * C.E, 4 * C.M, a.phi_m19, a.phi_one};
     uint32_t* ctl = smem + a.table_words + tm.tidx * kCtlTeamWords;
     long long* ctl64 = reinterpret_cast<long long*>(ctl + 64);
 
@@ -407,12 +412,13 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
     __syncthreads();
 
     const bool belief = a.stop_rule <= 1;
-    const int64_t W = (a.stop_rule == 1) ? C.N : C.M;        // R4
+    const int W = (a.stop_rule == 1) ? C.N : C.M;            // R4 (N, M < 65536)
     const bool decoding = a.mode != MODE_CHANNEL;
 
     // per-slot control (uniform over the slot's lanes)
     bool active = false, exhausted = (tm.slot >= a.F), conv = false;
-    int64_t fidx = -1, ev = 0, consec = 0;
+    int64_t fidx = -1;
+    int ev_dc = 0, ev_part = 0, consec = 0;   // edge visits = ev_dc * Z + ev_part
     int sweep = 1, fires = 0;
     // per-lane counters (ber_sim)
     unsigned long long cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -436,7 +442,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
                 active = fresh = true;
                 fidx = f;
                 conv = false;
-                ev = 0;
+                ev_dc = ev_part = 0;
                 consec = 0;
                 sweep = 1;
                 fires = 0;
@@ -488,7 +494,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
                     }
                 }
                 // ---- Step 2(3): stopping criterion, counted per check update (R4, R5)
-                int first_bad = Z, last_bad = -1;
+                int first_bad = Z, last_bad = -1;   // first / last unclean check of the row
                 if (MULTI) {
                     const int buf = (i & 1) * 32;
                     const unsigned m = __ballot_sync(kFull, tm.lane_on && !ro.ok);
@@ -513,13 +519,13 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
                     }
                 }
                 bool fire = false;
-                int64_t rstar = 0;
+                int rstar = 0;
                 if (live && belief) {
                     rstar = W - consec - 1;           // the window fills at check i*Z + rstar
                     fire = rstar < Z && first_bad > rstar;
                     if (!fire) consec = (last_bad < 0) ? consec + Z : (Z - 1 - last_bad);
                 }
-                if (live && !fire) ev += static_cast<int64_t>(dc) * Z;
+                if (live && !fire) ev_dc += dc;
                 if (tm.team_any(fire)) {
                     // the sequential decoder stops right after check i*Z + rstar: lanes r > rstar
                     // show their pre-row hard bits and S while the syndrome is verified (R5)
@@ -534,11 +540,11 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
                     if (fire) {
                         if (!nz) {
                             conv = true;             // converged: output = state after check i*Z + rstar
-                            ev += static_cast<int64_t>(dc) * (rstar + 1);
+                            ev_part += dc * (rstar + 1);
                         } else {
                             fires += 1;              // undetected fire: resume (R5)
-                            ev += static_cast<int64_t>(dc) * Z;
-                            consec = Z - 1 - max(static_cast<int64_t>(last_bad), rstar);
+                            ev_dc += dc;
+                            consec = Z - 1 - max(last_bad, rstar);
                             if (back) {
                                 swap_row_bits(ent, e0, dc, r, Z, newbits, s);
                                 st1(s.S, 4 * (i * Z + r), ro.Snew);
@@ -596,7 +602,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
                     if (r == 0) {
                         a.iters[fidx] = iters;
                         a.flags[fidx] = flags;
-                        if (a.ev) a.ev[fidx] = ev;
+                        if (a.ev) a.ev[fidx] = static_cast<int64_t>(ev_dc) * Z + ev_part;
                     }
                 }
             } else if (a.mode == MODE_BER_SIM) {
@@ -624,7 +630,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
                     cnt[2] += fe;
                     cnt[3] += ce;
                     cnt[4] += iters;
-                    cnt[5] += ev;
+                    cnt[5] += static_cast<int64_t>(ev_dc) * Z + ev_part;
                     cnt[6] += conv ? 0 : 1;
                     cnt[7] += fires;
                 }

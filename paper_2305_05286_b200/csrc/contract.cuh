@@ -141,12 +141,16 @@ __device__ __forceinline__ float4 phi_segment_coeffs(int seg)
 // (x >= 2), one 16-byte table load, three FMA.  The contract's output clamp is
 // omitted: on every float of [PHI_LO, 30] the cubic already lies in [PHI_LO, 30]
 // (exhaustive check, tests/test_oracle_contract.py), so results are identical.
-__device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab)
+// m19 = 0x7ffff and one = 0x3f800000 are passed in registers so that
+// (b & m19) | one is a single LOP3 (immediates would take two).
+__device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab, uint32_t m19, uint32_t one)
 {
     x = fminf(fmaxf(x, kPhiLo), kPhiHi);
     const uint32_t b = __float_as_uint(x);
     const int seg_lo = static_cast<int>(b >> 19) - 1344;
-    const float u_lo = __fsub_rn(__uint_as_float((b & 0x7ffffu) | 0x3f800000u), 1.0f);   // u/16, see phi_segment_coeffs
+    uint32_t ub;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(ub) : "r"(b), "r"(m19), "r"(one));   // (b & m19) | one
+    const float u_lo = __fsub_rn(__uint_as_float(ub), 1.0f);   // u/16, see phi_segment_coeffs
     const float t = __fmaf_rn(x, 8.0f, -16.0f);
     const int i = static_cast<int>(t);
     const float u_hi = __fsub_rn(t, static_cast<float>(i));
@@ -158,6 +162,11 @@ __device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab)
     float p = __fmaf_rn(c.w, u, c.z);
     p = __fmaf_rn(p, u, c.y);
     return __fmaf_rn(p, u, c.x);
+}
+
+__device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab)
+{
+    return phi32(x, tab, 0x7ffffu, 0x3f800000u);
 }
 
 // sin / cos of 2 pi m 2^-24 with exact integer quadrant reduction (Box-Muller)
