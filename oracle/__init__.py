@@ -15,7 +15,8 @@ _HERE = Path(__file__).resolve().parent
 _LIB = None
 
 STOP_BELIEF_M, STOP_BELIEF_N, STOP_SYNDROME, STOP_NONE = 0, 1, 2, 3
-FP32_CONTRACT, FP64, FP64_LITERAL = 0, 1, 2
+FP32_CONTRACT, FP64, FP64_LITERAL, MINSUM = 0, 1, 2, 3
+ALPHA_DEFAULT = 0.75   # normalized min-sum parameter (reading R20; the paper leaves alpha open)
 PHI_LO = float.fromhex("0x1.a56e0cp-43")
 PHI_HI = 30.0
 
@@ -24,7 +25,7 @@ _i32, _i64, _u64, _f32, _f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, 
 
 
 class Opts(ctypes.Structure):
-    _fields_ = [("max_iter", _i32), ("stop_rule", _i32), ("arith", _i32), ("reserved", _i32)]
+    _fields_ = [("max_iter", _i32), ("stop_rule", _i32), ("arith", _i32), ("alpha", _f32)]
 
 
 def _lib():
@@ -49,6 +50,8 @@ def _lib():
             "oracle_ber_sim": ([_p, _f64, _u64, _i64, _i64, _p, _i32, _p], ctypes.c_int),
             "oracle_cbp_trace_f64": ([_p, _p, _i32, _p], ctypes.c_int),
             "oracle_lbp_trace_f64": ([_p, _p, _i32, _p], ctypes.c_int),
+            "oracle_minsum_cbp_trace": ([_p, _p, _i32, _f32, _p], ctypes.c_int),
+            "oracle_minsum_lbp_trace": ([_p, _p, _i32, _f32, _p], ctypes.c_int),
             "oracle_ml_decode": ([_p, _p, _p], ctypes.c_int),
             "oracle_phi32": ([_f32], _f32),
             "oracle_ln32": ([_f32], _f32),
@@ -105,14 +108,14 @@ class OracleCode:
         return H
 
     def decode(self, llr: np.ndarray, max_iter: int, stop_rule: int = STOP_BELIEF_M,
-               arith: int = FP32_CONTRACT, want_omega: bool = False) -> dict:
+               arith: int = FP32_CONTRACT, want_omega: bool = False, alpha: float = ALPHA_DEFAULT) -> dict:
         llr = np.ascontiguousarray(llr, dtype=np.float32).reshape(-1, self.N)
         F = llr.shape[0]
         out = {"bits": np.zeros((F, self.words), np.uint32), "iters": np.zeros(F, np.int32),
                "flags": np.zeros(F, np.uint8), "edge_visits": np.zeros(F, np.int64),
                "fires": np.zeros(F, np.int32)}
         om = np.zeros((F, self.M), np.float32) if want_omega else None
-        o = Opts(max_iter, stop_rule, arith, 0)
+        o = Opts(max_iter, stop_rule, arith, alpha)
         rc = _lib().oracle_decode(self._h, _ptr(llr), self.N, F, ctypes.byref(o), _ptr(out["bits"]), self.words,
                                   _ptr(out["iters"]), _ptr(out["flags"]), _ptr(out["edge_visits"]),
                                   _ptr(out["fires"]), _ptr(om))
@@ -146,9 +149,10 @@ class OracleCode:
         return llr, cw
 
     def ber_sim(self, ebn0_db: float, seed: int, frame_begin: int, frames: int, max_iter: int,
-                stop_rule: int = STOP_BELIEF_M, llr_mode: int = 0, arith: int = FP32_CONTRACT) -> np.ndarray:
+                stop_rule: int = STOP_BELIEF_M, llr_mode: int = 0, arith: int = FP32_CONTRACT,
+                alpha: float = ALPHA_DEFAULT) -> np.ndarray:
         counts = np.zeros(8, np.int64)
-        o = Opts(max_iter, stop_rule, arith, 0)
+        o = Opts(max_iter, stop_rule, arith, alpha)
         rc = _lib().oracle_ber_sim(self._h, ebn0_db, seed, frame_begin, frames, ctypes.byref(o), llr_mode,
                                    _ptr(counts))
         if rc:
@@ -163,6 +167,18 @@ class OracleCode:
     def lbp_trace(self, llr: np.ndarray, sweeps: int) -> np.ndarray:
         lam = np.zeros((sweeps, self.E), np.float64)
         _lib().oracle_lbp_trace_f64(self._h, _ptr(np.ascontiguousarray(llr, np.float32)), sweeps, _ptr(lam))
+        return lam
+
+    def minsum_cbp_trace(self, llr: np.ndarray, sweeps: int, alpha: float = ALPHA_DEFAULT) -> np.ndarray:
+        lam = np.zeros((sweeps, self.E), np.float32)
+        _lib().oracle_minsum_cbp_trace(self._h, _ptr(np.ascontiguousarray(llr, np.float32)), sweeps, alpha,
+                                       _ptr(lam))
+        return lam
+
+    def minsum_lbp_trace(self, llr: np.ndarray, sweeps: int, alpha: float = ALPHA_DEFAULT) -> np.ndarray:
+        lam = np.zeros((sweeps, self.E), np.float32)
+        _lib().oracle_minsum_lbp_trace(self._h, _ptr(np.ascontiguousarray(llr, np.float32)), sweeps, alpha,
+                                       _ptr(lam))
         return lam
 
     def ml_decode(self, llr: np.ndarray) -> np.ndarray:

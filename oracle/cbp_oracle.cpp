@@ -405,10 +405,107 @@ static FrameResult cbp_frame(const or_code* c, const float* L, const or_opts* o,
     return res;
 }
 
+// ---------------------------------------------------------------- normalized min-sum CBP
+// B2V equ_s4e18xx  R^new = (Omega^min_cj == Q) ? Omega^submin_cj : Omega^min_cj,
+// C2B equ_s4e21xx  (Omega^min, Omega^submin) updated with alpha * Q^new.  Completion (reading
+// R20): magnitudes compared after scaling, m = fl(alpha |Q^new|) < min (strict); the minimum's
+// owner is tracked by edge instead of comparing values; signs as in psi- (equ_s4e13):
+// sgn(R^new) = sgn(Omega_cj) sgn(Q), sgn(Omega_c) = prod sgn(Q^new).  Omega^(-1) = (inf, inf).
+// Everything else (Step 1, V2C, commit, stop rule) is the CBP schedule of cbp_frame.
+static FrameResult minsum_frame(const or_code* c, const float* L, const or_opts* o, std::vector<uint8_t>& xhat,
+                                std::vector<float>* om_out, float* trace)
+{
+    const int32_t N = c->N, M = c->M;
+    const int32_t NONE = -1;
+    const float INF = std::numeric_limits<float>::infinity();
+    const float alpha = o->alpha;
+    std::vector<float> Q(N), R(c->E, 0.0f);
+    std::vector<float> mn(M, INF), smn(M, INF);
+    std::vector<int32_t> own(M, NONE), latest(N, NONE);
+    std::vector<uint8_t> neg(M, 0);
+    xhat.assign(N, 0);
+    for (int32_t v = 0; v < N; ++v) {
+        Q[v] = L[v];
+        xhat[v] = Q[v] < 0.0f;
+    }
+    const int64_t W = (o->stop_rule == OR_STOP_BELIEF_N) ? (int64_t)N : (int64_t)M;
+    const bool belief = o->stop_rule == OR_STOP_BELIEF_M || o->stop_rule == OR_STOP_BELIEF_N;
+    int64_t consec = 0;
+    FrameResult res;
+    bool converged = false;
+    for (int32_t sweep = 1; sweep <= o->max_iter && !converged; ++sweep) {
+        for (int32_t ci = 0; ci < M && !converged; ++ci) {
+            float m1 = INF, m2 = INF;
+            int32_t ow = NONE;
+            uint8_t ng = 0;
+            bool flip = false;
+            for (int32_t e = c->chk_ptr[ci]; e < c->chk_ptr[ci + 1]; ++e) {
+                const int32_t v = c->e_var[e];
+                const int32_t ej = latest[v];
+                float Rn = 0.0f;
+                if (ej != NONE) {                                 // B2V, equ_s4e18xx
+                    const int32_t cj = c->e_chk[ej];
+                    const float mag = (own[cj] == ej) ? smn[cj] : mn[cj];
+                    const bool sg = (neg[cj] != 0) != (Q[v] < 0.0f);
+                    Rn = sg ? -mag : mag;
+                    R[ej] = Rn;                                   // commit before the read (R2, R3)
+                }
+                const float lam = Q[v] + Rn;                      // V2C, equ_s4e20 / equ_s4e19
+                const float qn = lam - R[e];
+                if (trace) trace[e] = lam;
+                const uint8_t bit = lam < 0.0f;
+                if (bit != xhat[v]) flip = true;
+                xhat[v] = bit;
+                const float m = alpha * std::fabs(qn);            // C2B, equ_s4e21xx
+                if (m < m1) {
+                    m2 = m1;
+                    m1 = m;
+                    ow = e;
+                } else if (m < m2) {
+                    m2 = m;
+                }
+                ng ^= (uint8_t)(qn < 0.0f);
+                Q[v] = qn;
+                latest[v] = e;
+            }
+            mn[ci] = m1;
+            smn[ci] = m2;
+            own[ci] = ow;
+            neg[ci] = ng;
+            res.edge_visits += c->chk_ptr[ci + 1] - c->chk_ptr[ci];
+            if (belief) {                                         // stop rule, as cbp_frame
+                const bool ok = (ng == 0) && !flip;
+                consec = ok ? consec + 1 : 0;
+                if (consec >= W) {
+                    if (syndrome_weight_bits(c, xhat) == 0) {
+                        converged = true;
+                        res.iters = sweep;
+                    } else {
+                        res.fires += 1;
+                        consec = 0;
+                    }
+                }
+            }
+        }
+        if (!converged && o->stop_rule == OR_STOP_SYNDROME && syndrome_weight_bits(c, xhat) == 0) {
+            converged = true;
+            res.iters = sweep;
+        }
+    }
+    if (!converged) res.iters = o->max_iter;
+    res.flags = (uint8_t)((converged ? 1 : 0) | (syndrome_weight_bits(c, xhat) == 0 ? 2 : 0) |
+                          (res.fires > 0 ? 4 : 0));
+    if (om_out) {
+        om_out->resize(M);
+        for (int32_t ck = 0; ck < M; ++ck) (*om_out)[ck] = neg[ck] ? -mn[ck] : mn[ck];   // signed minimum
+    }
+    return res;
+}
+
 static bool opts_ok(const or_opts* o)
 {
     return o && o->max_iter >= 1 && o->max_iter <= 65535 && o->stop_rule >= 0 && o->stop_rule <= 3 &&
-           o->arith >= 0 && o->arith <= 2;
+           o->arith >= 0 && o->arith <= 3 && (o->arith != OR_MINSUM || (o->alpha > 0.0f && o->alpha <= 1.0f));
 }
 
 int oracle_decode(const or_code* c, const float* llr, int64_t ld, int64_t frames, const or_opts* o,
@@ -420,7 +517,11 @@ int oracle_decode(const or_code* c, const float* llr, int64_t ld, int64_t frames
     for (int64_t f = 0; f < frames; ++f) {
         const float* L = llr + f * ld;
         FrameResult r;
-        if (o->arith == OR_FP32_CONTRACT) {
+        if (o->arith == OR_MINSUM) {
+            std::vector<float> om;
+            r = minsum_frame(c, L, o, xhat, omega ? &om : nullptr, nullptr);
+            if (omega) std::copy(om.begin(), om.end(), omega + f * c->M);
+        } else if (o->arith == OR_FP32_CONTRACT) {
             std::vector<float> S;
             std::vector<uint8_t> neg;
             r = cbp_frame<float>(c, L, o, false, xhat, omega ? &S : nullptr, &neg, nullptr);
@@ -566,4 +667,52 @@ void oracle_phi32_n(const float* x, float* y, int64_t n)
 void oracle_ln32_n(const float* x, float* y, int64_t n)
 {
     for (int64_t i = 0; i < n; ++i) y[i] = oracle_ln32(x[i]);
+}
+
+int oracle_minsum_cbp_trace(const or_code* c, const float* llr, int32_t sweeps, float alpha, float* lam)
+{
+    if (!c || sweeps < 1) return 1;
+    or_opts o = {sweeps, OR_STOP_NONE, OR_MINSUM, alpha};
+    std::vector<uint8_t> xhat;
+    for (int32_t s = 1; s <= sweeps; ++s) {       // prefix re-runs, as oracle_cbp_trace_f64
+        o.max_iter = s;
+        std::vector<float> tmp(c->E);
+        minsum_frame(c, llr, &o, xhat, nullptr, tmp.data());
+        std::copy(tmp.begin(), tmp.end(), lam + (int64_t)(s - 1) * c->E);
+    }
+    return 0;
+}
+
+int oracle_minsum_lbp_trace(const or_code* c, const float* llr, int32_t sweeps, float alpha, float* lam)
+{
+    // Layered normalized min-sum BP: Q = Lambda - R (equ_s2e10); R^new_{c->v} = prod_{others} sgn(Q)
+    // * min_{others} fl(alpha |Q|) (the min-sum form of equ_s2e4, by brute force); Lambda = Q + R^new.
+    if (!c || sweeps < 1) return 1;
+    std::vector<float> Lam(c->N), R(c->E, 0.0f);
+    for (int32_t v = 0; v < c->N; ++v) Lam[v] = llr[v];
+    for (int32_t s = 0; s < sweeps; ++s)
+        for (int32_t ck = 0; ck < c->M; ++ck) {
+            const int32_t b = c->chk_ptr[ck], d = c->chk_ptr[ck + 1] - b;
+            std::vector<float> Qe(d), Rn(d);
+            for (int32_t k = 0; k < d; ++k) {
+                const int32_t v = c->e_var[b + k];
+                lam[(int64_t)s * c->E + b + k] = Lam[v];
+                Qe[k] = Lam[v] - R[b + k];
+            }
+            for (int32_t k = 0; k < d; ++k) {
+                float m = std::numeric_limits<float>::infinity();
+                bool sg = false;
+                for (int32_t k2 = 0; k2 < d; ++k2) {
+                    if (k2 == k) continue;
+                    m = std::fmin(m, alpha * std::fabs(Qe[k2]));
+                    sg = sg != (Qe[k2] < 0.0f);
+                }
+                Rn[k] = sg ? -m : m;
+            }
+            for (int32_t k = 0; k < d; ++k) {
+                Lam[c->e_var[b + k]] = Qe[k] + Rn[k];
+                R[b + k] = Rn[k];
+            }
+        }
+    return 0;
 }

@@ -37,13 +37,14 @@ enum { OR_STOP_BELIEF_M = 0, OR_STOP_BELIEF_N = 1, OR_STOP_SYNDROME = 2, OR_STOP
 /* arithmetic */
 enum { OR_FP32_CONTRACT = 0,   /* fp32, phi from the arithmetic contract (parity reference) */
        OR_FP64 = 1,            /* fp64, phi = log1p(2/expm1(x)) (= -log tanh(x/2)), phi-domain C2B */
-       OR_FP64_LITERAL = 2 };  /* fp64, literal psi+ recursion of equ_s4e5/equ_s4e6 (test variant) */
+       OR_FP64_LITERAL = 2,    /* fp64, literal psi+ recursion of equ_s4e5/equ_s4e6 (test variant) */
+       OR_MINSUM = 3 };        /* fp32 normalized min-sum CBP (equ_s4e18xx / equ_s4e21xx, reading R20) */
 
 typedef struct {
     int32_t max_iter;
     int32_t stop_rule;
     int32_t arith;
-    int32_t reserved;
+    float alpha;               /* normalisation of the min-sum variant (OR_MINSUM only) */
 } or_opts;
 
 /* Decode `frames` LLR vectors (row f at llr + f*ld, N floats).
@@ -87,6 +88,10 @@ int oracle_ber_sim(const or_code* c, double ebn0_db, uint64_t seed, int64_t fram
  * sweep s (CBP: Lambda^new of equ_s4e20; LBP: Lambda_v before processing c). */
 int oracle_cbp_trace_f64(const or_code* c, const float* llr, int32_t sweeps, double* lam);
 int oracle_lbp_trace_f64(const or_code* c, const float* llr, int32_t sweeps, double* lam);
+/* fp32 traces of normalized min-sum CBP and of textbook layered normalized min-sum
+ * BP (leave-one-out minimum by brute force), same layout as above. */
+int oracle_minsum_cbp_trace(const or_code* c, const float* llr, int32_t sweeps, float alpha, float* lam);
+int oracle_minsum_lbp_trace(const or_code* c, const float* llr, int32_t sweeps, float alpha, float* lam);
 
 /* brute-force maximum-likelihood codeword (K <= 20): argmax sum_v L_v (1 - 2 c_v) */
 int oracle_ml_decode(const or_code* c, const float* llr, uint32_t* cw);
