@@ -85,10 +85,17 @@ typedef enum {
     CBP_STOP_NONE = 3       /* always run max_iter sweeps                              */
 } cbp_stop_rule;
 
+/* Check-belief update rules. */
+typedef enum {
+    CBP_ALG_LOG_TANH = 0,   /* phi-domain psi+/psi- (equ_s4e18, equ_s4e21), fp32 arithmetic contract */
+    CBP_ALG_MIN_SUM = 1     /* normalized min-sum (equ_s4e18xx, equ_s4e21xx, reading R20); needs row degree >= 2 */
+} cbp_algorithm;
+
 typedef struct {
     int32_t max_iter;       /* sweeps over all M checks, 1..65535                    */
     int32_t stop_rule;      /* cbp_stop_rule                                         */
-    int32_t reserved[2];    /* must be 0                                             */
+    int32_t algorithm;      /* cbp_algorithm                                         */
+    float alpha;            /* min-sum normalisation in (0, 1] (ignored for log-tanh) */
 } cbp_opts;
 
 /* Decode `frames` channel-LLR vectors (PAPER.md equ_s4e15: L_v = ln Pr(y|0)/Pr(y|1)).

@@ -35,7 +35,15 @@ class _Spec(ctypes.Structure):
 
 
 class _Opts(ctypes.Structure):
-    _fields_ = [("max_iter", _i32), ("stop_rule", _i32), ("reserved", _i32 * 2)]
+    _fields_ = [("max_iter", _i32), ("stop_rule", _i32), ("algorithm", _i32), ("alpha", _f32)]
+
+
+CBP_ALG_LOG_TANH, CBP_ALG_MIN_SUM = 0, 1
+ALPHA_DEFAULT = 0.75
+
+
+def _opts(max_iter, stop_rule, algorithm, alpha):
+    return _Opts(int(max_iter), int(stop_rule), int(algorithm), float(alpha))
 
 
 class LaunchInfo(ctypes.Structure):
@@ -153,11 +161,12 @@ class Code:
         return out
 
     def decode(self, llr: torch.Tensor, max_iter: int, stop_rule: int = CBP_STOP_BELIEF_M, out: dict | None = None,
-               omega: bool = False, ev: bool = False, stream=None) -> dict:
+               omega: bool = False, ev: bool = False, stream=None, algorithm: int = CBP_ALG_LOG_TANH,
+               alpha: float = ALPHA_DEFAULT) -> dict:
         """cbp_decode: llr float32 [frames, ld] on the code's device (ld >= N, ld % 4 == 0)."""
         frames, ld = llr.shape
         out = out if out is not None else self.alloc_outputs(frames, omega, ev)
-        o = _Opts(max_iter, stop_rule, (_i32 * 2)(0, 0))
+        o = _opts(max_iter, stop_rule, algorithm, alpha)
         d = self.device
         rc = lib().cbp_decode(self._h, _dptr(llr, torch.float32, d, "llr"), ld, frames, ctypes.byref(o),
                               _dptr(out["bits"], torch.int32, d, "bits"), out["bits"].shape[1],
@@ -168,11 +177,12 @@ class Code:
         return out
 
     def decode_i8(self, q: torch.Tensor, scale: float, max_iter: int, stop_rule: int = CBP_STOP_BELIEF_M,
-                  out: dict | None = None, omega: bool = False, ev: bool = False, stream=None) -> dict:
+                  out: dict | None = None, omega: bool = False, ev: bool = False, stream=None,
+                  algorithm: int = CBP_ALG_LOG_TANH, alpha: float = ALPHA_DEFAULT) -> dict:
         """cbp_decode_i8: q int8 [frames, ld] (ld % 16 == 0), L = scale * q."""
         frames, ld = q.shape
         out = out if out is not None else self.alloc_outputs(frames, omega, ev)
-        o = _Opts(max_iter, stop_rule, (_i32 * 2)(0, 0))
+        o = _opts(max_iter, stop_rule, algorithm, alpha)
         d = self.device
         rc = lib().cbp_decode_i8(self._h, _dptr(q, torch.int8, d, "q"), ld, scale, frames, ctypes.byref(o),
                                  _dptr(out["bits"], torch.int32, d, "bits"), out["bits"].shape[1],
@@ -199,11 +209,11 @@ class Code:
 
     def ber_sim(self, ebn0_db: float, seed: int, frame_begin: int, frames: int, max_iter: int,
                 stop_rule: int = CBP_STOP_BELIEF_M, llr_mode: int = 0, counts: torch.Tensor | None = None,
-                stream=None) -> torch.Tensor:
+                stream=None, algorithm: int = CBP_ALG_LOG_TANH, alpha: float = ALPHA_DEFAULT) -> torch.Tensor:
         """cbp_ber_sim: accumulates into `counts` (int64 [8] on device; zeroed if not given)."""
         if counts is None:
             counts = torch.zeros(8, dtype=torch.int64, device=self.device)
-        o = _Opts(max_iter, stop_rule, (_i32 * 2)(0, 0))
+        o = _opts(max_iter, stop_rule, algorithm, alpha)
         rc = lib().cbp_ber_sim(self._h, float(ebn0_db), seed, frame_begin, frames, ctypes.byref(o), llr_mode,
                                _dptr(counts, torch.int64, self.device, "counts"), _stream(stream))
         _check(rc, "cbp_ber_sim")

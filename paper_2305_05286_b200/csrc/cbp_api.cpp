@@ -74,15 +74,15 @@ const float4* phi_table(int device, std::string* err)
 
 struct cbp_code {
     int device = 0;
-    int32_t mb = 0, nb = 0, Z = 0, N = 0, K = 0, M = 0, kb = 0, core = 0, mid = 0, nent = 0, max_dc = 0;
+    int32_t mb = 0, nb = 0, Z = 0, N = 0, K = 0, M = 0, kb = 0, core = 0, mid = 0, nent = 0, max_dc = 0, min_dc = 0;
     int64_t E = 0;
     bool can_encode = false;
     int4* d_ent = nullptr;
     int32_t* d_row_ptr = nullptr;
     int16_t* d_pshift = nullptr;
     const float4* phi_tab = nullptr;   // per-device table, not owned
-    cbp::Geometry geo{};
-    int ctas_per_sm = 1, num_sms = 1;
+    cbp::Geometry geo[2]{};           // per cbp_algorithm
+    int ctas_per_sm[2] = {1, 1}, num_sms = 1;
 };
 
 extern "C" {
@@ -153,7 +153,7 @@ cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t 
     }
     const int nent = static_cast<int>(ent_row.size());
     // two int4 per entry b (layout documented in cbp_kernels.cu):
-    //   A = {8 jZ, 4 row(p) Z, 4 bZ, 4 pZ},  B = {8 s, 4 ds, first, jZ}
+    //   A = {8 jZ, 4 row(p) Z, 4 bZ, 4 pZ},  B = {8 s, 4 ds, first | kp << 8, jZ}
     std::vector<int4> ent(2 * static_cast<size_t>(nent));
     for (int j = 0; j < nb; ++j) {
         const auto& L = col_ent[j];
@@ -162,8 +162,11 @@ cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t 
             const int p = L[(k + L.size() - 1) % L.size()];       // previous nonzero row of column j, cyclic
             const int ds = ((ent_s[b] - ent_s[p]) % Z + Z) % Z;
             const int first = (k == 0) ? 1 : 0;                   // R1: no latest check before this visit
+            // kp: position of prev(b) among its row's entries = the variable's edge index inside
+            // the previous check (min-sum minimum owner, reading R20)
+            const int kp = p - row_ptr[ent_row[p]];
             ent[2 * b] = make_int4(8 * j * Z, 4 * ent_row[p] * Z, 4 * b * Z, 4 * p * Z);
-            ent[2 * b + 1] = make_int4(8 * ent_s[b], 4 * ds, first, j * Z);
+            ent[2 * b + 1] = make_int4(8 * ent_s[b], 4 * ds, first | (kp << 8), j * Z);
         }
     }
 
@@ -229,45 +232,52 @@ cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t 
         return cuda_fail(e, "cbp_code_create: cudaMemcpy");
     }
 
-    // ---- launch geometry
-    cbp::Geometry& G = c->geo;
-    const int nwords = (c->N + 31) / 32;
-    if (Z <= 16) {
-        int zp = 1;
-        while (zp < Z) zp <<= 1;
-        G.Zp = zp; G.F = 32 / zp; G.threads = 32; G.multi = 0;
-    } else if (Z <= 32) {
-        G.Zp = 32; G.F = 1; G.threads = 32; G.multi = 0;
-    } else {
-        G.Zp = (Z + 31) / 32 * 32; G.F = 1; G.threads = G.Zp; G.multi = 1;
-    }
-    const int64_t raw = 2LL * c->N + c->E + c->M + nwords;
-    G.slot_words = static_cast<int32_t>(G.F > 1 ? (raw + 31) / 32 * 32 + G.Zp : (raw + 3) / 4 * 4);
-    G.table_words = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4;
-    G.team_threads = G.threads;
+    // ---- launch geometry per algorithm
     int smem_optin = 0, nsm = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-    // teams per CTA: as many independent teams as shared memory, 512 threads and
-    // 15 named barriers allow (they share the staged tables)
-    const int64_t per_team = 4LL * (cbp::kCtlTeamWords + static_cast<int64_t>(G.F) * G.slot_words);
-    const int64_t fixed = 4LL * G.table_words;
-    int nt = static_cast<int>((smem_optin - fixed) / per_team);
-    nt = std::min(nt, std::max(1, 512 / G.team_threads));
-    if (G.multi) nt = std::min(nt, 15);
-    G.state_in_smem = nt >= 1 ? 1 : 0;
-    G.teams = std::max(nt, 1);
-    G.threads = G.teams * G.team_threads;
-    G.smem_bytes = static_cast<int32_t>(G.state_in_smem ? fixed + G.teams * per_team
-                                                        : fixed + 4LL * cbp::kCtlTeamWords * G.teams);
     c->num_sms = nsm > 0 ? nsm : 1;
-    int occ = 0;
-    if (cbp::occupancy_ctas_per_sm(G, &occ) != 0 || occ < 1) {
-        cudaGetLastError();
-        cbp_code_destroy(c);
-        return fail(CBP_E_UNSUPPORTED, "cbp_code_create: kernel does not fit on this device");
+    c->min_dc = *std::min_element(roww.begin(), roww.end());
+    const int nwords = (c->N + 31) / 32;
+    for (int alg = 0; alg < 2; ++alg) {
+        cbp::Geometry& G = c->geo[alg];
+        G.alg = alg;
+        if (Z <= 16) {
+            int zp = 1;
+            while (zp < Z) zp <<= 1;
+            G.Zp = zp; G.F = 32 / zp; G.threads = 32; G.multi = 0;
+        } else if (Z <= 32) {
+            G.Zp = 32; G.F = 1; G.threads = 32; G.multi = 0;
+        } else {
+            G.Zp = (Z + 31) / 32 * 32; G.F = 1; G.threads = G.Zp; G.multi = 1;
+        }
+        // per check: S (log-tanh) or a 16-byte (min, submin, owner|sign, -) record (min-sum)
+        // (slot layout in cbp_kernel: QP, pad to 4 words, S records, R, cw; slots 16-byte aligned;
+        // F > 1 slots are staggered by max(Zp, 4) words across banks)
+        const int64_t raw = (2LL * c->N + 3) / 4 * 4 + c->E + (alg ? 4LL : 1LL) * c->M + nwords;
+        G.slot_words = static_cast<int32_t>(G.F > 1 ? (raw + 31) / 32 * 32 + std::max(G.Zp, 4) : (raw + 3) / 4 * 4);
+        G.table_words = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4;
+        G.team_threads = G.threads;
+        // teams per CTA: as many independent teams as shared memory, 512 threads and
+        // 15 named barriers allow (they share the staged tables)
+        const int64_t per_team = 4LL * (cbp::kCtlTeamWords + static_cast<int64_t>(G.F) * G.slot_words);
+        const int64_t fixed = 4LL * G.table_words;
+        int nt = static_cast<int>((smem_optin - fixed) / per_team);
+        nt = std::min(nt, std::max(1, 512 / G.team_threads));
+        if (G.multi) nt = std::min(nt, 15);
+        G.state_in_smem = nt >= 1 ? 1 : 0;
+        G.teams = std::max(nt, 1);
+        G.threads = G.teams * G.team_threads;
+        G.smem_bytes = static_cast<int32_t>(G.state_in_smem ? fixed + G.teams * per_team
+                                                            : fixed + 4LL * cbp::kCtlTeamWords * G.teams);
+        int occ = 0;
+        if (cbp::occupancy_ctas_per_sm(G, &occ) != 0 || occ < 1) {
+            cudaGetLastError();
+            cbp_code_destroy(c);
+            return fail(CBP_E_UNSUPPORTED, "cbp_code_create: kernel does not fit on this device");
+        }
+        c->ctas_per_sm[alg] = G.state_in_smem ? occ : 1;
     }
-    c->ctas_per_sm = G.state_in_smem ? occ : 1;
     *out = c;
     return CBP_OK;
 }
@@ -285,11 +295,12 @@ cbp_status cbp_code_dims(const cbp_code* c, int32_t* N, int32_t* K, int32_t* M, 
 cbp_status cbp_get_launch_info(const cbp_code* c, cbp_launch_info* o)
 {
     if (!c || !o) return fail(CBP_E_INVALID, "cbp_get_launch_info: null argument");
-    o->threads = c->geo.threads;
-    o->ctas_per_sm = c->ctas_per_sm;
-    o->frames_per_cta = c->geo.F * c->geo.teams;
-    o->smem_bytes = c->geo.smem_bytes;
-    o->state_in_smem = c->geo.state_in_smem;
+    const cbp::Geometry& G = c->geo[0];     // log-tanh geometry (min-sum: same teams, larger slots)
+    o->threads = G.threads;
+    o->ctas_per_sm = c->ctas_per_sm[0];
+    o->frames_per_cta = G.F * G.teams;
+    o->smem_bytes = G.smem_bytes;
+    o->state_in_smem = G.state_in_smem;
     o->num_sms = c->num_sms;
     return CBP_OK;
 }
@@ -298,28 +309,35 @@ cbp_status cbp_get_launch_info(const cbp_code* c, cbp_launch_info* o)
 
 namespace {
 
-cbp::KernelArgs base_args(const cbp_code* c)
+cbp::KernelArgs base_args(const cbp_code* c, int alg = 0)
 {
     cbp::KernelArgs a{};
     cbp::DevCode& d = a.code;
+    const cbp::Geometry& G = c->geo[alg];
     d.N = c->N; d.K = c->K; d.M = c->M; d.Z = c->Z; d.mb = c->mb; d.nb = c->nb; d.kb = c->kb; d.core = c->core;
     d.nent = c->nent; d.E = static_cast<int32_t>(c->E); d.nwords = (c->N + 31) / 32; d.kwords = (c->K + 31) / 32;
     d.max_dc = c->max_dc; d.can_encode = c->can_encode; d.mid = c->mid;
     d.ent = c->d_ent; d.row_ptr = c->d_row_ptr; d.pshift = c->d_pshift; d.phi_tab = c->phi_tab;
-    a.Zp = c->geo.Zp; a.F = c->geo.F; a.slot_words = c->geo.slot_words; a.table_words = c->geo.table_words;
-    a.team_threads = c->geo.team_threads;
+    a.Zp = G.Zp; a.F = G.F; a.slot_words = G.slot_words; a.table_words = G.table_words;
+    a.team_threads = G.team_threads;
     a.phi_m19 = 0x7ffffu;
     a.phi_one = 0x3f800000u;
     a.max_iter = 1; a.stop_rule = 0;
+    a.alpha = 1.0f;
     return a;
 }
 
-cbp_status check_opts(const cbp_opts* o)
+cbp_status check_opts(const cbp_code* c, const cbp_opts* o)
 {
     if (!o) return fail(CBP_E_INVALID, "null opts");
     if (o->max_iter < 1 || o->max_iter > 65535) return fail(CBP_E_INVALID, "opts.max_iter must be in [1, 65535]");
     if (o->stop_rule < 0 || o->stop_rule > 3) return fail(CBP_E_INVALID, "opts.stop_rule must be in [0, 3]");
-    if (o->reserved[0] || o->reserved[1]) return fail(CBP_E_INVALID, "opts.reserved must be 0");
+    if (o->algorithm != CBP_ALG_LOG_TANH && o->algorithm != CBP_ALG_MIN_SUM)
+        return fail(CBP_E_INVALID, "opts.algorithm must be CBP_ALG_LOG_TANH or CBP_ALG_MIN_SUM");
+    if (o->algorithm == CBP_ALG_MIN_SUM) {
+        if (!(o->alpha > 0.0f && o->alpha <= 1.0f)) return fail(CBP_E_INVALID, "opts.alpha must be in (0, 1]");
+        if (c->min_dc < 2) return fail(CBP_E_UNSUPPORTED, "min-sum needs every base row degree >= 2");
+    }
     return CBP_OK;
 }
 
@@ -329,16 +347,18 @@ cbp_status run(const cbp_code* c, cbp::KernelArgs& a, int64_t frames, void* stre
     DeviceGuard g(c->device);
     if (!g.ok) return fail(CBP_E_CUDA, std::string(who) + ": cudaSetDevice failed");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int64_t per_cta = static_cast<int64_t>(c->geo.F) * c->geo.teams;
+    const cbp::Geometry& G = c->geo[a.algorithm];
+    const int64_t per_cta = static_cast<int64_t>(G.F) * G.teams;
     const int64_t ctas_needed = (frames + per_cta - 1) / per_cta;
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(c->num_sms) * c->ctas_per_sm, ctas_needed)));
+    const int grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(static_cast<int64_t>(c->num_sms) * c->ctas_per_sm[a.algorithm], ctas_needed)));
     cudaError_t e;
     unsigned long long* q = nullptr;
     if ((e = cudaMallocAsync(reinterpret_cast<void**>(&q), sizeof(unsigned long long), st)) != cudaSuccess)
         return fail(CBP_E_NOMEM, std::string(who) + ": " + cudaGetErrorString(e));
     float* gs = nullptr;
-    if (!c->geo.state_in_smem) {
-        const size_t bytes = sizeof(float) * static_cast<size_t>(grid) * per_cta * c->geo.slot_words;
+    if (!G.state_in_smem) {
+        const size_t bytes = sizeof(float) * static_cast<size_t>(grid) * per_cta * G.slot_words;
         if ((e = cudaMallocAsync(reinterpret_cast<void**>(&gs), bytes, st)) != cudaSuccess) {
             cudaFreeAsync(q, st);
             return fail(CBP_E_NOMEM, std::string(who) + ": " + cudaGetErrorString(e));
@@ -347,7 +367,7 @@ cbp_status run(const cbp_code* c, cbp::KernelArgs& a, int64_t frames, void* stre
     a.queue = q;
     a.gstate = gs;
     e = cudaMemsetAsync(q, 0, sizeof(unsigned long long), st);
-    int le = (e == cudaSuccess) ? cbp::launch_cbp(a, c->geo, grid, stream) : static_cast<int>(e);
+    int le = (e == cudaSuccess) ? cbp::launch_cbp(a, G, grid, stream) : static_cast<int>(e);
     cudaFreeAsync(q, st);
     if (gs) cudaFreeAsync(gs, st);
     if (le != 0) return cuda_fail(static_cast<cudaError_t>(le), who);
@@ -368,7 +388,7 @@ cbp_status decode_common(const cbp_code* c, const void* in, int32_t mode, int64_
                          float* d_omega, int64_t* d_ev, void* stream, const char* who)
 {
     if (!c) return fail(CBP_E_INVALID, std::string(who) + ": null code");
-    cbp_status s = check_opts(opts);
+    cbp_status s = check_opts(c, opts);
     if (s != CBP_OK) return s;
     if (frames < 0) return fail(CBP_E_INVALID, std::string(who) + ": frames < 0");
     if (frames == 0) return CBP_OK;
@@ -379,10 +399,12 @@ cbp_status decode_common(const cbp_code* c, const void* in, int32_t mode, int64_
     if (ld_words < (c->N + 31) / 32) return fail(CBP_E_INVALID, std::string(who) + ": ld_words < ceil(N/32)");
     if (mode == cbp::MODE_DECODE_I8 && !(std::isfinite(scale) && scale > 0.0f))
         return fail(CBP_E_INVALID, std::string(who) + ": scale must be finite and > 0");
-    cbp::KernelArgs a = base_args(c);
+    cbp::KernelArgs a = base_args(c, opts->algorithm);
     a.mode = mode;
     a.max_iter = opts->max_iter;
     a.stop_rule = opts->stop_rule;
+    a.algorithm = opts->algorithm;
+    a.alpha = opts->alpha;
     a.llr = static_cast<const float*>(in);
     a.q = static_cast<const int8_t*>(in);
     a.ld = ld;
@@ -448,17 +470,19 @@ cbp_status cbp_ber_sim(const cbp_code* c, double ebn0_db, uint64_t seed, int64_t
 {
     if (!c) return fail(CBP_E_INVALID, "cbp_ber_sim: null code");
     if (!c->can_encode) return fail(CBP_E_UNSUPPORTED, "cbp_ber_sim: base has no dual-diagonal encoder structure");
-    cbp_status s = check_opts(opts);
+    cbp_status s = check_opts(c, opts);
     if (s != CBP_OK) return s;
     if (frames < 0 || frame_begin < 0) return fail(CBP_E_INVALID, "cbp_ber_sim: negative frame range");
     if (llr_mode != 0 && llr_mode != 1) return fail(CBP_E_INVALID, "cbp_ber_sim: llr_mode must be 0 or 1");
     if (!std::isfinite(ebn0_db)) return fail(CBP_E_INVALID, "cbp_ber_sim: ebn0_db not finite");
     if (!d_counts) return fail(CBP_E_INVALID, "cbp_ber_sim: null counts");
     if (frames == 0) return CBP_OK;
-    cbp::KernelArgs a = base_args(c);
+    cbp::KernelArgs a = base_args(c, opts->algorithm);
     a.mode = cbp::MODE_BER_SIM;
     a.max_iter = opts->max_iter;
     a.stop_rule = opts->stop_rule;
+    a.algorithm = opts->algorithm;
+    a.alpha = opts->alpha;
     a.frames = frames;
     a.frame_begin = frame_begin;
     a.seed = seed;

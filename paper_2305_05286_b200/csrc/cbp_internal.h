@@ -31,6 +31,8 @@ struct KernelArgs {
     DevCode code;
     int32_t mode;
     int32_t max_iter, stop_rule;
+    int32_t algorithm;     // 0 log-tanh, 1 normalized min-sum
+    float alpha;           // min-sum normalisation
     int32_t llr_mode;
     // inputs
     const float* llr;
@@ -63,6 +65,7 @@ constexpr int kCtlTeamWords = 72;   // shared control words per team: 2 x 32 bal
 struct Geometry {
     int32_t threads, F, Zp, slot_words, table_words, smem_bytes, state_in_smem, multi;
     int32_t team_threads, teams;   // threads per team, teams per CTA
+    int32_t alg;                   // cbp_algorithm of this geometry
 };
 
 // launch (cbp_kernels.cu); returns cudaError_t as int

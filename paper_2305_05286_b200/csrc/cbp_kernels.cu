@@ -155,7 +155,7 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
         aqp[u] = A.x + t8;
         aw[u] = A.w + rp4;
         ar[u] = A.z + L.r4;
-        fst[u] = SWEEP1 && B.z != 0;
+        fst[u] = SWEEP1 && (B.z & 1) != 0;
         const float2 qp = ld2(s.qp, aqp[u]);
         q[u] = qp.x;
         p[u] = qp.y;
@@ -194,8 +194,9 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
     }
 }
 
+// check record of the row (log-tanh: S in .x; min-sum: the 16-byte record) before / after
 struct RowOut {
-    float Snew, Sold;
+    float4 Snew, Sold;
     uint32_t oldbits;
     bool ok;
 };
@@ -212,10 +213,103 @@ __device__ __forceinline__ RowOut process_row(const int4* __restrict__ ent, cons
     const float Snew = __uint_as_float(__float_as_uint(acc.Ssum) | (acc.negw & kSign));
     st1(s.S, sidx4, Snew);                                   // equ_s4e23
     RowOut o;
+    o.Snew.x = Snew;
+    o.Sold.x = Sold;
+    o.oldbits = acc.oldbits;
+    o.ok = ((acc.negw | acc.flipw) & kSign) == 0u;           // equ_s4e2 and equ_s4e24 for this check
+    return o;
+}
+
+// ---------------------------------------------------------------- normalized min-sum CBP
+// PAPER.md l.577-603 (equ_s4e18xx, equ_s4e21xx) with reading R20: per check a 16-byte
+// record {min, submin, owner | sign << 31, -} of m = fl(alpha |Q^new|); B2V magnitude =
+// submin if v owns the minimum (owner = v's edge index in the check) else min; signs as
+// psi- (equ_s4e13).  Schedule, V2C, commit and stop rule are those of the log-tanh path.
+struct MsAcc {
+    float m1, m2;
+    uint32_t own, negw, flipw, oldbits;
+};
+
+__device__ __forceinline__ float4 ld4(const char* b, int off) { return *reinterpret_cast<const float4*>(b + off); }
+__device__ __forceinline__ void st4(char* b, int off, float4 v) { *reinterpret_cast<float4*>(b + off) = v; }
+
+template <int U, bool SWEEP1, bool TRACK>
+__device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int e0, int k0, const Lane& L,
+                                              const SlotPtrs& s, float alpha, MsAcc& acc)
+{
+    int aqp[U], aw[U], ar[U], kp[U];
+    float q[U], p[U], Rn[U];
+    float4 cs[U];
+    bool fst[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int4 A = ent[2 * (e0 + k0 + u)];
+        const int4 B = ent[2 * (e0 + k0 + u) + 1];
+        int t8 = L.r8 + B.x;
+        t8 = (t8 >= L.Z8) ? t8 - L.Z8 : t8;
+        int rp4 = L.r4 + B.y;
+        rp4 = (rp4 >= L.Z4) ? rp4 - L.Z4 : rp4;
+        CBP_CHECK(4 * (A.y + rp4) + 16 <= 4 * L.S_bytes);
+        aqp[u] = A.x + t8;
+        aw[u] = A.w + rp4;
+        ar[u] = A.z + L.r4;
+        fst[u] = SWEEP1 && (B.z & 1) != 0;
+        kp[u] = B.z >> 8;
+        const float2 qp = ld2(s.qp, aqp[u]);
+        q[u] = qp.x;
+        p[u] = qp.y;
+        cs[u] = ld4(s.S, 4 * (A.y + rp4));                   // record of the previous check c_j
+    }
+    // B2V (equ_s4e18xx)
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint32_t ow = __float_as_uint(cs[u].z);
+        const float mag = (static_cast<int>(ow & 0xffu) == kp[u]) ? cs[u].y : cs[u].x;
+        Rn[u] = __uint_as_float(__float_as_uint(mag) | ((ow ^ __float_as_uint(q[u])) & kSign));
+        if (SWEEP1 && fst[u]) Rn[u] = 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (!(SWEEP1 && fst[u])) st1(s.R, aw[u], Rn[u]);   // commit of R_{cj->v} (R2, R3)
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const float ro = ld1(s.R, ar[u]);
+        const float lam = __fadd_rn(q[u], Rn[u]);            // equ_s4e20
+        const float qn = __fsub_rn(lam, ro);                 // equ_s4e19
+        const uint32_t lb = __float_as_uint(lam) & kSign;
+        acc.flipw |= __float_as_uint(lam) ^ __float_as_uint(p[u]);
+        if (TRACK) acc.oldbits |= (__float_as_uint(p[u]) >> 31) << (k0 + u);
+        // C2B (equ_s4e21xx), in ascending edge order
+        const float m = __fmul_rn(alpha, fabsf(qn));
+        if (m < acc.m1) {
+            acc.m2 = acc.m1;
+            acc.m1 = m;
+            acc.own = static_cast<uint32_t>(k0 + u);
+        } else if (m < acc.m2) {
+            acc.m2 = m;
+        }
+        acc.negw ^= __float_as_uint(qn);
+        st2(s.qp, aqp[u], make_float2(qn, __uint_as_float(lb)));
+    }
+}
+
+template <bool SWEEP1, bool TRACK>
+__device__ __forceinline__ RowOut process_row_ms(const int4* __restrict__ ent, int e0, int dc, int sidx4, const Lane& L,
+                                                 const SlotPtrs& s, float alpha)
+{
+    const float inf = __uint_as_float(0x7f800000u);
+    MsAcc acc{inf, inf, 0u, 0u, 0u, 0u};                    // Omega^(-1) = (inf, inf)
+    const float4 Sold = ld4(s.S, 4 * sidx4);
+    int k0 = 0;
+    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) edge_chunk_ms<CBP_CHUNK, SWEEP1, TRACK>(ent, e0, k0, L, s, alpha, acc);
+    for (; k0 < dc; ++k0) edge_chunk_ms<1, SWEEP1, TRACK>(ent, e0, k0, L, s, alpha, acc);
+    const float4 Snew = make_float4(acc.m1, acc.m2, __uint_as_float(acc.own | (acc.negw & kSign)), 0.0f);
+    st4(s.S, 4 * sidx4, Snew);
+    RowOut o;
     o.Snew = Snew;
     o.Sold = Sold;
     o.oldbits = acc.oldbits;
-    o.ok = ((acc.negw | acc.flipw) & kSign) == 0u;           // equ_s4e2 and equ_s4e24 for this check
+    o.ok = ((acc.negw | acc.flipw) & kSign) == 0u;
     return o;
 }
 
@@ -263,7 +357,8 @@ __device__ __forceinline__ uint32_t info_parity(const int4* __restrict__ ent, co
 // ---------------------------------------------------------------- channel (a2-a4)
 template <bool MULTI>
 __device__ void channel_frame(const KernelArgs& a, const Team<MULTI>& tm, bool fresh, int64_t gframe,
-                              const int4* ent, const int32_t* row_ptr, const int16_t* pshift, const SlotPtrs& s)
+                              const int4* ent, const int32_t* row_ptr, const int16_t* pshift, const SlotPtrs& s,
+                              int s_words)
 {
     const DevCode& C = a.code;
     const int Z = C.Z, r = tm.r;
@@ -357,13 +452,13 @@ __device__ void channel_frame(const KernelArgs& a, const Team<MULTI>& tm, bool f
             }
         }
         for (int e = r; e < C.E; e += Z) s.Rf()[e] = 0.0f;
-        for (int c = r; c < C.M; c += Z) s.Sf()[c] = 0.0f;
+        for (int c = r; c < s_words; c += Z) s.Sf()[c] = 0.0f;
     }
     tm.sync();
 }
 
 // ---------------------------------------------------------------- the kernel
-template <bool MULTI, bool SMEM, int MAXT>
+template <bool MULTI, bool SMEM, int MAXT, int ALG>
 __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
 {
     extern __shared__ __align__(16) uint32_t smem[];
@@ -396,7 +491,8 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
     }
     tm.lane_on = tm.r < Z && tm.slot < a.F;
     const int r = tm.r;
-    const Lane lane{r, 4 * r, 8 * r, Z, 4 * Z, 8 * Z, 8 * C.N, 4 * C.E, 4 * C.M, a.phi_m19, a.phi_one};
+    const int s_words = ALG ? 4 * C.M : C.M;               // words of the per-check records
+    const Lane lane{r, 4 * r, 8 * r, Z, 4 * Z, 8 * Z, 8 * C.N, 4 * C.E, 4 * s_words, a.phi_m19, a.phi_one};
     uint32_t* ctl = smem + a.table_words + tm.tidx * kCtlTeamWords;
     long long* ctl64 = reinterpret_cast<long long*>(ctl + 64);
 
@@ -405,11 +501,17 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
                         : a.gstate + static_cast<size_t>(blockIdx.x) * nteams * a.F * a.slot_words;
     SlotPtrs s;
     float* slot0 = sbase + static_cast<size_t>(tm.tidx * a.F + (tm.slot < a.F ? tm.slot : 0)) * a.slot_words;
+    // slot layout (word offsets; slot_words % 4 == 0): QP [2N] | pad to 4 | S [s_words] | R [E] | cw
+    const int s_off = (2 * C.N + 3) & ~3;                  // 16-byte aligned check records
     s.qp = reinterpret_cast<char*>(slot0);
-    s.R = reinterpret_cast<char*>(slot0 + 2 * C.N);
-    s.S = reinterpret_cast<char*>(slot0 + 2 * C.N + C.E);
-    s.cw = reinterpret_cast<uint32_t*>(slot0 + 2 * C.N + C.E + C.M);
+    s.S = reinterpret_cast<char*>(slot0 + s_off);
+    s.R = reinterpret_cast<char*>(slot0 + s_off + s_words);
+    s.cw = reinterpret_cast<uint32_t*>(slot0 + s_off + s_words + C.E);
     __syncthreads();
+    auto put_check = [&](const SlotPtrs& sp, int c, float4 v) {
+        if constexpr (ALG == 1) st4(sp.S, 16 * c, v);
+        else st1(sp.S, 4 * c, v.x);
+    };
 
     const bool belief = a.stop_rule <= 1;
     const int W = (a.stop_rule == 1) ? C.N : C.M;            // R4 (N, M < 65536)
@@ -453,7 +555,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
         // ---- Step 1: initialisation (a4/a5)
         if (a.mode == MODE_BER_SIM || a.mode == MODE_CHANNEL) {
             if (tm.team_any(fresh))
-                channel_frame<MULTI>(a, tm, fresh, a.frame_begin + fidx, ent, row_ptr, pshift, s);
+                channel_frame<MULTI>(a, tm, fresh, a.frame_begin + fidx, ent, row_ptr, pshift, s, s_words);
         } else {
             if (fresh && tm.lane_on) {
                 const size_t base = static_cast<size_t>(fidx) * a.ld;
@@ -463,7 +565,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
                     s.QP()[v] = make_float2(Lv, Lv < 0.0f ? -0.0f : 0.0f);   // equ_s4e15, hard bit from L (R7)
                 }
                 for (int e = r; e < C.E; e += Z) s.Rf()[e] = 0.0f;   // equ_s4e17
-                for (int c = r; c < C.M; c += Z) s.Sf()[c] = 0.0f;   // equ_s4e16: Omega = inf <=> S = 0
+                for (int c = r; c < s_words; c += Z) s.Sf()[c] = 0.0f;   // equ_s4e16: Omega = inf <=> S = 0
             }
             tm.sync();
         }
@@ -479,18 +581,26 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
                 RowOut ro;
                 ro.ok = true;
                 ro.oldbits = 0;
-                ro.Snew = ro.Sold = 0.0f;
+                ro.Snew = ro.Sold = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                 if (live && tm.lane_on) {
                     // the window can only fill in this row if consec + Z >= W (R4); otherwise
                     // no rollback information is needed
                     const bool track = belief && consec + Z >= W;
                     const int sidx4 = 4 * (i * Z + r);
                     if (sweep == 1) {
-                        ro = track ? process_row<true, true>(ent, ptab, e0, dc, sidx4, lane, s)
-                                   : process_row<true, false>(ent, ptab, e0, dc, sidx4, lane, s);
+                        if constexpr (ALG == 1)
+                            ro = track ? process_row_ms<true, true>(ent, e0, dc, sidx4, lane, s, a.alpha)
+                                       : process_row_ms<true, false>(ent, e0, dc, sidx4, lane, s, a.alpha);
+                        else
+                            ro = track ? process_row<true, true>(ent, ptab, e0, dc, sidx4, lane, s)
+                                       : process_row<true, false>(ent, ptab, e0, dc, sidx4, lane, s);
                     } else {
-                        ro = track ? process_row<false, true>(ent, ptab, e0, dc, sidx4, lane, s)
-                                   : process_row<false, false>(ent, ptab, e0, dc, sidx4, lane, s);
+                        if constexpr (ALG == 1)
+                            ro = track ? process_row_ms<false, true>(ent, e0, dc, sidx4, lane, s, a.alpha)
+                                       : process_row_ms<false, false>(ent, e0, dc, sidx4, lane, s, a.alpha);
+                        else
+                            ro = track ? process_row<false, true>(ent, ptab, e0, dc, sidx4, lane, s)
+                                       : process_row<false, false>(ent, ptab, e0, dc, sidx4, lane, s);
                     }
                 }
                 // ---- Step 2(3): stopping criterion, counted per check update (R4, R5)
@@ -533,7 +643,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
                     uint32_t newbits = 0;
                     if (back) {
                         newbits = swap_row_bits(ent, e0, dc, r, Z, ro.oldbits, s);
-                        st1(s.S, 4 * (i * Z + r), ro.Sold);
+                        put_check(s, i * Z + r, ro.Sold);
                     }
                     tm.sync();
                     const bool nz = tm.slot_any(fire && tm.lane_on && lane_syndrome(ent, row_ptr, mb, r, Z, s));
@@ -547,7 +657,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
                             consec = Z - 1 - max(last_bad, rstar);
                             if (back) {
                                 swap_row_bits(ent, e0, dc, r, Z, newbits, s);
-                                st1(s.S, 4 * (i * Z + r), ro.Snew);
+                                put_check(s, i * Z + r, ro.Snew);
                             }
                         }
                     }
@@ -594,8 +704,15 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
                     if (a.omega) {
                         float* om = a.omega + static_cast<size_t>(fidx) * C.M;
                         for (int c = r; c < C.M; c += Z) {
-                            const float Sv = s.Sf()[c];
-                            const float m = phi32(fabsf(Sv), ptab);
+                            float Sv, m;
+                            if constexpr (ALG == 1) {
+                                const float4 cs = reinterpret_cast<const float4*>(s.S)[c];
+                                Sv = cs.z;                               // sign bit = sign of Omega
+                                m = cs.x;                                // Omega = sgn * min (reading R20)
+                            } else {
+                                Sv = s.Sf()[c];
+                                m = phi32(fabsf(Sv), ptab);               // Omega = sgn * phi(S)
+                            }
                             om[c] = (__float_as_uint(Sv) >> 31) ? -m : m;
                         }
                     }
@@ -710,7 +827,7 @@ int launch_phi_table(float4* out, void* stream)
 template <bool MULTI, bool SMEM, int MAXT>
 static int launch_t(const KernelArgs& a, const Geometry& g, int grid, cudaStream_t st)
 {
-    auto k = cbp_kernel<MULTI, SMEM, MAXT>;
+    auto k = (g.alg == 1) ? cbp_kernel<MULTI, SMEM, MAXT, 1> : cbp_kernel<MULTI, SMEM, MAXT, 0>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
     k<<<grid, g.threads, g.smem_bytes, st>>>(a);
@@ -720,7 +837,7 @@ static int launch_t(const KernelArgs& a, const Geometry& g, int grid, cudaStream
 template <bool MULTI, bool SMEM, int MAXT>
 static int occ_t(const Geometry& g, int* out)
 {
-    auto k = cbp_kernel<MULTI, SMEM, MAXT>;
+    auto k = (g.alg == 1) ? cbp_kernel<MULTI, SMEM, MAXT, 1> : cbp_kernel<MULTI, SMEM, MAXT, 0>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
     return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, g.threads, g.smem_bytes));

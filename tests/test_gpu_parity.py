@@ -32,12 +32,12 @@ def codes():
     return get
 
 
-def gpu_decode(g, llr_np, max_iter, rule=0, ld=None):
+def gpu_decode(g, llr_np, max_iter, rule=0, ld=None, **alg):
     F, N = llr_np.shape
     ld = ld or (N + 3) // 4 * 4
     x = torch.zeros((F, ld), dtype=torch.float32)
     x[:, :N] = torch.from_numpy(llr_np)
-    out = g.decode(x.cuda(), max_iter, rule, omega=True, ev=True)
+    out = g.decode(x.cuda(), max_iter, rule, omega=True, ev=True, **alg)
     torch.cuda.synchronize()
     return {k: v.cpu().numpy() for k, v in out.items()}
 
@@ -242,3 +242,79 @@ def test_c4_ber_sim_parity(codes):
     want = o.ber_sim(2.0, 5, 0, 6, 25, stop_rule=oracle.STOP_SYNDROME)
     got = g.ber_sim(2.0, 5, 0, 6, 25, stop_rule=oracle.STOP_SYNDROME).cpu().numpy()
     assert list(got) == list(want)
+
+
+# ---------------------------------------------------------------- NEXT-1: normalized min-sum CBP
+MS = dict(algorithm=1)
+
+
+@pytest.mark.parametrize("name,ebn0,frames,alpha", [("C1", 2.0, 3000, 0.75), ("C2", 2.0, 1000, 0.75),
+                                                    ("C2", 1.5, 500, 1.0), ("C2", 3.0, 500, 0.625),
+                                                    ("C3a", 2.0, 150, 0.75), ("C3b", 3.5, 150, 0.8),
+                                                    ("T24", 4.0, 1000, 0.75)])
+def test_minsum_decode_parity(codes, name, ebn0, frames, alpha):
+    """Normalized min-sum CBP (reading R20) on the GPU equals
+    the oracle's min-sum CBP bit for bit, Omega = sgn * min included."""
+    g, o = codes(name)
+    mi = inputs.CONFIGS[name].max_iter
+    llr, _ = o.channel(ebn0, seed=31, frame_begin=0, frames=frames)
+    oo = o.decode(llr, mi, want_omega=True, arith=oracle.MINSUM, alpha=alpha)
+    go = gpu_decode(g, llr, mi, alpha=alpha, **MS)
+    assert_same(go, oo, o.N, omega=False)
+    assert (go["omega"].view(np.uint32) == oo["omega"].view(np.uint32)).all()
+
+
+@pytest.mark.parametrize("rule", [oracle.STOP_BELIEF_M, oracle.STOP_BELIEF_N, oracle.STOP_SYNDROME, oracle.STOP_NONE])
+def test_minsum_stop_rules_and_extremes(codes, rule):
+    g, o = codes("C2")
+    llr = inputs.random_llr(o.N, 200, 2.5, seed=9)
+    llr[0] = 0.0
+    llr[1] = 1e30
+    llr[2, ::3] = np.float32(-0.0)
+    llr[3] = np.where(np.arange(o.N) % 2 == 0, 4.0, -4.0)      # many equal magnitudes: owner ties
+    for mi in (1, 7):
+        oo = o.decode(llr, mi, rule, oracle.MINSUM, want_omega=True, alpha=0.75)
+        go = gpu_decode(g, llr, mi, rule, alpha=0.75, **MS)
+        assert_same(go, oo, o.N, omega=False)
+        assert (go["omega"].view(np.uint32) == oo["omega"].view(np.uint32)).all()
+
+
+def test_minsum_multi_warp_team_and_global_state(codes):
+    """Z > 32 (multi-warp teams) and Z = 384 with the state in global memory."""
+    g, o = codes("C4")
+    llr, _ = o.channel(1.5, seed=13, frame_begin=0, frames=4)
+    oo = o.decode(llr, 20, oracle.STOP_SYNDROME, oracle.MINSUM, want_omega=True, alpha=0.75)
+    assert_same(gpu_decode(g, llr, 20, oracle.STOP_SYNDROME, alpha=0.75, **MS), oo, o.N, omega=False)
+    base = inputs.construct_base((6, 18, 96, 6, 1, 2, 4), 2)
+    g2, o2 = cbp.Code(base, 96), oracle.OracleCode(base, 96)
+    llr, _ = o2.channel(2.0, seed=14, frame_begin=0, frames=60)
+    for rule in (0, 2):
+        oo = o2.decode(llr, 15, rule, oracle.MINSUM, want_omega=True, alpha=0.75)
+        assert_same(gpu_decode(g2, llr, 15, rule, alpha=0.75, **MS), oo, o2.N)
+
+
+@pytest.mark.parametrize("name,ebn0,frames,llr_mode", [("C2", 2.0, 2000, 0), ("C2", 2.5, 1000, 1),
+                                                       ("C3a", 2.5, 150, 0)])
+def test_minsum_ber_sim_parity(codes, name, ebn0, frames, llr_mode):
+    g, o = codes(name)
+    mi = inputs.CONFIGS[name].max_iter
+    want = o.ber_sim(ebn0, 23, 500, frames, mi, llr_mode=llr_mode, arith=oracle.MINSUM, alpha=0.75)
+    got = g.ber_sim(ebn0, 23, 500, frames, mi, llr_mode=llr_mode, alpha=0.75, **MS).cpu().numpy()
+    assert list(got) == list(want), dict(zip(oracle.COUNT_NAMES, zip(got, want)))
+
+
+def test_minsum_rejects_bad_options(codes):
+    g, o = codes("C2")
+    x = torch.zeros((2, 648), dtype=torch.float32, device="cuda")
+    for a in (0.0, -0.5, 1.5, float("nan")):
+        with pytest.raises(RuntimeError):
+            g.decode(x, 5, alpha=a, **MS)
+    with pytest.raises(RuntimeError):
+        g.decode(x, 5, algorithm=7)
+    # a degree-1 check row has no leave-one-out minimum: min-sum is refused, log-tanh decodes
+    base = np.array([[0, 1, -1, 2], [-1, 2, 0, -1], [-1, -1, 3, -1]], np.int16)   # last base row: degree 1
+    g1 = cbp.Code(base, 8)
+    y = torch.zeros((2, 32), dtype=torch.float32, device="cuda")
+    g1.decode(y, 5)
+    with pytest.raises(RuntimeError):
+        g1.decode(y, 5, **MS)

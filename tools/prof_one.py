@@ -23,7 +23,10 @@ ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--warm", type=float, default=1.0, help="seconds of warm-up (0 under ncu)")
 ap.add_argument("--mode", default="ber", choices=["ber", "decode"])
 ap.add_argument("--rule", type=int, default=0)
+ap.add_argument("--alg", type=int, default=0, help="0 log-tanh, 1 normalized min-sum")
+ap.add_argument("--alpha", type=float, default=0.75)
 a = ap.parse_args()
+ALG = dict(algorithm=a.alg, alpha=a.alpha)
 cfg = inputs.CONFIGS[a.config]
 base, Z = inputs.config_base(a.config)
 g = cbp.Code(base, Z)
@@ -34,16 +37,16 @@ g.ber_sim(a.ebn0, 1, 0, 4096, cfg.max_iter)
 torch.cuda.synchronize()
 t_end = time.perf_counter() + a.warm
 while time.perf_counter() < t_end:
-    g.ber_sim(a.ebn0, 1, 0, a.frames, cfg.max_iter, stop_rule=a.rule)
+    g.ber_sim(a.ebn0, 1, 0, a.frames, cfg.max_iter, stop_rule=a.rule, **ALG)
     torch.cuda.synchronize()
 best = None
 for _ in range(a.reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     if a.mode == "ber":
-        c = g.ber_sim(a.ebn0, 1, 0, a.frames, cfg.max_iter, stop_rule=a.rule)
+        c = g.ber_sim(a.ebn0, 1, 0, a.frames, cfg.max_iter, stop_rule=a.rule, **ALG)
     else:
-        out = g.decode(llr, cfg.max_iter, a.rule, ev=True)
+        out = g.decode(llr, cfg.max_iter, a.rule, ev=True, **ALG)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
