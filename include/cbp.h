@@ -72,6 +72,19 @@ cbp_status cbp_construct_base(const cbp_construct_spec* spec, uint64_t seed, int
 typedef struct cbp_code cbp_code;
 cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t Z, int32_t device, cbp_code** out);
 void       cbp_code_destroy(cbp_code* code);
+/* Optional build settings of a code handle (cbp_code_create_ex).
+ *   frames_per_lane: 0 = automatic (default), 1 or 2.  With 2, every lane of a frame
+ *   group decodes its lifted check for two frames at once (interleaved state,
+ *   DESIGN.md §5); results are identical for every setting -- it is a performance
+ *   choice only.  2 needs the per-frame state in shared memory and teams of at most
+ *   256 threads (Z <= 256), else CBP_E_UNSUPPORTED.  With 0 the environment variable
+ *   CBP_FRAMES_PER_LANE=1|2 (A/B measurements) overrides the automatic choice. */
+typedef struct {
+    int32_t frames_per_lane;
+} cbp_code_config;
+/* cbp_code_create with settings; cfg == NULL is cbp_code_create. */
+cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32_t Z, int32_t device,
+                              const cbp_code_config* cfg, cbp_code** out);
 /* any output pointer may be NULL */
 cbp_status cbp_code_dims(const cbp_code* code, int32_t* N, int32_t* K, int32_t* M, int64_t* E);
 
@@ -151,10 +164,11 @@ cbp_status cbp_ber_sim(const cbp_code* code, double ebn0_db, uint64_t seed, int6
 
 /* ----------------------------------------------------------- introspection */
 
-/* Launch geometry the library picks for this code (for reports): threads per
- * CTA, CTAs per SM, frames per CTA, dynamic smem bytes, state in smem (1) or global (0). */
+/* Launch geometry the library picks for this code's log-tanh decoder (for reports):
+ * threads per CTA, CTAs per SM, frames per CTA, dynamic smem bytes, state in smem (1)
+ * or global (0), SMs, frames per lane (1 or 2). */
 typedef struct {
-    int32_t threads, ctas_per_sm, frames_per_cta, smem_bytes, state_in_smem, num_sms;
+    int32_t threads, ctas_per_sm, frames_per_cta, smem_bytes, state_in_smem, num_sms, frames_per_lane;
 } cbp_launch_info;
 cbp_status cbp_get_launch_info(const cbp_code* code, cbp_launch_info* out);
 

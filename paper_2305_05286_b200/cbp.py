@@ -48,7 +48,11 @@ def _opts(max_iter, stop_rule, algorithm, alpha):
 
 class LaunchInfo(ctypes.Structure):
     _fields_ = [(n, _i32) for n in ("threads", "ctas_per_sm", "frames_per_cta", "smem_bytes", "state_in_smem",
-                                    "num_sms")]
+                                    "num_sms", "frames_per_lane")]
+
+
+class _CodeConfig(ctypes.Structure):
+    _fields_ = [("frames_per_lane", _i32)]
 
 
 SIGNATURES = {
@@ -56,6 +60,7 @@ SIGNATURES = {
     "cbp_version": ([], ctypes.c_char_p),
     "cbp_construct_base": ([_p, _u64, _p], _i32),
     "cbp_code_create": ([_p, _i32, _i32, _i32, _i32, _p], _i32),
+    "cbp_code_create_ex": ([_p, _i32, _i32, _i32, _i32, _p, _p], _i32),
     "cbp_code_destroy": ([_p], None),
     "cbp_code_dims": ([_p, _p, _p, _p, _p], _i32),
     "cbp_decode": ([_p, _p, _i64, _i64, _p, _p, _i64, _p, _p, _p, _p, _p], _i32),
@@ -115,17 +120,19 @@ def construct_base(spec, seed: int):
 
 
 class Code:
-    """cbp_code_create / cbp_code_destroy: a QC code resident on one CUDA device."""
+    """cbp_code_create_ex / cbp_code_destroy: a QC code resident on one CUDA device.
+    frames_per_lane: 0 automatic, 1 or 2 (a performance setting; results are identical)."""
 
-    def __init__(self, base, Z: int, device=None):
+    def __init__(self, base, Z: int, device=None, frames_per_lane: int = 0):
         base_t = torch.as_tensor(base, dtype=torch.int16).contiguous().cpu()
         self.mb, self.nb = base_t.shape
         self.Z = int(Z)
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
                                    torch.device(device).index or 0)
         h = ctypes.c_void_p()
-        _check(lib().cbp_code_create(base_t.data_ptr(), self.mb, self.nb, self.Z, self.device.index,
-                                     ctypes.byref(h)), "cbp_code_create")
+        cfg = _CodeConfig(int(frames_per_lane))
+        _check(lib().cbp_code_create_ex(base_t.data_ptr(), self.mb, self.nb, self.Z, self.device.index,
+                                        ctypes.byref(cfg), ctypes.byref(h)), "cbp_code_create_ex")
         self._h = h
         N, K, M, E = _i32(), _i32(), _i32(), _i64()
         _check(lib().cbp_code_dims(h, ctypes.byref(N), ctypes.byref(K), ctypes.byref(M), ctypes.byref(E)),

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <mutex>
@@ -12,6 +13,10 @@
 #include "cbp.h"
 #include "cbp_inputs.h"
 #include "cbp_internal.h"
+
+#ifndef CBP_SCHED_SMEM
+#define CBP_SCHED_SMEM 1
+#endif
 
 namespace {
 
@@ -77,9 +82,9 @@ struct cbp_code {
     int32_t mb = 0, nb = 0, Z = 0, N = 0, K = 0, M = 0, kb = 0, core = 0, mid = 0, nent = 0, max_dc = 0, min_dc = 0;
     int64_t E = 0;
     bool can_encode = false;
-    int4* d_ent = nullptr;
-    int32_t* d_row_ptr = nullptr;
-    int16_t* d_pshift = nullptr;
+    std::vector<int4> ent[2];             // schedule tables scaled for geo[alg] (kernel parameters)
+    std::vector<int32_t> row_ptr;
+    std::vector<int16_t> pshift;
     const float4* phi_tab = nullptr;   // per-device table, not owned
     cbp::Geometry geo[2]{};           // per cbp_algorithm
     int ctas_per_sm[2] = {1, 1}, num_sms = 1;
@@ -105,15 +110,25 @@ void cbp_code_destroy(cbp_code* c)
 {
     if (!c) return;
     DeviceGuard g(c->device);
-    cudaFree(c->d_ent);
-    cudaFree(c->d_row_ptr);
-    cudaFree(c->d_pshift);
     delete c;
 }
 
 cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t Z, int32_t device, cbp_code** out)
 {
+    return cbp_code_create_ex(base, mb, nb, Z, device, nullptr, out);
+}
+
+cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32_t Z, int32_t device,
+                              const cbp_code_config* cfg, cbp_code** out)
+{
     if (!base || !out) return fail(CBP_E_INVALID, "cbp_code_create: null argument");
+    int want_P = cfg ? cfg->frames_per_lane : 0;
+    if (want_P < 0 || want_P > 2) return fail(CBP_E_INVALID, "cbp_code_create: frames_per_lane must be 0, 1 or 2");
+    if (want_P == 0) {
+        // debugging override of the automatic choice (A/B measurements)
+        const char* ev = std::getenv("CBP_FRAMES_PER_LANE");
+        if (ev && (ev[0] == '1' || ev[0] == '2') && ev[1] == 0) want_P = ev[0] - '0';
+    }
     *out = nullptr;
     if (mb < 1 || nb <= mb) return fail(CBP_E_INVALID, "cbp_code_create: need 1 <= mb < nb");
     if (Z < 1 || Z > 1024) return fail(CBP_E_INVALID, "cbp_code_create: need 1 <= Z <= 1024");
@@ -152,23 +167,30 @@ cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t 
         row_ptr[i + 1] = static_cast<int>(ent_row.size());
     }
     const int nent = static_cast<int>(ent_row.size());
-    // two int4 per entry b (layout documented in cbp_kernels.cu):
-    //   A = {8 jZ, 4 row(p) Z, 4 bZ, 4 pZ},  B = {8 s, 4 ds, first | kp << 8, jZ}
-    std::vector<int4> ent(2 * static_cast<size_t>(nent));
-    for (int j = 0; j < nb; ++j) {
-        const auto& L = col_ent[j];
-        for (size_t k = 0; k < L.size(); ++k) {
-            const int b = L[k];
-            const int p = L[(k + L.size() - 1) % L.size()];       // previous nonzero row of column j, cyclic
-            const int ds = ((ent_s[b] - ent_s[p]) % Z + Z) % Z;
-            const int first = (k == 0) ? 1 : 0;                   // R1: no latest check before this visit
-            // kp: position of prev(b) among its row's entries = the variable's edge index inside
-            // the previous check (min-sum minimum owner, reading R20)
-            const int kp = p - row_ptr[ent_row[p]];
-            ent[2 * b] = make_int4(8 * j * Z, 4 * ent_row[p] * Z, 4 * b * Z, 4 * p * Z);
-            ent[2 * b + 1] = make_int4(8 * ent_s[b], 4 * ds, first | (kp << 8), j * Z);
+    if (nent > cbp::kMaxEnt || mb > cbp::kMaxRows)
+        return fail(CBP_E_UNSUPPORTED, "cbp_code_create: more than 512 nonzero base entries or 128 base rows");
+    // two int4 per entry b for a geometry with P frames per lane (layout documented in
+    // cbp_kernels.cu; QS = 8P bytes per variable, RS = 4P bytes per edge):
+    //   A = {QS jZ, RS row(p) Z, RS bZ, RS pZ},  B = {QS s, RS ds, first | kp << 8 | s << 16, jZ}
+    auto make_ent = [&](int P) {
+        const int QS = 8 * P, RS = 4 * P;
+        std::vector<int4> ent(2 * static_cast<size_t>(nent));
+        for (int j = 0; j < nb; ++j) {
+            const auto& L = col_ent[j];
+            for (size_t k = 0; k < L.size(); ++k) {
+                const int b = L[k];
+                const int p = L[(k + L.size() - 1) % L.size()];       // previous nonzero row of column j, cyclic
+                const int ds = ((ent_s[b] - ent_s[p]) % Z + Z) % Z;
+                const int first = (k == 0) ? 1 : 0;                   // R1: no latest check before this visit
+                // kp: position of prev(b) among its row's entries = the variable's edge index inside
+                // the previous check (min-sum minimum owner, reading R20)
+                const int kp = p - row_ptr[ent_row[p]];
+                ent[2 * b] = make_int4(QS * j * Z, RS * ent_row[p] * Z, RS * b * Z, RS * p * Z);
+                ent[2 * b + 1] = make_int4(QS * ent_s[b], RS * ds, first | (kp << 8) | (ent_s[b] << 16), j * Z);
+            }
         }
-    }
+        return ent;
+    };
 
     cbp_code* c = new cbp_code();
     c->device = device;
@@ -218,19 +240,8 @@ cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t 
         c->phi_tab = phi_table(device, &terr);
         if (!c->phi_tab) { delete c; return fail(CBP_E_CUDA, "cbp_code_create: " + terr); }
     }
-    cudaError_t e;
-    if ((e = cudaMalloc(&c->d_ent, sizeof(int4) * 2 * nent)) != cudaSuccess ||
-        (e = cudaMalloc(&c->d_row_ptr, sizeof(int32_t) * (mb + 1))) != cudaSuccess ||
-        (e = cudaMalloc(&c->d_pshift, sizeof(int16_t) * mb)) != cudaSuccess) {
-        cbp_code_destroy(c);
-        return fail(CBP_E_NOMEM, std::string("cbp_code_create: ") + cudaGetErrorString(e));
-    }
-    if ((e = cudaMemcpy(c->d_ent, ent.data(), sizeof(int4) * 2 * nent, cudaMemcpyHostToDevice)) != cudaSuccess ||
-        (e = cudaMemcpy(c->d_row_ptr, row_ptr.data(), sizeof(int32_t) * (mb + 1), cudaMemcpyHostToDevice)) != cudaSuccess ||
-        (e = cudaMemcpy(c->d_pshift, pshift.data(), sizeof(int16_t) * mb, cudaMemcpyHostToDevice)) != cudaSuccess) {
-        cbp_code_destroy(c);
-        return cuda_fail(e, "cbp_code_create: cudaMemcpy");
-    }
+    c->row_ptr = row_ptr;
+    c->pshift = pshift;
 
     // ---- launch geometry per algorithm
     int smem_optin = 0, nsm = 0;
@@ -239,9 +250,11 @@ cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t 
     c->num_sms = nsm > 0 ? nsm : 1;
     c->min_dc = *std::min_element(roww.begin(), roww.end());
     const int nwords = (c->N + 31) / 32;
-    for (int alg = 0; alg < 2; ++alg) {
-        cbp::Geometry& G = c->geo[alg];
+    // geometry with P frames per lane; G.teams == 0 if it does not apply
+    auto make_geo = [&](int alg, int P) {
+        cbp::Geometry G{};
         G.alg = alg;
+        G.P = P;
         if (Z <= 16) {
             int zp = 1;
             while (zp < Z) zp <<= 1;
@@ -251,25 +264,43 @@ cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t 
         } else {
             G.Zp = (Z + 31) / 32 * 32; G.F = 1; G.threads = G.Zp; G.multi = 1;
         }
-        // per check: S (log-tanh) or a 16-byte (min, submin, owner|sign, -) record (min-sum)
-        // (slot layout in cbp_kernel: QP, pad to 4 words, S records, R, cw; slots 16-byte aligned;
-        // F > 1 slots are staggered by max(Zp, 4) words across banks)
-        const int64_t raw = (2LL * c->N + 3) / 4 * 4 + c->E + (alg ? 4LL : 1LL) * c->M + nwords;
+        // group of P frames: QP (2P words per variable), pad to 4 words, check records
+        // (P words, or 4P for min-sum's 16-byte records), R (P words per edge), P codewords;
+        // groups 16-byte aligned, F > 1 groups staggered by max(Zp, 4) words across banks
+        const int64_t raw = (2LL * P * c->N + 3) / 4 * 4 + P * ((alg ? 4LL : 1LL) * c->M + c->E + nwords);
         G.slot_words = static_cast<int32_t>(G.F > 1 ? (raw + 31) / 32 * 32 + std::max(G.Zp, 4) : (raw + 3) / 4 * 4);
-        G.table_words = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4;
+        G.table_words = 4 * cbp::kPhiTableSegs + (CBP_SCHED_SMEM ? (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4 : 0);
         G.team_threads = G.threads;
-        // teams per CTA: as many independent teams as shared memory, 512 threads and
-        // 15 named barriers allow (they share the staged tables)
+        // teams per CTA: as many independent teams as shared memory, the thread limit of the
+        // instantiation (512 for P = 1, 256 for P = 2) and 15 named barriers allow
+        const int maxt = (P == 2) ? 256 : 512;
+        if (G.team_threads > maxt && P == 2) return G;
         const int64_t per_team = 4LL * (cbp::kCtlTeamWords + static_cast<int64_t>(G.F) * G.slot_words);
         const int64_t fixed = 4LL * G.table_words;
         int nt = static_cast<int>((smem_optin - fixed) / per_team);
-        nt = std::min(nt, std::max(1, 512 / G.team_threads));
+        nt = std::min(nt, std::max(1, maxt / G.team_threads));
         if (G.multi) nt = std::min(nt, 15);
         G.state_in_smem = nt >= 1 ? 1 : 0;
+        if (P == 2 && !G.state_in_smem) return G;
         G.teams = std::max(nt, 1);
         G.threads = G.teams * G.team_threads;
         G.smem_bytes = static_cast<int32_t>(G.state_in_smem ? fixed + G.teams * per_team
                                                             : fixed + 4LL * cbp::kCtlTeamWords * G.teams);
+        return G;
+    };
+    for (int alg = 0; alg < 2; ++alg) {
+        const cbp::Geometry g1 = make_geo(alg, 1), g2 = make_geo(alg, 2);
+        // automatic: one frame per lane.  Two interleaved frames per lane halve the warps
+        // per SM at the same shared memory and measured slower on every config (C2
+        // ber_sim 12.0 vs 7.65 ms); they remain a selectable geometry.
+        const int P = want_P ? want_P : 1;
+        if (P == 2 && g2.teams == 0) {
+            cbp_code_destroy(c);
+            return fail(CBP_E_UNSUPPORTED, "cbp_code_create: two frames per lane need the state in shared memory "
+                                           "and at most 256 threads per team");
+        }
+        cbp::Geometry& G = c->geo[alg];
+        G = (P == 2) ? g2 : g1;
         int occ = 0;
         if (cbp::occupancy_ctas_per_sm(G, &occ) != 0 || occ < 1) {
             cudaGetLastError();
@@ -277,6 +308,7 @@ cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t 
             return fail(CBP_E_UNSUPPORTED, "cbp_code_create: kernel does not fit on this device");
         }
         c->ctas_per_sm[alg] = G.state_in_smem ? occ : 1;
+        c->ent[alg] = make_ent(G.P);
     }
     *out = c;
     return CBP_OK;
@@ -298,10 +330,11 @@ cbp_status cbp_get_launch_info(const cbp_code* c, cbp_launch_info* o)
     const cbp::Geometry& G = c->geo[0];     // log-tanh geometry (min-sum: same teams, larger slots)
     o->threads = G.threads;
     o->ctas_per_sm = c->ctas_per_sm[0];
-    o->frames_per_cta = G.F * G.teams;
+    o->frames_per_cta = G.F * G.teams * G.P;
     o->smem_bytes = G.smem_bytes;
     o->state_in_smem = G.state_in_smem;
     o->num_sms = c->num_sms;
+    o->frames_per_lane = G.P;
     return CBP_OK;
 }
 
@@ -317,7 +350,10 @@ cbp::KernelArgs base_args(const cbp_code* c, int alg = 0)
     d.N = c->N; d.K = c->K; d.M = c->M; d.Z = c->Z; d.mb = c->mb; d.nb = c->nb; d.kb = c->kb; d.core = c->core;
     d.nent = c->nent; d.E = static_cast<int32_t>(c->E); d.nwords = (c->N + 31) / 32; d.kwords = (c->K + 31) / 32;
     d.max_dc = c->max_dc; d.can_encode = c->can_encode; d.mid = c->mid;
-    d.ent = c->d_ent; d.row_ptr = c->d_row_ptr; d.pshift = c->d_pshift; d.phi_tab = c->phi_tab;
+    d.phi_tab = c->phi_tab;
+    std::memcpy(a.ent, c->ent[alg].data(), sizeof(int4) * c->ent[alg].size());
+    std::memcpy(a.row_ptr, c->row_ptr.data(), sizeof(int32_t) * c->row_ptr.size());
+    std::memcpy(a.pshift, c->pshift.data(), sizeof(int16_t) * c->pshift.size());
     a.Zp = G.Zp; a.F = G.F; a.slot_words = G.slot_words; a.table_words = G.table_words;
     a.team_threads = G.team_threads;
     a.phi_m19 = 0x7ffffu;
@@ -348,7 +384,7 @@ cbp_status run(const cbp_code* c, cbp::KernelArgs& a, int64_t frames, void* stre
     if (!g.ok) return fail(CBP_E_CUDA, std::string(who) + ": cudaSetDevice failed");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const cbp::Geometry& G = c->geo[a.algorithm];
-    const int64_t per_cta = static_cast<int64_t>(G.F) * G.teams;
+    const int64_t per_cta = static_cast<int64_t>(G.F) * G.teams * G.P;
     const int64_t ctas_needed = (frames + per_cta - 1) / per_cta;
     const int grid = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>(static_cast<int64_t>(c->num_sms) * c->ctas_per_sm[a.algorithm], ctas_needed)));
@@ -358,7 +394,7 @@ cbp_status run(const cbp_code* c, cbp::KernelArgs& a, int64_t frames, void* stre
         return fail(CBP_E_NOMEM, std::string(who) + ": " + cudaGetErrorString(e));
     float* gs = nullptr;
     if (!G.state_in_smem) {
-        const size_t bytes = sizeof(float) * static_cast<size_t>(grid) * per_cta * G.slot_words;
+        const size_t bytes = sizeof(float) * static_cast<size_t>(grid) * G.F * G.teams * G.slot_words;
         if ((e = cudaMallocAsync(reinterpret_cast<void**>(&gs), bytes, st)) != cudaSuccess) {
             cudaFreeAsync(q, st);
             return fail(CBP_E_NOMEM, std::string(who) + ": " + cudaGetErrorString(e));

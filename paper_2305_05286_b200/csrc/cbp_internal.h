@@ -4,31 +4,29 @@
 
 namespace cbp {
 
-// Per nonzero base entry b (row-major over nonzero entries), packed in an int4:
-//   x = var_base (j*Z)            | s_prev_base (row(prev(b))*Z) << 16
-//   y = shift s | ds << 11 | first << 22 | self << 23
-//       ds = (s - s_prev) mod Z: lifted row of the previous check of the same
-//       variable is (r + ds) mod Z; first: b is the first nonzero row of its
-//       column (no latest check in sweep 1, reading R1); self: prev(b) == b
-//       (degree-1 column, reading R3)
-//   z = R slot base of b      (b*Z; edge (check i*Z+r, its variable) = z + r)
-//   w = R slot base of prev(b)
+// Schedule tables: two int4 per nonzero base entry, byte offsets scaled for the
+// launch geometry's frames per lane P (layout documented in cbp_kernels.cu).
 struct DevCode {
     int32_t N, K, M, Z, mb, nb, kb, core;
     int32_t nent, E, nwords, kwords;
     int32_t max_dc;
     int32_t can_encode;
     int32_t mid;           // floor(core/2)
-    const int4* ent;       // [nent]
-    const int32_t* row_ptr;// [mb+1]
-    const int16_t* pshift; // [mb]: shift of column kb in row i (-1 if none)
     const float4* phi_tab; // [929] phi contract v2 coefficients
 };
 
 enum Mode : int32_t { MODE_DECODE_F32 = 0, MODE_DECODE_I8 = 1, MODE_BER_SIM = 2, MODE_CHANNEL = 3 };
 
+// Limits of the schedule tables carried in the kernel parameters (constant bank):
+// read through the constant cache, they take no shared-memory bandwidth.
+constexpr int kMaxEnt = 512;    // nonzero base entries
+constexpr int kMaxRows = 128;   // base rows
+
 struct KernelArgs {
     DevCode code;
+    int4 ent[2 * kMaxEnt];          // schedule entries of this geometry (cbp_kernels.cu)
+    int32_t row_ptr[kMaxRows + 1];  // entry range of base row i
+    int16_t pshift[kMaxRows];       // shift of column kb in row i (-1 if none)
     int32_t mode;
     int32_t max_iter, stop_rule;
     int32_t algorithm;     // 0 log-tanh, 1 normalized min-sum
@@ -60,12 +58,13 @@ struct KernelArgs {
     float* gstate;         // per-CTA global state (state_in_smem == 0)
 };
 
-constexpr int kCtlTeamWords = 72;   // shared control words per team: 2 x 32 ballot words + broadcast
+constexpr int kCtlTeamWords = 136;  // shared control words per team: 2 x P(2) x 32 ballot words + broadcast
 
 struct Geometry {
     int32_t threads, F, Zp, slot_words, table_words, smem_bytes, state_in_smem, multi;
     int32_t team_threads, teams;   // threads per team, teams per CTA
     int32_t alg;                   // cbp_algorithm of this geometry
+    int32_t P;                     // frames per lane (1 or 2), interleaved in a group
 };
 
 // launch (cbp_kernels.cu); returns cudaError_t as int

@@ -2,12 +2,15 @@
 //
 // One persistent kernel serves cbp_decode, cbp_decode_i8, cbp_channel and
 // cbp_ber_sim.  A CTA holds several independent teams; a team
-// owns F frame slots of Zp lanes, and lane r of a slot processes lifted check
-// i*Z + r of the current base row i.  The Z lifted checks of one base row touch
-// disjoint variables (each block is a permutation), so processing them in
-// parallel is bit-identical to the paper's sequential check order (reading
-// R12).  Per-frame state lives in shared memory:
-//   QP[N] float2 (Q_v, Phi_v | hard bit in the sign), R[E], S[M] (sign = Omega<0)
+// owns F groups of Zp lanes, a group holds P frames (P = 1 or 2) and lane r of
+// a group processes lifted check i*Z + r of the current base row i for all P
+// frames at once.  The Z lifted checks of one base row touch disjoint
+// variables (each block is a permutation), so processing them in parallel is
+// bit-identical to the paper's sequential check order (reading R12).
+// Per-group state lives in shared memory with the P frames interleaved, so one
+// schedule entry, one address computation and one wide load/store serve all P
+// frames (and P = 2 pairs run on the packed FADD2 pipe):
+//   QP[N] {Q_v(0..P-1), Phi_v(0..P-1) | hard bit in the sign}, S[M] records, R[E] x P, cw[P][nwords]
 // The phi table (contract v2) and the code's schedule tables are staged once per CTA.
 //
 // Paper steps (§IV-C): init = Step 1 (l.402-422, equ_s4e15-17);
@@ -25,31 +28,111 @@ namespace cbp {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr uint32_t kSign = 0x80000000u;
 
-// independent edges of a check processed together (ILP); remainder one at a time
+// independent edges of a check processed together (ILP); remainder two / one at a time
 #ifndef CBP_CHUNK
 #define CBP_CHUNK 3
 #endif
+// A/B switch: 1 = stage the schedule tables in shared memory (default), 0 = read them
+// from the kernel parameters in the hot loop
+#ifndef CBP_SCHED_SMEM
+#define CBP_SCHED_SMEM 1
+#endif
 
-// Per-slot state.  Byte-addressed bases plus typed views for the cold paths.
-struct SlotPtrs {
-    char* qp;       // float2 [N]: (Q_{v->c*}, Phi_v = phi(|Q_v|) with sign bit = hard decision x_v)
-    char* R;        // float [E]: C2V message of edge (check i*Z+r, entry b) at byte 4*(b*Z + r)
-    char* S;        // float [M]: phi-domain check-belief sum S_c, sign bit = (Omega_c < 0)
-    uint32_t* cw;   // [nwords] transmitted codeword (ber_sim) / scratch
-    __device__ __forceinline__ float2* QP() const { return reinterpret_cast<float2*>(qp); }
-    __device__ __forceinline__ float* Rf() const { return reinterpret_cast<float*>(R); }
-    __device__ __forceinline__ float* Sf() const { return reinterpret_cast<float*>(S); }
+// ---------------------------------------------------------------- byte-addressed vector access
+template <int N>
+__device__ __forceinline__ void ldf(const char* b, int off, float* o)
+{
+    if constexpr (N == 1) {
+        o[0] = *reinterpret_cast<const float*>(b + off);
+    } else if constexpr (N == 2) {
+        const float2 t = *reinterpret_cast<const float2*>(b + off);
+        o[0] = t.x; o[1] = t.y;
+    } else {
+        const float4 t = *reinterpret_cast<const float4*>(b + off);
+        o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void stf(char* b, int off, const float* v)
+{
+    if constexpr (N == 1) *reinterpret_cast<float*>(b + off) = v[0];
+    else if constexpr (N == 2) *reinterpret_cast<float2*>(b + off) = make_float2(v[0], v[1]);
+    else *reinterpret_cast<float4*>(b + off) = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// o = a + b and o = a - b over the P frames (FADD2 for a pair; IEEE rn either way)
+template <int P>
+__device__ __forceinline__ void vadd(const float* a, const float* b, float* o)
+{
+    if constexpr (P == 2) {
+        const float2 t = __fadd2_rn(make_float2(a[0], a[1]), make_float2(b[0], b[1]));
+        o[0] = t.x; o[1] = t.y;
+    } else {
+        o[0] = __fadd_rn(a[0], b[0]);
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void vsub(const float* a, const float* b, float* o)
+{
+    if constexpr (P == 2) {
+        const float2 t = __fadd2_rn(make_float2(a[0], a[1]), make_float2(-b[0], -b[1]));
+        o[0] = t.x; o[1] = t.y;
+    } else {
+        o[0] = __fsub_rn(a[0], b[0]);
+    }
+}
+
+// |a| - |b| over the P frames
+template <int P>
+__device__ __forceinline__ void vabsdiff(const float* a, const float* b, float* o)
+{
+    if constexpr (P == 2) {
+        const float2 t = __fadd2_rn(make_float2(fabsf(a[0]), fabsf(a[1])), make_float2(-fabsf(b[0]), -fabsf(b[1])));
+        o[0] = t.x; o[1] = t.y;
+    } else {
+        o[0] = __fsub_rn(fabsf(a[0]), fabsf(b[0]));
+    }
+}
+
+// ---------------------------------------------------------------- group state
+// Byte strides: QS per variable (QP), RS per edge (R), SS per check record.
+template <int P, int ALG>
+struct Lay {
+    static constexpr int QS = 8 * P;
+    static constexpr int RS = 4 * P;
+    static constexpr int SU = ALG ? 4 : 1;   // check-record stride in units of RS
+    static constexpr int SS = RS * SU;
+    static constexpr int SW = ALG ? 4 : 1;   // words per frame in a check record
 };
 
-__device__ __forceinline__ float2 ld2(const char* b, int off) { return *reinterpret_cast<const float2*>(b + off); }
-__device__ __forceinline__ float ld1(const char* b, int off) { return *reinterpret_cast<const float*>(b + off); }
-__device__ __forceinline__ void st2(char* b, int off, float2 v) { *reinterpret_cast<float2*>(b + off) = v; }
-__device__ __forceinline__ void st1(char* b, int off, float v) { *reinterpret_cast<float*>(b + off) = v; }
+// A group of P frames.  Record word k of frame p at byte 4 (k P + p) of the record
+// (log-tanh: k = 0, S_c with sign = Omega < 0; min-sum: {min, submin, owner | sign, pad}).
+template <int P, int ALG>
+struct Grp {
+    char* qp;
+    char* S;
+    char* R;
+    uint32_t* cw;
+    int nwords;
+    using Ly = Lay<P, ALG>;
+    __device__ __forceinline__ float& Q(int v, int p) const { return reinterpret_cast<float*>(qp + v * Ly::QS)[p]; }
+    __device__ __forceinline__ float& PH(int v, int p) const { return reinterpret_cast<float*>(qp + v * Ly::QS)[P + p]; }
+    __device__ __forceinline__ float& Rw(int e, int p) const { return reinterpret_cast<float*>(R + e * Ly::RS)[p]; }
+    __device__ __forceinline__ float& Sw(int c, int k, int p) const
+    {
+        return reinterpret_cast<float*>(S + c * Ly::SS)[k * P + p];
+    }
+    __device__ __forceinline__ uint32_t* cwp(int p) const { return cw + p * nwords; }
+};
 
-// Schedule table entry b (two int4, built in cbp_api.cpp):
-//   A = {8 j Z, 4 row(prev(b)) Z, 4 b Z, 4 prev(b) Z}    byte bases: variable block (QP),
-//        S block of the previous check of the same variables, own R block, R block of prev(b)
-//   B = {8 s, 4 ds, first, j Z}   ds = (s - s_prev) mod Z; first: no latest check in sweep 1 (R1)
+// Schedule table entry b (two int4, built in cbp_api.cpp for the launch's P and algorithm):
+//   A = {QS jZ, RS row(prev(b)) Z, RS b Z, RS prev(b) Z}   byte bases: variable block (QP),
+//        check block of the previous check of the same variables (x SU for the S records),
+//        own R block, R block of prev(b)
+//   B = {QS s, RS ds, first | kp << 8 | s << 16, jZ}   ds = (s - s_prev) mod Z; first: no latest
+//        check in sweep 1 (R1); kp = position of prev(b) in its row (min-sum owner, R20)
 // prev(b) = previous nonzero row of b's column, cyclically (the static "latest check" of
 // every variable of the block after sweep 1); prev(b) == b for a degree-1
 // column (R3).  Variable of lane r: j Z + (r + s) mod Z; its previous check's row (r + ds) mod Z.
@@ -57,14 +140,14 @@ __device__ __forceinline__ void st1(char* b, int off, float v) { *reinterpret_ca
 __device__ __forceinline__ int lane_var(const int4* ent, int e, int r, int Z)
 {
     const int4 B = ent[2 * e + 1];
-    int t = r + (B.x >> 3);
+    int t = r + (B.z >> 16);
     t = (t >= Z) ? t - Z : t;
     return B.w + t;
 }
 
 // ---------------------------------------------------------------- team helpers
-// !MULTI: a team is one warp holding F frame slots of Zp lanes; MULTI: a team is
-// TW warps holding one frame.  Teams synchronise with their own named barrier.
+// !MULTI: a team is one warp holding F groups of Zp lanes; MULTI: a team is TW
+// warps holding one group.  Teams synchronise with their own named barrier.
 __device__ __forceinline__ void named_bar_sync(int id, int n)
 {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -91,22 +174,22 @@ struct Team {
     int tl;               // thread index within the team
     int slot, r, lane_base;
     bool lane_on;
-    unsigned slot_mask;   // lanes of this slot within the warp (!MULTI)
+    unsigned slot_mask;   // lanes of this group within the warp (!MULTI)
 
     __device__ __forceinline__ void sync() const
     {
         if (MULTI) named_bar_sync(1 + tidx, nthreads);
         else __syncwarp();
     }
-    // OR of a slot-uniform predicate over the team's slots.  A MULTI team holds one
-    // frame and every thread derives the control state identically, so the predicate
-    // is already team-uniform (no barrier); a warp team votes over its F slots.
+    // OR of a group-uniform predicate over the team's groups.  A MULTI team holds one
+    // group and every thread derives the control state identically, so the predicate
+    // is already team-uniform (no barrier); a warp team votes over its F groups.
     __device__ __forceinline__ bool team_any(bool pred) const
     {
         if (MULTI) return pred;
         return __any_sync(kFull, pred) != 0;
     }
-    // OR over the lanes of this slot (a synchronisation point)
+    // OR over the lanes of this group (a synchronisation point)
     __device__ __forceinline__ bool slot_any(bool pred) const
     {
         if (MULTI) return named_bar_or(1 + tidx, nthreads, pred);
@@ -116,226 +199,318 @@ struct Team {
 
 // ---------------------------------------------------------------- per-row edge chain
 struct Lane {
-    int r, r4, r8, Z, Z4, Z8;
-    int qp_bytes, R_bytes, S_bytes;   // slot array sizes (bounds checks of debug builds)
+    int r, rq, rr, ZQ, ZR;            // lane, r QS, r RS, Z QS, Z RS
+    int qp_bytes, R_bytes, S_bytes;   // group array sizes (bounds checks of debug builds)
     uint32_t m19, one;                // phi local-variable masks as runtime operands (one LOP3)
 };
 
+template <int P>
 struct RowAcc {
-    float Ssum;
-    uint32_t negw;     // bit 31: XOR of the signs of Q^new over the check (sign of Omega)
-    uint32_t flipw;    // bit 31: some posterior sign flipped (equ_s4e24)
-    uint32_t oldbits;  // previous hard bits of the check's variables (rollback of a mid-row stop)
+    float Ssum[P];
+    uint32_t negw[P];     // bit 31: XOR of the signs of Q^new over the check (sign of Omega)
+    uint32_t flipw[P];    // bit 31: some posterior sign flipped (equ_s4e24)
+    uint32_t oldbits[P];  // previous hard bits of the check's variables (rollback of a mid-row stop)
 };
 
-// U consecutive edges of lane r's check.  Loads first, then U independent B2V
-// phi chains, commits / V2C, U independent C2B phi chains and the ordered S
-// accumulation (reading R12).  SWEEP1 handles first visits (reading R1); TRACK
+// U consecutive edges of lane r's check for the P frames.  Loads first, then U x P
+// independent B2V phi chains, commits / V2C, U x P independent C2B phi chains and
+// the ordered S accumulation (reading R12).  SW1: some frame of the group is in
+// sweep 1 (s1[p]); its first visits get R^new = 0 (reading R1) -- the commit then
+// writes that 0 into an R slot that still holds its initial 0 (no edge of the
+// column has been processed yet in sweep 1), identical to not writing.  TRACK
 // records the previous hard bits (only rows where the belief window can fire).
 // R_{ci->v} is read after the commit of R_{cj->v}: for a degree-1 column both are
 // the same slot, which realises "commit before read" (R3) through memory order.
-template <int U, bool SWEEP1, bool TRACK>
+template <int U, int P, bool SW1, bool TRACK>
 __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int k0,
-                                           const Lane& L, const SlotPtrs& s, RowAcc& acc)
+                                           const Lane& L, const Grp<P, 0>& g, const bool (&s1)[P], RowAcc<P>& acc)
 {
+    using Ly = Lay<P, 0>;
     int aqp[U], aw[U], ar[U];
-    float q[U], p[U], scj[U], Rn[U];
+    float q[U][P], p0[U][P], scj[U][P], Rn[U][P];
     bool fst[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int4 A = ent[2 * (e0 + k0 + u)];
         const int4 B = ent[2 * (e0 + k0 + u) + 1];
-        int t8 = L.r8 + B.x;
-        t8 = (t8 >= L.Z8) ? t8 - L.Z8 : t8;
-        int rp4 = L.r4 + B.y;
-        rp4 = (rp4 >= L.Z4) ? rp4 - L.Z4 : rp4;
-        CBP_CHECK(t8 >= 0 && t8 < L.Z8 && rp4 >= 0 && rp4 < L.Z4);
-        CBP_CHECK(A.x + t8 + 8 <= L.qp_bytes && A.y + rp4 + 4 <= L.S_bytes && A.z + L.r4 + 4 <= L.R_bytes &&
-                  A.w + rp4 + 4 <= L.R_bytes);
-        aqp[u] = A.x + t8;
-        aw[u] = A.w + rp4;
-        ar[u] = A.z + L.r4;
-        fst[u] = SWEEP1 && (B.z & 1) != 0;
-        const float2 qp = ld2(s.qp, aqp[u]);
-        q[u] = qp.x;
-        p[u] = qp.y;
-        scj[u] = ld1(s.S, A.y + rp4);
+        int tq = L.rq + B.x;
+        tq = (tq >= L.ZQ) ? tq - L.ZQ : tq;
+        int tr = L.rr + B.y;
+        tr = (tr >= L.ZR) ? tr - L.ZR : tr;
+        CBP_CHECK(tq >= 0 && tq < L.ZQ && tr >= 0 && tr < L.ZR);
+        CBP_CHECK(A.x + tq + Ly::QS <= L.qp_bytes && A.y + tr + Ly::RS <= L.S_bytes && A.z + L.rr + Ly::RS <= L.R_bytes &&
+                  A.w + tr + Ly::RS <= L.R_bytes);
+        aqp[u] = A.x + tq;
+        aw[u] = A.w + tr;
+        ar[u] = A.z + L.rr;
+        fst[u] = SW1 && (B.z & 1) != 0;
+        float qp[2 * P];
+        ldf<2 * P>(g.qp, aqp[u], qp);
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            q[u][p] = qp[p];
+            p0[u][p] = qp[P + p];
+        }
+        ldf<P>(g.S, A.y + tr, scj[u]);
     }
     // B2V (equ_s4e18): R^new_{cj->v} = sgn(Omega_cj) sgn(Q) phi(|phi(|Omega_cj|) - phi(|Q|)|), phi(|Omega|) = S (R11)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const float mag = phi32(fabsf(__fsub_rn(fabsf(scj[u]), fabsf(p[u]))), ptab, L.m19, L.one);
-        const uint32_t sg = (__float_as_uint(scj[u]) ^ __float_as_uint(q[u])) & kSign;
-        Rn[u] = __uint_as_float(__float_as_uint(mag) | sg);
-        if (SWEEP1 && fst[u]) Rn[u] = 0.0f;
+        float d[P];
+        vabsdiff<P>(scj[u], p0[u], d);
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const float mag = phi32(fabsf(d[p]), ptab, L.m19, L.one);
+            const uint32_t sg = (__float_as_uint(scj[u][p]) ^ __float_as_uint(q[u][p])) & kSign;
+            Rn[u][p] = __uint_as_float(__float_as_uint(mag) | sg);
+            if (SW1 && fst[u] && s1[p]) Rn[u][p] = 0.0f;
+        }
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u) stf<P>(g.R, aw[u], Rn[u]);   // equ_s4e22 commit of R_{cj->v} (R2), before the read (R3)
+    float qn[U][P];
+    uint32_t lb[U][P];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        float ro[P], lam[P];
+        ldf<P>(g.R, ar[u], ro);                              // R_{ci->v}
+        vadd<P>(q[u], Rn[u], lam);                           // equ_s4e20 (Lambda is never -0)
+        vsub<P>(lam, ro, qn[u]);                             // equ_s4e19 (R15)
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            lb[u][p] = __float_as_uint(lam[p]) & kSign;      // hard decision, equ_s2e7
+            acc.flipw[p] |= __float_as_uint(lam[p]) ^ __float_as_uint(p0[u][p]);   // equ_s4e24 (R7), bit 31
+            if (TRACK) acc.oldbits[p] |= (__float_as_uint(p0[u][p]) >> 31) << (k0 + u);
+        }
+    }
+    float ph[U][P];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-        if (!(SWEEP1 && fst[u])) st1(s.R, aw[u], Rn[u]);   // equ_s4e22 commit of R_{cj->v} (R2), before the read (R3)
-    float qn[U];
-    uint32_t lb[U];
+#pragma unroll
+        for (int p = 0; p < P; ++p) ph[u][p] = phi32(fabsf(qn[u][p]), ptab, L.m19, L.one);   // C2B (equ_s4e21, App. equ_ae4)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const float ro = ld1(s.R, ar[u]);                    // R_{ci->v}
-        const float lam = __fadd_rn(q[u], Rn[u]);            // equ_s4e20 (Lambda is never -0)
-        qn[u] = __fsub_rn(lam, ro);                          // equ_s4e19 (R15)
-        lb[u] = __float_as_uint(lam) & kSign;                // hard decision, equ_s2e7
-        acc.flipw |= __float_as_uint(lam) ^ __float_as_uint(p[u]);   // equ_s4e24 (R7), bit 31
-        if (TRACK) acc.oldbits |= (__float_as_uint(p[u]) >> 31) << (k0 + u);
-    }
-    float ph[U];
+        vadd<P>(acc.Ssum, ph[u], acc.Ssum);
+        float st[2 * P];
 #pragma unroll
-    for (int u = 0; u < U; ++u) ph[u] = phi32(fabsf(qn[u]), ptab, L.m19, L.one);   // C2B (equ_s4e21, App. equ_ae4)
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        acc.Ssum = __fadd_rn(acc.Ssum, ph[u]);
-        acc.negw ^= __float_as_uint(qn[u]);                  // Q^new is never -0
-        st2(s.qp, aqp[u], make_float2(qn[u], __uint_as_float(__float_as_uint(ph[u]) | lb[u])));
+        for (int p = 0; p < P; ++p) {
+            acc.negw[p] ^= __float_as_uint(qn[u][p]);        // Q^new is never -0
+            st[p] = qn[u][p];
+            st[P + p] = __uint_as_float(__float_as_uint(ph[u][p]) | lb[u][p]);
+        }
+        stf<2 * P>(g.qp, aqp[u], st);
     }
 }
 
-// check record of the row (log-tanh: S in .x; min-sum: the 16-byte record) before / after
+// check records of the row before / after (log-tanh: S in .x; min-sum: the record)
+template <int P>
 struct RowOut {
-    float4 Snew, Sold;
-    uint32_t oldbits;
-    bool ok;
+    float4 Snew[P], Sold[P];
+    uint32_t oldbits[P];
+    bool ok[P];
 };
 
-template <bool SWEEP1, bool TRACK>
-__device__ __forceinline__ RowOut process_row(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
-                                              int dc, int sidx4, const Lane& L, const SlotPtrs& s)
+template <int P, bool SW1, bool TRACK>
+__device__ __forceinline__ RowOut<P> process_row(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
+                                                 int dc, int sidx, const Lane& L, const Grp<P, 0>& g,
+                                                 const bool (&s1)[P])
 {
-    RowAcc acc{0.0f, 0u, 0u, 0u};
-    const float Sold = ld1(s.S, sidx4);
+    RowAcc<P> acc;
+    float Sold[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        acc.Ssum[p] = 0.0f;
+        acc.negw[p] = acc.flipw[p] = acc.oldbits[p] = 0u;
+    }
+    ldf<P>(g.S, sidx, Sold);
     int k0 = 0;
-    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) edge_chunk<CBP_CHUNK, SWEEP1, TRACK>(ent, ptab, e0, k0, L, s, acc);
-    for (; k0 < dc; ++k0) edge_chunk<1, SWEEP1, TRACK>(ent, ptab, e0, k0, L, s, acc);
-    const float Snew = __uint_as_float(__float_as_uint(acc.Ssum) | (acc.negw & kSign));
-    st1(s.S, sidx4, Snew);                                   // equ_s4e23
-    RowOut o;
-    o.Snew.x = Snew;
-    o.Sold.x = Sold;
-    o.oldbits = acc.oldbits;
-    o.ok = ((acc.negw | acc.flipw) & kSign) == 0u;           // equ_s4e2 and equ_s4e24 for this check
+    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) edge_chunk<CBP_CHUNK, P, SW1, TRACK>(ent, ptab, e0, k0, L, g, s1, acc);
+    if (CBP_CHUNK > 2 && k0 + 2 <= dc) {
+        edge_chunk<2, P, SW1, TRACK>(ent, ptab, e0, k0, L, g, s1, acc);
+        k0 += 2;
+    }
+    if (k0 < dc) edge_chunk<1, P, SW1, TRACK>(ent, ptab, e0, k0, L, g, s1, acc);
+    RowOut<P> o;
+    float Snew[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        Snew[p] = __uint_as_float(__float_as_uint(acc.Ssum[p]) | (acc.negw[p] & kSign));
+        o.Snew[p] = make_float4(Snew[p], 0.0f, 0.0f, 0.0f);
+        o.Sold[p] = make_float4(Sold[p], 0.0f, 0.0f, 0.0f);
+        o.oldbits[p] = acc.oldbits[p];
+        o.ok[p] = ((acc.negw[p] | acc.flipw[p]) & kSign) == 0u;   // equ_s4e2 and equ_s4e24 for this check
+    }
+    stf<P>(g.S, sidx, Snew);                                      // equ_s4e23
     return o;
 }
 
 // ---------------------------------------------------------------- normalized min-sum CBP
-// PAPER.md l.577-603 (equ_s4e18xx, equ_s4e21xx) with reading R20: per check a 16-byte
+// PAPER.md l.577-603 (equ_s4e18xx, equ_s4e21xx) with reading R20: per check and frame a
 // record {min, submin, owner | sign << 31, -} of m = fl(alpha |Q^new|); B2V magnitude =
 // submin if v owns the minimum (owner = v's edge index in the check) else min; signs as
 // psi- (equ_s4e13).  Schedule, V2C, commit and stop rule are those of the log-tanh path.
+template <int P>
 struct MsAcc {
-    float m1, m2;
-    uint32_t own, negw, flipw, oldbits;
+    float m1[P], m2[P];
+    uint32_t own[P], negw[P], flipw[P], oldbits[P];
 };
 
-__device__ __forceinline__ float4 ld4(const char* b, int off) { return *reinterpret_cast<const float4*>(b + off); }
-__device__ __forceinline__ void st4(char* b, int off, float4 v) { *reinterpret_cast<float4*>(b + off) = v; }
-
-template <int U, bool SWEEP1, bool TRACK>
-__device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int e0, int k0, const Lane& L,
-                                              const SlotPtrs& s, float alpha, MsAcc& acc)
+// words {m1, m2, ow} of the P frames of a record: P = 1 one 16-byte load, P = 2 16 + 8 bytes
+template <int P>
+__device__ __forceinline__ void ld_rec(const char* S, int off, float (&m1)[P], float (&m2)[P], uint32_t (&ow)[P])
 {
+    if constexpr (P == 1) {
+        const float4 t = *reinterpret_cast<const float4*>(S + off);
+        m1[0] = t.x; m2[0] = t.y; ow[0] = __float_as_uint(t.z);
+    } else {
+        const float4 t = *reinterpret_cast<const float4*>(S + off);
+        const uint2 w = *reinterpret_cast<const uint2*>(S + off + 16);
+        m1[0] = t.x; m1[1] = t.y; m2[0] = t.z; m2[1] = t.w; ow[0] = w.x; ow[1] = w.y;
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void st_rec(char* S, int off, const float (&m1)[P], const float (&m2)[P], const uint32_t (&ow)[P])
+{
+    if constexpr (P == 1) {
+        *reinterpret_cast<float4*>(S + off) = make_float4(m1[0], m2[0], __uint_as_float(ow[0]), 0.0f);
+    } else {
+        *reinterpret_cast<float4*>(S + off) = make_float4(m1[0], m1[1], m2[0], m2[1]);
+        *reinterpret_cast<uint2*>(S + off + 16) = make_uint2(ow[0], ow[1]);
+    }
+}
+
+template <int U, int P, bool SW1, bool TRACK>
+__device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int e0, int k0, const Lane& L,
+                                              const Grp<P, 1>& g, const bool (&s1)[P], float alpha, MsAcc<P>& acc)
+{
+    using Ly = Lay<P, 1>;
     int aqp[U], aw[U], ar[U], kp[U];
-    float q[U], p[U], Rn[U];
-    float4 cs[U];
+    float q[U][P], p0[U][P], Rn[U][P];
+    float cm1[U][P], cm2[U][P];
+    uint32_t cow[U][P];
     bool fst[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int4 A = ent[2 * (e0 + k0 + u)];
         const int4 B = ent[2 * (e0 + k0 + u) + 1];
-        int t8 = L.r8 + B.x;
-        t8 = (t8 >= L.Z8) ? t8 - L.Z8 : t8;
-        int rp4 = L.r4 + B.y;
-        rp4 = (rp4 >= L.Z4) ? rp4 - L.Z4 : rp4;
-        CBP_CHECK(4 * (A.y + rp4) + 16 <= 4 * L.S_bytes);
-        aqp[u] = A.x + t8;
-        aw[u] = A.w + rp4;
-        ar[u] = A.z + L.r4;
-        fst[u] = SWEEP1 && (B.z & 1) != 0;
-        kp[u] = B.z >> 8;
-        const float2 qp = ld2(s.qp, aqp[u]);
-        q[u] = qp.x;
-        p[u] = qp.y;
-        cs[u] = ld4(s.S, 4 * (A.y + rp4));                   // record of the previous check c_j
+        int tq = L.rq + B.x;
+        tq = (tq >= L.ZQ) ? tq - L.ZQ : tq;
+        int tr = L.rr + B.y;
+        tr = (tr >= L.ZR) ? tr - L.ZR : tr;
+        CBP_CHECK(Ly::SU * (A.y + tr) + Ly::SS <= L.S_bytes);
+        aqp[u] = A.x + tq;
+        aw[u] = A.w + tr;
+        ar[u] = A.z + L.rr;
+        fst[u] = SW1 && (B.z & 1) != 0;
+        kp[u] = (B.z >> 8) & 0xff;
+        float qp[2 * P];
+        ldf<2 * P>(g.qp, aqp[u], qp);
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            q[u][p] = qp[p];
+            p0[u][p] = qp[P + p];
+        }
+        ld_rec<P>(g.S, Ly::SU * (A.y + tr), cm1[u], cm2[u], cow[u]);   // record of the previous check c_j
     }
     // B2V (equ_s4e18xx)
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const uint32_t ow = __float_as_uint(cs[u].z);
-        const float mag = (static_cast<int>(ow & 0xffu) == kp[u]) ? cs[u].y : cs[u].x;
-        Rn[u] = __uint_as_float(__float_as_uint(mag) | ((ow ^ __float_as_uint(q[u])) & kSign));
-        if (SWEEP1 && fst[u]) Rn[u] = 0.0f;
-    }
-#pragma unroll
     for (int u = 0; u < U; ++u)
-        if (!(SWEEP1 && fst[u])) st1(s.R, aw[u], Rn[u]);   // commit of R_{cj->v} (R2, R3)
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const uint32_t ow = cow[u][p];
+            const float mag = (static_cast<int>(ow & 0xffu) == kp[u]) ? cm2[u][p] : cm1[u][p];
+            Rn[u][p] = __uint_as_float(__float_as_uint(mag) | ((ow ^ __float_as_uint(q[u][p])) & kSign));
+            if (SW1 && fst[u] && s1[p]) Rn[u][p] = 0.0f;
+        }
+#pragma unroll
+    for (int u = 0; u < U; ++u) stf<P>(g.R, aw[u], Rn[u]);   // commit of R_{cj->v} (R2, R3)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const float ro = ld1(s.R, ar[u]);
-        const float lam = __fadd_rn(q[u], Rn[u]);            // equ_s4e20
-        const float qn = __fsub_rn(lam, ro);                 // equ_s4e19
-        const uint32_t lb = __float_as_uint(lam) & kSign;
-        acc.flipw |= __float_as_uint(lam) ^ __float_as_uint(p[u]);
-        if (TRACK) acc.oldbits |= (__float_as_uint(p[u]) >> 31) << (k0 + u);
-        // C2B (equ_s4e21xx), in ascending edge order
-        const float m = __fmul_rn(alpha, fabsf(qn));
-        if (m < acc.m1) {
-            acc.m2 = acc.m1;
-            acc.m1 = m;
-            acc.own = static_cast<uint32_t>(k0 + u);
-        } else if (m < acc.m2) {
-            acc.m2 = m;
+        float ro[P], lam[P], qn[P], st[2 * P];
+        ldf<P>(g.R, ar[u], ro);
+        vadd<P>(q[u], Rn[u], lam);                           // equ_s4e20
+        vsub<P>(lam, ro, qn);                                // equ_s4e19
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const uint32_t lb = __float_as_uint(lam[p]) & kSign;
+            acc.flipw[p] |= __float_as_uint(lam[p]) ^ __float_as_uint(p0[u][p]);
+            if (TRACK) acc.oldbits[p] |= (__float_as_uint(p0[u][p]) >> 31) << (k0 + u);
+            // C2B (equ_s4e21xx), in ascending edge order, branch-free:
+            // m < m1: (m1, m2, own) <- (m, m1, k); else m2 <- min(m2, m).  m1 <= m2 always.
+            const float m = __fmul_rn(alpha, fabsf(qn[p]));
+            const bool lt = m < acc.m1[p];
+            acc.m2[p] = fminf(acc.m2[p], fmaxf(acc.m1[p], m));
+            acc.own[p] = lt ? static_cast<uint32_t>(k0 + u) : acc.own[p];
+            acc.m1[p] = fminf(acc.m1[p], m);
+            acc.negw[p] ^= __float_as_uint(qn[p]);
+            st[p] = qn[p];
+            st[P + p] = __uint_as_float(lb);
         }
-        acc.negw ^= __float_as_uint(qn);
-        st2(s.qp, aqp[u], make_float2(qn, __uint_as_float(lb)));
+        stf<2 * P>(g.qp, aqp[u], st);
     }
 }
 
-template <bool SWEEP1, bool TRACK>
-__device__ __forceinline__ RowOut process_row_ms(const int4* __restrict__ ent, int e0, int dc, int sidx4, const Lane& L,
-                                                 const SlotPtrs& s, float alpha)
+template <int P, bool SW1, bool TRACK>
+__device__ __forceinline__ RowOut<P> process_row_ms(const int4* __restrict__ ent, int e0, int dc, int sidx,
+                                                    const Lane& L, const Grp<P, 1>& g, const bool (&s1)[P], float alpha)
 {
+    using Ly = Lay<P, 1>;
     const float inf = __uint_as_float(0x7f800000u);
-    MsAcc acc{inf, inf, 0u, 0u, 0u, 0u};                    // Omega^(-1) = (inf, inf)
-    const float4 Sold = ld4(s.S, 4 * sidx4);
+    MsAcc<P> acc;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        acc.m1[p] = acc.m2[p] = inf;                         // Omega^(-1) = (inf, inf)
+        acc.own[p] = acc.negw[p] = acc.flipw[p] = acc.oldbits[p] = 0u;
+    }
+    float om1[P], om2[P];
+    uint32_t oow[P];
+    ld_rec<P>(g.S, Ly::SU * sidx, om1, om2, oow);
     int k0 = 0;
-    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) edge_chunk_ms<CBP_CHUNK, SWEEP1, TRACK>(ent, e0, k0, L, s, alpha, acc);
-    for (; k0 < dc; ++k0) edge_chunk_ms<1, SWEEP1, TRACK>(ent, e0, k0, L, s, alpha, acc);
-    const float4 Snew = make_float4(acc.m1, acc.m2, __uint_as_float(acc.own | (acc.negw & kSign)), 0.0f);
-    st4(s.S, 4 * sidx4, Snew);
-    RowOut o;
-    o.Snew = Snew;
-    o.Sold = Sold;
-    o.oldbits = acc.oldbits;
-    o.ok = ((acc.negw | acc.flipw) & kSign) == 0u;
+    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) edge_chunk_ms<CBP_CHUNK, P, SW1, TRACK>(ent, e0, k0, L, g, s1, alpha, acc);
+    if (CBP_CHUNK > 2 && k0 + 2 <= dc) {
+        edge_chunk_ms<2, P, SW1, TRACK>(ent, e0, k0, L, g, s1, alpha, acc);
+        k0 += 2;
+    }
+    if (k0 < dc) edge_chunk_ms<1, P, SW1, TRACK>(ent, e0, k0, L, g, s1, alpha, acc);
+    uint32_t nw[P];
+    RowOut<P> o;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        nw[p] = acc.own[p] | (acc.negw[p] & kSign);
+        o.Snew[p] = make_float4(acc.m1[p], acc.m2[p], __uint_as_float(nw[p]), 0.0f);
+        o.Sold[p] = make_float4(om1[p], om2[p], __uint_as_float(oow[p]), 0.0f);
+        o.oldbits[p] = acc.oldbits[p];
+        o.ok[p] = ((acc.negw[p] | acc.flipw[p]) & kSign) == 0u;
+    }
+    st_rec<P>(g.S, Ly::SU * sidx, acc.m1, acc.m2, nw);
     return o;
 }
 
-// write hard bits (sign of Phi) of lane r's variables in row (e0, dc); returns the previous ones
-__device__ __forceinline__ uint32_t swap_row_bits(const int4* __restrict__ ent, int e0, int dc, int r, int Z,
-                                                  uint32_t bits, const SlotPtrs& s)
+// write hard bits (sign of Phi) of lane r's variables of frame p in row (e0, dc); returns the previous ones
+template <int P, int ALG>
+__device__ __forceinline__ uint32_t swap_row_bits(const int4* __restrict__ ent, int e0, int dc, int r, int Z, int p,
+                                                  uint32_t bits, const Grp<P, ALG>& g)
 {
     uint32_t prev = 0;
     for (int k = 0; k < dc; ++k) {
         const int v = lane_var(ent, e0 + k, r, Z);
-        const uint32_t w = __float_as_uint(s.QP()[v].y);
+        const uint32_t w = __float_as_uint(g.PH(v, p));
         prev |= (w >> 31) << k;
-        s.QP()[v].y = __uint_as_float((w & ~kSign) | (((bits >> k) & 1u) << 31));
+        g.PH(v, p) = __uint_as_float((w & ~kSign) | (((bits >> k) & 1u) << 31));
     }
     return prev;
 }
 
-// parity of lane r's checks over all rows, from the hard bits (sign of Phi)
+// parity of lane r's checks over all rows, from the hard bits (sign of Phi) of frame p
+template <int P, int ALG>
 __device__ __forceinline__ bool lane_syndrome(const int4* __restrict__ ent, const int32_t* row_ptr, int mb, int r,
-                                              int Z, const SlotPtrs& s)
+                                              int Z, int p, const Grp<P, ALG>& g)
 {
     uint32_t nz = 0;
     for (int i = 0; i < mb; ++i) {
         uint32_t par = 0;
-        for (int k = row_ptr[i]; k < row_ptr[i + 1]; ++k)
-            par ^= __float_as_uint(s.QP()[lane_var(ent, k, r, Z)].y) >> 31;
+        for (int k = row_ptr[i]; k < row_ptr[i + 1]; ++k) par ^= __float_as_uint(g.PH(lane_var(ent, k, r, Z), p)) >> 31;
         nz |= par;
     }
     return nz != 0u;
@@ -355,19 +530,24 @@ __device__ __forceinline__ uint32_t info_parity(const int4* __restrict__ ent, co
 }
 
 // ---------------------------------------------------------------- channel (a2-a4)
-template <bool MULTI>
-__device__ void channel_frame(const KernelArgs& a, const Team<MULTI>& tm, bool fresh, int64_t gframe,
-                              const int4* ent, const int32_t* row_ptr, const int16_t* pshift, const SlotPtrs& s,
-                              int s_words)
+// Frames p with fresh[p] of the group: info bits, encoding, BPSK/AWGN LLRs written into
+// the group state (Q_v = L_v, hard bit of L_v), R and the check records zeroed.
+template <bool MULTI, int P, int ALG>
+__device__ void channel_frames(const KernelArgs& a, const Team<MULTI>& tm, const bool (&fresh)[P],
+                               const int64_t (&fidx)[P], const int4* ent, const int32_t* row_ptr,
+                               const int16_t* pshift, const Grp<P, ALG>& g)
 {
+    using Ly = Lay<P, ALG>;
     const DevCode& C = a.code;
     const int Z = C.Z, r = tm.r;
-    const bool on = fresh && tm.lane_on;
-    float2* QP = s.QP();
-    const uint32_t flo = static_cast<uint32_t>(gframe), fhi = static_cast<uint32_t>(static_cast<uint64_t>(gframe) >> 32);
     const uint32_t k0 = static_cast<uint32_t>(a.seed), k1 = static_cast<uint32_t>(a.seed >> 32);
     // (a2) info words: word w = Philox(w/4, f_lo, f_hi, 0)[w%4]
-    if (on) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        if (!(fresh[p] && tm.lane_on)) continue;
+        const int64_t gframe = a.frame_begin + fidx[p];
+        const uint32_t flo = static_cast<uint32_t>(gframe), fhi = static_cast<uint32_t>(static_cast<uint64_t>(gframe) >> 32);
+        uint32_t* cw = g.cwp(p);
         const int nblk = (C.kwords + 3) / 4;
         for (int b = r; b < nblk; b += Z) {
             const u32x4 x = philox4x32_10(u32x4{static_cast<uint32_t>(b), flo, fhi, 0u}, k0, k1);
@@ -378,59 +558,70 @@ __device__ void channel_frame(const KernelArgs& a, const Team<MULTI>& tm, bool f
                 if (w < C.kwords) {
                     uint32_t word = xs[m];
                     if (w == C.kwords - 1 && (C.K & 31)) word &= (1u << (C.K & 31)) - 1u;
-                    s.cw[w] = word;
+                    cw[w] = word;
                 }
             }
         }
     }
     tm.sync();
-    // (a3) systematic part and p0 = XOR of the core rows' lambda (QP.x holds the symbol 1 - 2c)
-    if (on) {
-        for (int v = r; v < C.K; v += Z) QP[v].x = ((s.cw[v >> 5] >> (v & 31)) & 1u) ? -1.0f : 1.0f;
+    // (a3) systematic part and p0 = XOR of the core rows' lambda (Q holds the symbol 1 - 2c)
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        if (!(fresh[p] && tm.lane_on)) continue;
+        const uint32_t* cw = g.cwp(p);
+        for (int v = r; v < C.K; v += Z) g.Q(v, p) = ((cw[v >> 5] >> (v & 31)) & 1u) ? -1.0f : 1.0f;
         uint32_t p0 = 0;
         for (int i = 0; i < C.core; ++i) {
-            const uint32_t lam = info_parity(ent, row_ptr, i, r, Z, C.K, s.cw);
-            s.Sf()[i * Z + r] = __uint_as_float(lam);      // lambda_i[r] kept for the next pass (S is free here)
+            const uint32_t lam = info_parity(ent, row_ptr, i, r, Z, C.K, cw);
+            g.Sw(i * Z + r, 0, p) = __uint_as_float(lam);   // lambda_i[r] kept for the next pass (S is free here)
             p0 ^= lam;
         }
-        QP[C.kb * Z + r].x = p0 ? -1.0f : 1.0f;
+        g.Q(C.kb * Z + r, p) = p0 ? -1.0f : 1.0f;
     }
     tm.sync();
     // p_t = lambda_{t-1} ^ p_{t-1} ^ P^{s0} p0 (row t-1), extension p = lambda
-    if (on) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        if (!(fresh[p] && tm.lane_on)) continue;
         uint32_t pprev = 0;
         for (int t = 1; t < C.core; ++t) {
-            uint32_t pt = __float_as_uint(s.Sf()[(t - 1) * Z + r]);   // lambda_{t-1}[r]
+            uint32_t pt = __float_as_uint(g.Sw((t - 1) * Z + r, 0, p));   // lambda_{t-1}[r]
             if (t >= 2) pt ^= pprev;
             const int s0 = pshift[t - 1];
             if (s0 >= 0) {
                 int rr = r + s0;
                 rr = (rr >= Z) ? rr - Z : rr;
-                pt ^= QP[C.kb * Z + rr].x < 0.0f ? 1u : 0u;
+                pt ^= g.Q(C.kb * Z + rr, p) < 0.0f ? 1u : 0u;
             }
-            QP[(C.kb + t) * Z + r].x = pt ? -1.0f : 1.0f;
+            g.Q((C.kb + t) * Z + r, p) = pt ? -1.0f : 1.0f;
             pprev = pt;
         }
         for (int k = 0; k < C.mb - C.core; ++k) {
-            const uint32_t pe = info_parity(ent, row_ptr, C.core + k, r, Z, C.K, s.cw);
-            QP[(C.kb + C.core + k) * Z + r].x = pe ? -1.0f : 1.0f;
+            const uint32_t pe = info_parity(ent, row_ptr, C.core + k, r, Z, C.K, g.cwp(p));
+            g.Q((C.kb + C.core + k) * Z + r, p) = pe ? -1.0f : 1.0f;
         }
     }
     tm.sync();
     // transmitted codeword words
-    if (on) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        if (!(fresh[p] && tm.lane_on)) continue;
         for (int w = r; w < C.nwords; w += Z) {
             uint32_t word = 0;
             for (int b = 0; b < 32; ++b) {
                 const int v = 32 * w + b;
-                if (v < C.N && QP[v].x < 0.0f) word |= 1u << b;
+                if (v < C.N && g.Q(v, p) < 0.0f) word |= 1u << b;
             }
-            s.cw[w] = word;
+            g.cwp(p)[w] = word;
         }
     }
     tm.sync();
     // (a4) BPSK + AWGN + LLR: y = (1-2c) + sigma n, L = (2/sigma^2) y  (equ_s4e15, R17)
-    if (on) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        if (!(fresh[p] && tm.lane_on)) continue;
+        const int64_t gframe = a.frame_begin + fidx[p];
+        const uint32_t flo = static_cast<uint32_t>(gframe), fhi = static_cast<uint32_t>(static_cast<uint64_t>(gframe) >> 32);
         const int nblk = (C.N + 3) / 4;
         for (int b = r; b < nblk; b += Z) {
             const u32x4 x = philox4x32_10(u32x4{static_cast<uint32_t>(b), flo, fhi, 1u}, k0, k1);
@@ -441,39 +632,51 @@ __device__ void channel_frame(const KernelArgs& a, const Team<MULTI>& tm, bool f
             for (int m = 0; m < 4; ++m) {
                 const int v = 4 * b + m;
                 if (v >= C.N) break;
-                const float y = __fadd_rn(QP[v].x, __fmul_rn(a.sigma, n[m]));
+                const float y = __fadd_rn(g.Q(v, p), __fmul_rn(a.sigma, n[m]));
                 float Lv = __fmul_rn(a.scale, y);
                 if (a.llr_mode == 1) {
                     float qq = rintf(__fmul_rn(Lv, 4.0f));
                     qq = fminf(fmaxf(qq, -127.0f), 127.0f);
                     Lv = __fmul_rn(qq, 0.25f);
                 }
-                QP[v] = make_float2(Lv, Lv < 0.0f ? -0.0f : 0.0f);
+                g.Q(v, p) = Lv;
+                g.PH(v, p) = Lv < 0.0f ? -0.0f : 0.0f;
             }
         }
-        for (int e = r; e < C.E; e += Z) s.Rf()[e] = 0.0f;
-        for (int c = r; c < s_words; c += Z) s.Sf()[c] = 0.0f;
+        for (int e = r; e < C.E; e += Z) g.Rw(e, p) = 0.0f;
+        for (int c = r; c < C.M; c += Z)
+#pragma unroll
+            for (int k = 0; k < Ly::SW; ++k) g.Sw(c, k, p) = 0.0f;
     }
     tm.sync();
 }
 
 // ---------------------------------------------------------------- the kernel
-template <bool MULTI, bool SMEM, int MAXT, int ALG>
-__global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
+template <bool MULTI, bool SMEM, int MAXT, int ALG, int P>
+__global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ KernelArgs a)
 {
+    using Ly = Lay<P, ALG>;
     extern __shared__ __align__(16) uint32_t smem[];
     const DevCode& C = a.code;
     const int Z = C.Z, mb = C.mb;
 
-    // ---- stage the phi table and the schedule tables (a1)
+    // ---- stage the phi table and the schedule tables (a1).  The tables travel in the
+    // kernel parameters; reading them in the hot loop straight from the constant bank
+    // (CBP_SCHED_SMEM=0) measured 20% slower on C2 than from shared memory.
     float4* ptab = reinterpret_cast<float4*>(smem);
+    for (int k = threadIdx.x; k < kPhiSegs; k += blockDim.x) ptab[k] = C.phi_tab[k];
+#if CBP_SCHED_SMEM
     int4* ent = reinterpret_cast<int4*>(smem + 4 * kPhiSegs);
     int32_t* row_ptr = reinterpret_cast<int32_t*>(smem + 4 * kPhiSegs + 8 * C.nent);
     int16_t* pshift = reinterpret_cast<int16_t*>(row_ptr + mb + 1);
-    for (int k = threadIdx.x; k < kPhiSegs; k += blockDim.x) ptab[k] = C.phi_tab[k];
-    for (int k = threadIdx.x; k < 2 * C.nent; k += blockDim.x) ent[k] = C.ent[k];
-    for (int k = threadIdx.x; k <= mb; k += blockDim.x) row_ptr[k] = C.row_ptr[k];
-    for (int k = threadIdx.x; k < mb; k += blockDim.x) pshift[k] = C.pshift[k];
+    for (int k = threadIdx.x; k < 2 * C.nent; k += blockDim.x) ent[k] = a.ent[k];
+    for (int k = threadIdx.x; k <= mb; k += blockDim.x) row_ptr[k] = a.row_ptr[k];
+    for (int k = threadIdx.x; k < mb; k += blockDim.x) pshift[k] = a.pshift[k];
+#else
+    const int4* ent = a.ent;
+    const int32_t* row_ptr = a.row_ptr;
+    const int16_t* pshift = a.pshift;
+#endif
     Team<MULTI> tm;
     tm.nthreads = a.team_threads;
     tm.tidx = threadIdx.x / a.team_threads;
@@ -491,247 +694,112 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
     }
     tm.lane_on = tm.r < Z && tm.slot < a.F;
     const int r = tm.r;
-    const int s_words = ALG ? 4 * C.M : C.M;               // words of the per-check records
-    const Lane lane{r, 4 * r, 8 * r, Z, 4 * Z, 8 * Z, 8 * C.N, 4 * C.E, 4 * s_words, a.phi_m19, a.phi_one};
+    const Lane lane{r, r * Ly::QS, r * Ly::RS, Z * Ly::QS, Z * Ly::RS, Ly::QS * C.N, Ly::RS * C.E, Ly::SS * C.M,
+                    a.phi_m19, a.phi_one};
     uint32_t* ctl = smem + a.table_words + tm.tidx * kCtlTeamWords;
-    long long* ctl64 = reinterpret_cast<long long*>(ctl + 64);
+    long long* ctl64 = reinterpret_cast<long long*>(ctl + 128);
 
     const int nteams = blockDim.x / a.team_threads;
     float* sbase = SMEM ? reinterpret_cast<float*>(smem + a.table_words + nteams * kCtlTeamWords)
                         : a.gstate + static_cast<size_t>(blockIdx.x) * nteams * a.F * a.slot_words;
-    SlotPtrs s;
-    float* slot0 = sbase + static_cast<size_t>(tm.tidx * a.F + (tm.slot < a.F ? tm.slot : 0)) * a.slot_words;
-    // slot layout (word offsets; slot_words % 4 == 0): QP [2N] | pad to 4 | S [s_words] | R [E] | cw
-    const int s_off = (2 * C.N + 3) & ~3;                  // 16-byte aligned check records
-    s.qp = reinterpret_cast<char*>(slot0);
-    s.S = reinterpret_cast<char*>(slot0 + s_off);
-    s.R = reinterpret_cast<char*>(slot0 + s_off + s_words);
-    s.cw = reinterpret_cast<uint32_t*>(slot0 + s_off + s_words + C.E);
+    float* grp0 = sbase + static_cast<size_t>(tm.tidx * a.F + (tm.slot < a.F ? tm.slot : 0)) * a.slot_words;
+    // group layout (word offsets; slot_words % 4 == 0): QP [2PN] | pad to 4 | S [P SW M] | R [P E] | cw [P nwords]
+    Grp<P, ALG> g;
+    const int s_off = (2 * P * C.N + 3) & ~3;              // 16-byte aligned check records
+    g.qp = reinterpret_cast<char*>(grp0);
+    g.S = reinterpret_cast<char*>(grp0 + s_off);
+    g.R = reinterpret_cast<char*>(grp0 + s_off + P * Ly::SW * C.M);
+    g.cw = reinterpret_cast<uint32_t*>(grp0 + s_off + P * Ly::SW * C.M + P * C.E);
+    g.nwords = C.nwords;
     __syncthreads();
-    auto put_check = [&](const SlotPtrs& sp, int c, float4 v) {
-        if constexpr (ALG == 1) st4(sp.S, 16 * c, v);
-        else st1(sp.S, 4 * c, v.x);
+    auto put_check = [&](int p, int c, float4 v) {
+        g.Sw(c, 0, p) = v.x;
+        if constexpr (ALG == 1) {
+            g.Sw(c, 1, p) = v.y;
+            g.Sw(c, 2, p) = v.z;
+        }
     };
 
     const bool belief = a.stop_rule <= 1;
     const int W = (a.stop_rule == 1) ? C.N : C.M;            // R4 (N, M < 65536)
     const bool decoding = a.mode != MODE_CHANNEL;
 
-    // per-slot control (uniform over the slot's lanes)
-    bool active = false, exhausted = (tm.slot >= a.F), conv = false;
-    int64_t fidx = -1;
-    int ev_dc = 0, ev_part = 0, consec = 0;   // edge visits = ev_dc * Z + ev_part
-    int sweep = 1, fires = 0;
+    // per-frame control (uniform over the group's lanes)
+    bool active[P], exhausted[P], conv[P];
+    int64_t fidx[P];
+    int ev_dc[P], ev_part[P], consec[P], sweep[P], fires[P];   // edge visits = ev_dc * Z + ev_part
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        active[p] = conv[p] = false;
+        exhausted[p] = tm.slot >= a.F;
+        fidx[p] = -1;
+        ev_dc[p] = ev_part[p] = consec[p] = fires[p] = 0;
+        sweep[p] = 1;
+    }
     // per-lane counters (ber_sim)
     unsigned long long cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
-    for (;;) {
-        // ---- refill free slots from the frame queue
-        const bool need = !active && !exhausted;
-        long long f = -1;
-        if (need && r == 0) f = static_cast<long long>(atomicAdd(a.queue, 1ull));
-        if (MULTI) {
-            if (tm.tl == 0) ctl64[0] = f;
-            tm.sync();
-            f = ctl64[0];
-            tm.sync();
-        } else {
-            f = __shfl_sync(kFull, f, tm.lane_base);
-        }
-        bool fresh = false;
-        if (need) {
-            if (f < a.frames) {
-                active = fresh = true;
-                fidx = f;
-                conv = false;
-                ev_dc = ev_part = 0;
-                consec = 0;
-                sweep = 1;
-                fires = 0;
-            } else {
-                exhausted = true;
-            }
-        }
-        // ---- Step 1: initialisation (a4/a5)
-        if (a.mode == MODE_BER_SIM || a.mode == MODE_CHANNEL) {
-            if (tm.team_any(fresh))
-                channel_frame<MULTI>(a, tm, fresh, a.frame_begin + fidx, ent, row_ptr, pshift, s, s_words);
-        } else {
-            if (fresh && tm.lane_on) {
-                const size_t base = static_cast<size_t>(fidx) * a.ld;
-                for (int v = r; v < C.N; v += Z) {
-                    const float Lv = (a.mode == MODE_DECODE_I8) ? __fmul_rn(static_cast<float>(a.q[base + v]), a.qscale)
-                                                                : a.llr[base + v];
-                    s.QP()[v] = make_float2(Lv, Lv < 0.0f ? -0.0f : 0.0f);   // equ_s4e15, hard bit from L (R7)
-                }
-                for (int e = r; e < C.E; e += Z) s.Rf()[e] = 0.0f;   // equ_s4e17
-                for (int c = r; c < s_words; c += Z) s.Sf()[c] = 0.0f;   // equ_s4e16: Omega = inf <=> S = 0
-            }
-            tm.sync();
-        }
-        if (!tm.team_any(active)) break;
-
-        bool done = false;
-        if (decoding) {
-            // ---- Step 2: one sweep over the base rows (checks in ascending order)
-            for (int i = 0; i < mb; ++i) {
-                const bool live = active && !conv;
-                if (!tm.team_any(live)) break;
-                const int e0 = row_ptr[i], dc = row_ptr[i + 1] - e0;
-                RowOut ro;
-                ro.ok = true;
-                ro.oldbits = 0;
-                ro.Snew = ro.Sold = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-                if (live && tm.lane_on) {
-                    // the window can only fill in this row if consec + Z >= W (R4); otherwise
-                    // no rollback information is needed
-                    const bool track = belief && consec + Z >= W;
-                    const int sidx4 = 4 * (i * Z + r);
-                    if (sweep == 1) {
-                        if constexpr (ALG == 1)
-                            ro = track ? process_row_ms<true, true>(ent, e0, dc, sidx4, lane, s, a.alpha)
-                                       : process_row_ms<true, false>(ent, e0, dc, sidx4, lane, s, a.alpha);
-                        else
-                            ro = track ? process_row<true, true>(ent, ptab, e0, dc, sidx4, lane, s)
-                                       : process_row<true, false>(ent, ptab, e0, dc, sidx4, lane, s);
-                    } else {
-                        if constexpr (ALG == 1)
-                            ro = track ? process_row_ms<false, true>(ent, e0, dc, sidx4, lane, s, a.alpha)
-                                       : process_row_ms<false, false>(ent, e0, dc, sidx4, lane, s, a.alpha);
-                        else
-                            ro = track ? process_row<false, true>(ent, ptab, e0, dc, sidx4, lane, s)
-                                       : process_row<false, false>(ent, ptab, e0, dc, sidx4, lane, s);
-                    }
-                }
-                // ---- Step 2(3): stopping criterion, counted per check update (R4, R5)
-                int first_bad = Z, last_bad = -1;   // first / last unclean check of the row
-                if (MULTI) {
-                    const int buf = (i & 1) * 32;
-                    const unsigned m = __ballot_sync(kFull, tm.lane_on && !ro.ok);
-                    if ((tm.tl & 31) == 0) ctl[buf + (tm.tl >> 5)] = m;
-                    tm.sync();
-                    if (belief) {
-                        const int nw = tm.nthreads >> 5;
-                        for (int w = 0; w < nw; ++w) {
-                            const unsigned mw = ctl[buf + w];
-                            if (mw) {
-                                first_bad = min(first_bad, 32 * w + __ffs(mw) - 1);
-                                last_bad = max(last_bad, 32 * w + 31 - __clz(mw));
-                            }
-                        }
-                    }
-                } else {
-                    __syncwarp();
-                    const unsigned m = (__ballot_sync(kFull, tm.lane_on && !ro.ok) & tm.slot_mask) >> tm.lane_base;
-                    if (m) {
-                        first_bad = __ffs(m) - 1;
-                        last_bad = 31 - __clz(m);
-                    }
-                }
-                bool fire = false;
-                int rstar = 0;
-                if (live && belief) {
-                    rstar = W - consec - 1;           // the window fills at check i*Z + rstar
-                    fire = rstar < Z && first_bad > rstar;
-                    if (!fire) consec = (last_bad < 0) ? consec + Z : (Z - 1 - last_bad);
-                }
-                if (live && !fire) ev_dc += dc;
-                if (tm.team_any(fire)) {
-                    // the sequential decoder stops right after check i*Z + rstar: lanes r > rstar
-                    // show their pre-row hard bits and S while the syndrome is verified (R5)
-                    const bool back = fire && tm.lane_on && r > rstar;
-                    uint32_t newbits = 0;
-                    if (back) {
-                        newbits = swap_row_bits(ent, e0, dc, r, Z, ro.oldbits, s);
-                        put_check(s, i * Z + r, ro.Sold);
-                    }
-                    tm.sync();
-                    const bool nz = tm.slot_any(fire && tm.lane_on && lane_syndrome(ent, row_ptr, mb, r, Z, s));
-                    if (fire) {
-                        if (!nz) {
-                            conv = true;             // converged: output = state after check i*Z + rstar
-                            ev_part += dc * (rstar + 1);
-                        } else {
-                            fires += 1;              // undetected fire: resume (R5)
-                            ev_dc += dc;
-                            consec = Z - 1 - max(last_bad, rstar);
-                            if (back) {
-                                swap_row_bits(ent, e0, dc, r, Z, newbits, s);
-                                put_check(s, i * Z + r, ro.Snew);
-                            }
-                        }
-                    }
-                    tm.sync();
-                }
-            }
-            // ---- end of sweep
-            const bool want_syn = active && !conv && a.stop_rule == 2;
-            if (tm.team_any(want_syn)) {
-                tm.sync();
-                const bool nz = tm.slot_any(want_syn && tm.lane_on && lane_syndrome(ent, row_ptr, mb, r, Z, s));
-                if (want_syn && !nz) conv = true;
-            }
-            done = active && (conv || sweep >= a.max_iter);
-            if (active && !done) sweep += 1;
-        } else {
-            done = active;
-        }
-
-        // ---- Step 3: outputs of finished frames (a8)
-        if (tm.team_any(done)) {
-            tm.sync();
-            bool synd_zero = conv;
-            const bool need_syn = done && !conv && decoding;
+    // ---- Step 3: outputs of the frames with done[p] (a8); team-uniform call
+    auto finish = [&](const bool (&done)[P]) {
+        bool anyd = false;
+#pragma unroll
+        for (int p = 0; p < P; ++p) anyd |= done[p];
+        if (!tm.team_any(anyd)) return;
+        tm.sync();
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            bool synd_zero = conv[p];
+            const bool need_syn = done[p] && !conv[p] && decoding;
             if (tm.team_any(need_syn)) {
-                const bool nz = tm.slot_any(need_syn && tm.lane_on && lane_syndrome(ent, row_ptr, mb, r, Z, s));
+                const bool nz = tm.slot_any(need_syn && tm.lane_on && lane_syndrome<P, ALG>(ent, row_ptr, mb, r, Z, p, g));
                 if (need_syn) synd_zero = !nz;
             }
-            const int iters = conv ? sweep : a.max_iter;
-            const uint8_t flags = static_cast<uint8_t>((conv ? 1 : 0) | (synd_zero ? 2 : 0) | (fires > 0 ? 4 : 0));
-            const float2* QP = s.QP();
+            const int iters = conv[p] ? sweep[p] : a.max_iter;
+            const uint8_t flags = static_cast<uint8_t>((conv[p] ? 1 : 0) | (synd_zero ? 2 : 0) | (fires[p] > 0 ? 4 : 0));
+            const int64_t evs = static_cast<int64_t>(ev_dc[p]) * Z + ev_part[p];
             if (a.mode == MODE_DECODE_F32 || a.mode == MODE_DECODE_I8) {
-                if (done && tm.lane_on) {
-                    uint32_t* out = a.bits + static_cast<size_t>(fidx) * a.ld_words;
+                if (done[p] && tm.lane_on) {
+                    uint32_t* out = a.bits + static_cast<size_t>(fidx[p]) * a.ld_words;
                     for (int w = r; w < a.ld_words; w += Z) {
                         uint32_t word = 0;
                         if (w < C.nwords)
                             for (int b = 0; b < 32; ++b) {
                                 const int v = 32 * w + b;
-                                if (v < C.N) word |= (__float_as_uint(QP[v].y) >> 31) << b;
+                                if (v < C.N) word |= (__float_as_uint(g.PH(v, p)) >> 31) << b;
                             }
                         out[w] = word;
                     }
                     if (a.omega) {
-                        float* om = a.omega + static_cast<size_t>(fidx) * C.M;
+                        float* om = a.omega + static_cast<size_t>(fidx[p]) * C.M;
                         for (int c = r; c < C.M; c += Z) {
                             float Sv, m;
                             if constexpr (ALG == 1) {
-                                const float4 cs = reinterpret_cast<const float4*>(s.S)[c];
-                                Sv = cs.z;                               // sign bit = sign of Omega
-                                m = cs.x;                                // Omega = sgn * min (reading R20)
+                                Sv = g.Sw(c, 2, p);                      // sign bit = sign of Omega
+                                m = g.Sw(c, 0, p);                       // Omega = sgn * min (reading R20)
                             } else {
-                                Sv = s.Sf()[c];
-                                m = phi32(fabsf(Sv), ptab);               // Omega = sgn * phi(S)
+                                Sv = g.Sw(c, 0, p);
+                                m = phi32(fabsf(Sv), ptab);              // Omega = sgn * phi(S)
                             }
                             om[c] = (__float_as_uint(Sv) >> 31) ? -m : m;
                         }
                     }
                     if (r == 0) {
-                        a.iters[fidx] = iters;
-                        a.flags[fidx] = flags;
-                        if (a.ev) a.ev[fidx] = static_cast<int64_t>(ev_dc) * Z + ev_part;
+                        a.iters[fidx[p]] = iters;
+                        a.flags[fidx[p]] = flags;
+                        if (a.ev) a.ev[fidx[p]] = evs;
                     }
                 }
             } else if (a.mode == MODE_BER_SIM) {
                 bool info_err = false, cw_err = false;
-                if (done && tm.lane_on) {
+                if (done[p] && tm.lane_on) {
+                    const uint32_t* cw = g.cwp(p);
                     for (int w = r; w < C.nwords; w += Z) {
                         uint32_t word = 0;
                         for (int b = 0; b < 32; ++b) {
                             const int v = 32 * w + b;
-                            if (v < C.N) word |= (__float_as_uint(QP[v].y) >> 31) << b;
+                            if (v < C.N) word |= (__float_as_uint(g.PH(v, p)) >> 31) << b;
                         }
-                        const uint32_t d = word ^ s.cw[w];
+                        const uint32_t d = word ^ cw[w];
                         uint32_t im = 0;
                         if (32 * w + 32 <= C.K) im = kFull;
                         else if (32 * w < C.K) im = (1u << (C.K - 32 * w)) - 1u;
@@ -742,29 +810,256 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const KernelArgs a)
                 }
                 const bool fe = tm.slot_any(info_err);
                 const bool ce = tm.slot_any(cw_err);
-                if (done && r == 0) {
+                if (done[p] && r == 0) {
                     cnt[0] += 1;
                     cnt[2] += fe;
                     cnt[3] += ce;
                     cnt[4] += iters;
-                    cnt[5] += static_cast<int64_t>(ev_dc) * Z + ev_part;
-                    cnt[6] += conv ? 0 : 1;
-                    cnt[7] += fires;
+                    cnt[5] += evs;
+                    cnt[6] += conv[p] ? 0 : 1;
+                    cnt[7] += fires[p];
                 }
             } else {  // MODE_CHANNEL
-                if (done && tm.lane_on) {
+                if (done[p] && tm.lane_on) {
                     if (a.llr_out) {
-                        float* out = a.llr_out + static_cast<size_t>(fidx) * a.ld;
-                        for (int v = r; v < C.N; v += Z) out[v] = QP[v].x;
+                        float* out = a.llr_out + static_cast<size_t>(fidx[p]) * a.ld;
+                        for (int v = r; v < C.N; v += Z) out[v] = g.Q(v, p);
                     }
                     if (a.cw_out) {
-                        uint32_t* out = a.cw_out + static_cast<size_t>(fidx) * a.ld_words;
-                        for (int w = r; w < a.ld_words; w += Z) out[w] = (w < C.nwords) ? s.cw[w] : 0u;
+                        uint32_t* out = a.cw_out + static_cast<size_t>(fidx[p]) * a.ld_words;
+                        for (int w = r; w < a.ld_words; w += Z) out[w] = (w < C.nwords) ? g.cwp(p)[w] : 0u;
                     }
                 }
             }
-            if (done) active = false;
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+            if (done[p]) active[p] = false;
+        tm.sync();
+    };
+
+    for (;;) {
+        // ---- refill free frame slots from the queue
+        bool fresh[P], any_fresh = false;
+        long long f[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const bool need = !active[p] && !exhausted[p];
+            f[p] = -1;
+            if (need && r == 0) f[p] = static_cast<long long>(atomicAdd(a.queue, 1ull));
+        }
+        if (MULTI) {
+            if (tm.tl == 0)
+#pragma unroll
+                for (int p = 0; p < P; ++p) ctl64[p] = f[p];
             tm.sync();
+#pragma unroll
+            for (int p = 0; p < P; ++p) f[p] = ctl64[p];
+            tm.sync();
+        } else {
+#pragma unroll
+            for (int p = 0; p < P; ++p) f[p] = __shfl_sync(kFull, f[p], tm.lane_base);
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const bool need = !active[p] && !exhausted[p];
+            fresh[p] = false;
+            if (need) {
+                if (f[p] < a.frames) {
+                    active[p] = fresh[p] = true;
+                    fidx[p] = f[p];
+                    conv[p] = false;
+                    ev_dc[p] = ev_part[p] = 0;
+                    consec[p] = 0;
+                    sweep[p] = 1;
+                    fires[p] = 0;
+                } else {
+                    exhausted[p] = true;
+                }
+            }
+            any_fresh |= fresh[p];
+        }
+        // ---- Step 1: initialisation (a4/a5)
+        if (a.mode == MODE_BER_SIM || a.mode == MODE_CHANNEL) {
+            if (tm.team_any(any_fresh)) channel_frames<MULTI, P, ALG>(a, tm, fresh, fidx, ent, row_ptr, pshift, g);
+        } else {
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                if (!(fresh[p] && tm.lane_on)) continue;
+                const size_t base = static_cast<size_t>(fidx[p]) * a.ld;
+                for (int v = r; v < C.N; v += Z) {
+                    const float Lv = (a.mode == MODE_DECODE_I8) ? __fmul_rn(static_cast<float>(a.q[base + v]), a.qscale)
+                                                                : a.llr[base + v];
+                    g.Q(v, p) = Lv;                                  // equ_s4e15
+                    g.PH(v, p) = Lv < 0.0f ? -0.0f : 0.0f;           // hard bit from L (R7)
+                }
+                for (int e = r; e < C.E; e += Z) g.Rw(e, p) = 0.0f;   // equ_s4e17
+                for (int c = r; c < C.M; c += Z)                      // equ_s4e16: Omega = inf <=> S = 0
+#pragma unroll
+                    for (int k = 0; k < Ly::SW; ++k) g.Sw(c, k, p) = 0.0f;
+            }
+            tm.sync();
+        }
+        bool any_active = false;
+#pragma unroll
+        for (int p = 0; p < P; ++p) any_active |= active[p];
+        if (!tm.team_any(any_active)) break;
+
+        if (decoding) {
+            // ---- Step 2: one sweep over the base rows (checks in ascending order).  A frame
+            // that converges mid-sweep is finished at once; its lanes then idle on garbage
+            // state (never read again) while the other frame of the group continues.
+            for (int i = 0; i < mb; ++i) {
+                bool live = false;
+#pragma unroll
+                for (int p = 0; p < P; ++p) live |= active[p];
+                if (!tm.team_any(live)) break;
+                const int e0 = row_ptr[i], dc = row_ptr[i + 1] - e0;
+                RowOut<P> ro;
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    ro.ok[p] = true;
+                    ro.oldbits[p] = 0;
+                    ro.Snew[p] = ro.Sold[p] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                }
+                if (live && tm.lane_on) {
+                    // the window can only fill in this row if consec + Z >= W (R4); otherwise
+                    // no rollback information is needed
+                    bool s1[P], sw1 = false, track = false;
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        s1[p] = active[p] && sweep[p] == 1;
+                        sw1 |= s1[p];
+                        track |= active[p] && belief && consec[p] + Z >= W;
+                    }
+                    const int sidx = (i * Z + r) * Ly::RS;
+                    if (sw1) {
+                        if constexpr (ALG == 1)
+                            ro = track ? process_row_ms<P, true, true>(ent, e0, dc, sidx, lane, g, s1, a.alpha)
+                                       : process_row_ms<P, true, false>(ent, e0, dc, sidx, lane, g, s1, a.alpha);
+                        else
+                            ro = track ? process_row<P, true, true>(ent, ptab, e0, dc, sidx, lane, g, s1)
+                                       : process_row<P, true, false>(ent, ptab, e0, dc, sidx, lane, g, s1);
+                    } else {
+                        if constexpr (ALG == 1)
+                            ro = track ? process_row_ms<P, false, true>(ent, e0, dc, sidx, lane, g, s1, a.alpha)
+                                       : process_row_ms<P, false, false>(ent, e0, dc, sidx, lane, g, s1, a.alpha);
+                        else
+                            ro = track ? process_row<P, false, true>(ent, ptab, e0, dc, sidx, lane, g, s1)
+                                       : process_row<P, false, false>(ent, ptab, e0, dc, sidx, lane, g, s1);
+                    }
+                }
+                // ---- Step 2(3): stopping criterion, counted per check update (R4, R5)
+                int first_bad[P], last_bad[P];   // first / last unclean check of the row
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    first_bad[p] = Z;
+                    last_bad[p] = -1;
+                }
+                if (MULTI) {
+                    const int buf = (i & 1) * 64;
+                    const int nw = tm.nthreads >> 5;
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        const unsigned m = __ballot_sync(kFull, tm.lane_on && !ro.ok[p]);
+                        if ((tm.tl & 31) == 0) ctl[buf + 32 * p + (tm.tl >> 5)] = m;
+                    }
+                    tm.sync();
+                    if (belief)
+#pragma unroll
+                        for (int p = 0; p < P; ++p)
+                            for (int w = 0; w < nw; ++w) {
+                                const unsigned mw = ctl[buf + 32 * p + w];
+                                if (mw) {
+                                    first_bad[p] = min(first_bad[p], 32 * w + __ffs(mw) - 1);
+                                    last_bad[p] = max(last_bad[p], 32 * w + 31 - __clz(mw));
+                                }
+                            }
+                } else {
+                    __syncwarp();
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        const unsigned m = (__ballot_sync(kFull, tm.lane_on && !ro.ok[p]) & tm.slot_mask) >> tm.lane_base;
+                        if (m) {
+                            first_bad[p] = __ffs(m) - 1;
+                            last_bad[p] = 31 - __clz(m);
+                        }
+                    }
+                }
+                bool fire[P], any_fire = false;
+                int rstar[P];
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    fire[p] = false;
+                    rstar[p] = 0;
+                    if (active[p] && belief) {
+                        rstar[p] = W - consec[p] - 1;   // the window fills at check i*Z + rstar
+                        fire[p] = rstar[p] < Z && first_bad[p] > rstar[p];
+                        if (!fire[p]) consec[p] = (last_bad[p] < 0) ? consec[p] + Z : (Z - 1 - last_bad[p]);
+                    }
+                    if (active[p] && !fire[p]) ev_dc[p] += dc;
+                    any_fire |= fire[p];
+                }
+                if (tm.team_any(any_fire)) {
+                    // the sequential decoder stops right after check i*Z + rstar: lanes r > rstar
+                    // show their pre-row hard bits and S while the syndrome is verified (R5)
+                    bool back[P], conv_now[P];
+                    uint32_t newbits[P];
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        back[p] = fire[p] && tm.lane_on && r > rstar[p];
+                        newbits[p] = 0;
+                        if (back[p]) {
+                            newbits[p] = swap_row_bits<P, ALG>(ent, e0, dc, r, Z, p, ro.oldbits[p], g);
+                            put_check(p, i * Z + r, ro.Sold[p]);
+                        }
+                    }
+                    tm.sync();
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        const bool nz =
+                            tm.slot_any(fire[p] && tm.lane_on && lane_syndrome<P, ALG>(ent, row_ptr, mb, r, Z, p, g));
+                        conv_now[p] = false;
+                        if (fire[p]) {
+                            if (!nz) {
+                                conv[p] = conv_now[p] = true;   // converged: output = state after check i*Z + rstar
+                                ev_part[p] += dc * (rstar[p] + 1);
+                            } else {
+                                fires[p] += 1;                  // undetected fire: resume (R5)
+                                ev_dc[p] += dc;
+                                consec[p] = Z - 1 - max(last_bad[p], rstar[p]);
+                                if (back[p]) {
+                                    swap_row_bits<P, ALG>(ent, e0, dc, r, Z, p, newbits[p], g);
+                                    put_check(p, i * Z + r, ro.Snew[p]);
+                                }
+                            }
+                        }
+                    }
+                    tm.sync();
+                    finish(conv_now);
+                }
+            }
+            // ---- end of sweep
+            bool done[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const bool want_syn = active[p] && a.stop_rule == 2;
+                if (tm.team_any(want_syn)) {
+                    tm.sync();
+                    const bool nz = tm.slot_any(want_syn && tm.lane_on && lane_syndrome<P, ALG>(ent, row_ptr, mb, r, Z, p, g));
+                    if (want_syn && !nz) conv[p] = true;
+                }
+                done[p] = active[p] && (conv[p] || sweep[p] >= a.max_iter);
+            }
+            finish(done);
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+                if (active[p]) sweep[p] += 1;
+        } else {
+            bool done[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) done[p] = active[p];
+            finish(done);
         }
     }
 
@@ -824,39 +1119,61 @@ int launch_phi_table(float4* out, void* stream)
 }
 
 // ---------------------------------------------------------------- host-side launch
-template <bool MULTI, bool SMEM, int MAXT>
+// Instantiations: P = 1 for every geometry (state in smem or global, warp or multi-warp
+// teams up to 1024 threads); P = 2 only with state in smem and at most 256 threads.
+template <bool MULTI, bool SMEM, int MAXT, int P>
 static int launch_t(const KernelArgs& a, const Geometry& g, int grid, cudaStream_t st)
 {
-    auto k = (g.alg == 1) ? cbp_kernel<MULTI, SMEM, MAXT, 1> : cbp_kernel<MULTI, SMEM, MAXT, 0>;
+    auto k = (g.alg == 1) ? cbp_kernel<MULTI, SMEM, MAXT, 1, P> : cbp_kernel<MULTI, SMEM, MAXT, 0, P>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
     k<<<grid, g.threads, g.smem_bytes, st>>>(a);
     return static_cast<int>(cudaGetLastError());
 }
 
-template <bool MULTI, bool SMEM, int MAXT>
+template <bool MULTI, bool SMEM, int MAXT, int P>
 static int occ_t(const Geometry& g, int* out)
 {
-    auto k = (g.alg == 1) ? cbp_kernel<MULTI, SMEM, MAXT, 1> : cbp_kernel<MULTI, SMEM, MAXT, 0>;
+    auto k = (g.alg == 1) ? cbp_kernel<MULTI, SMEM, MAXT, 1, P> : cbp_kernel<MULTI, SMEM, MAXT, 0, P>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
     return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, g.threads, g.smem_bytes));
 }
 
+template <template <bool, bool, int, int> class Fn, typename... Args>
+static int dispatch(const Geometry& g, Args... args)
+{
+    if (g.P == 2) {
+        if (!g.state_in_smem || g.threads > 256) return static_cast<int>(cudaErrorInvalidConfiguration);
+        return g.multi ? Fn<true, true, 256, 2>::run(g, args...) : Fn<false, true, 256, 2>::run(g, args...);
+    }
+    if (!g.multi) return g.state_in_smem ? Fn<false, true, 512, 1>::run(g, args...) : Fn<false, false, 512, 1>::run(g, args...);
+    if (g.threads <= 512)
+        return g.state_in_smem ? Fn<true, true, 512, 1>::run(g, args...) : Fn<true, false, 512, 1>::run(g, args...);
+    return g.state_in_smem ? Fn<true, true, 1024, 1>::run(g, args...) : Fn<true, false, 1024, 1>::run(g, args...);
+}
+
+template <bool MULTI, bool SMEM, int MAXT, int P>
+struct LaunchFn {
+    static int run(const Geometry& g, const KernelArgs* a, int grid, cudaStream_t st)
+    {
+        return launch_t<MULTI, SMEM, MAXT, P>(*a, g, grid, st);
+    }
+};
+
+template <bool MULTI, bool SMEM, int MAXT, int P>
+struct OccFn {
+    static int run(const Geometry& g, int* out) { return occ_t<MULTI, SMEM, MAXT, P>(g, out); }
+};
+
 int launch_cbp(const KernelArgs& a, const Geometry& g, int grid, void* stream)
 {
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (!g.multi) return g.state_in_smem ? launch_t<false, true, 512>(a, g, grid, st) : launch_t<false, false, 512>(a, g, grid, st);
-    if (g.threads <= 512)
-        return g.state_in_smem ? launch_t<true, true, 512>(a, g, grid, st) : launch_t<true, false, 512>(a, g, grid, st);
-    return g.state_in_smem ? launch_t<true, true, 1024>(a, g, grid, st) : launch_t<true, false, 1024>(a, g, grid, st);
+    return dispatch<LaunchFn>(g, &a, grid, static_cast<cudaStream_t>(stream));
 }
 
 int occupancy_ctas_per_sm(const Geometry& g, int* out)
 {
-    if (!g.multi) return g.state_in_smem ? occ_t<false, true, 512>(g, out) : occ_t<false, false, 512>(g, out);
-    if (g.threads <= 512) return g.state_in_smem ? occ_t<true, true, 512>(g, out) : occ_t<true, false, 512>(g, out);
-    return g.state_in_smem ? occ_t<true, true, 1024>(g, out) : occ_t<true, false, 1024>(g, out);
+    return dispatch<OccFn>(g, out);
 }
 
 }  // namespace cbp

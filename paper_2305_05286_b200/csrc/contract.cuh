@@ -143,6 +143,10 @@ __device__ __forceinline__ float4 phi_segment_coeffs(int seg)
 // (exhaustive check, tests/test_oracle_contract.py), so results are identical.
 // m19 = 0x7ffff and one = 0x3f800000 are passed in registers so that
 // (b & m19) | one is a single LOP3 (immediates would take two).
+// x >= 2 without the XU pipe: m = fma_rz(x, 8, 2^23 - 16) = 2^23 + floor(8x - 16)
+// exactly (the fma is exact before its one rounding toward zero, ulp 1 in
+// [2^23, 2^24)), so seg = bits(m) - bits(2^23) + 704 and u = fma(x, 8, -(16 + i))
+// = t - i exactly: the contract's i = (int)t and u = t - (float)i, bit for bit.
 __device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab, uint32_t m19, uint32_t one)
 {
     x = fminf(fmaxf(x, kPhiLo), kPhiHi);
@@ -151,11 +155,11 @@ __device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab, 
     uint32_t ub;
     asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(ub) : "r"(b), "r"(m19), "r"(one));   // (b & m19) | one
     const float u_lo = __fsub_rn(__uint_as_float(ub), 1.0f);   // u/16, see phi_segment_coeffs
-    const float t = __fmaf_rn(x, 8.0f, -16.0f);
-    const int i = static_cast<int>(t);
-    const float u_hi = __fsub_rn(t, static_cast<float>(i));
+    const float m = __fmaf_rz(x, 8.0f, 8388592.0f);
+    const float u_hi = __fmaf_rn(x, 8.0f, __fsub_rn(8388592.0f, m));
+    const int seg_hi = static_cast<int>(__float_as_uint(m)) - (0x4b000000 - 704);
     const bool hi = x >= 2.0f;
-    const int seg = hi ? 704 + i : seg_lo;
+    const int seg = hi ? seg_hi : seg_lo;
     const float u = hi ? u_hi : u_lo;
     CBP_CHECK(seg >= 0 && seg < kPhiSegs);
     const float4 c = tab[seg];

@@ -19,15 +19,33 @@ def _need_gpu():
         pytest.skip("no CUDA device")
 
 
-@pytest.fixture(scope="module")
-def codes():
+@pytest.fixture(scope="module", params=[1, 2], ids=["P1", "P2"])
+def fpl(request):
+    """Frames per lane of the kernel geometry: every parity test runs
+    with one frame per lane and with two interleaved frames per lane."""
     _need_gpu()
+    return request.param
+
+
+def make_code(base, Z, fpl):
+    try:
+        return cbp.Code(base, Z, frames_per_lane=fpl)
+    except cbp.CbpError as e:
+        if fpl == 2 and "two frames per lane" in str(e):
+            pytest.skip("two frames per lane need the state in shared memory (Z <= 256)")
+        raise
+
+
+@pytest.fixture(scope="module")
+def codes(fpl):
     cache = {}
 
     def get(name):
         if name not in cache:
             base, Z = inputs.config_base(name)
-            cache[name] = (cbp.Code(base, Z), oracle.OracleCode(base, Z))
+            cache[name] = (make_code(base, Z, fpl), oracle.OracleCode(base, Z))
+        g = cache[name][0]
+        assert g.launch_info()["frames_per_lane"] == fpl
         return cache[name]
     return get
 
@@ -121,12 +139,11 @@ def test_decode_parity_stop_rules(codes, rule, max_iter):
     assert_same(gpu_decode(g, llr, max_iter, rule), o.decode(llr, max_iter, rule, want_omega=True), o.N)
 
 
-def test_decode_parity_degree_one_and_mid_row_stops(codes):
+def test_decode_parity_degree_one_and_mid_row_stops(fpl):
     """C4-like degree-1 extension rows (reading R3) and many belief fires that
     fail verification (mid-row stop + rollback path, reading R5)."""
-    _need_gpu()
     base = inputs.construct_base((8, 14, 8, 4, 0, 3, 3), 1)
-    g, o = cbp.Code(base, 8), oracle.OracleCode(base, 8)
+    g, o = make_code(base, 8, fpl), oracle.OracleCode(base, 8)
     for eb in (1.0, 3.0, 5.0):
         llr, _ = o.channel(eb, seed=5, frame_begin=0, frames=600)
         for rule in (0, 1, 2, 3):
@@ -279,18 +296,18 @@ def test_minsum_stop_rules_and_extremes(codes, rule):
         assert (go["omega"].view(np.uint32) == oo["omega"].view(np.uint32)).all()
 
 
-def test_minsum_multi_warp_team_and_global_state(codes):
+def test_minsum_multi_warp_team_and_global_state(codes, fpl):
     """Z > 32 (multi-warp teams) and Z = 384 with the state in global memory."""
-    g, o = codes("C4")
-    llr, _ = o.channel(1.5, seed=13, frame_begin=0, frames=4)
-    oo = o.decode(llr, 20, oracle.STOP_SYNDROME, oracle.MINSUM, want_omega=True, alpha=0.75)
-    assert_same(gpu_decode(g, llr, 20, oracle.STOP_SYNDROME, alpha=0.75, **MS), oo, o.N, omega=False)
     base = inputs.construct_base((6, 18, 96, 6, 1, 2, 4), 2)
-    g2, o2 = cbp.Code(base, 96), oracle.OracleCode(base, 96)
+    g2, o2 = make_code(base, 96, fpl), oracle.OracleCode(base, 96)
     llr, _ = o2.channel(2.0, seed=14, frame_begin=0, frames=60)
     for rule in (0, 2):
         oo = o2.decode(llr, 15, rule, oracle.MINSUM, want_omega=True, alpha=0.75)
         assert_same(gpu_decode(g2, llr, 15, rule, alpha=0.75, **MS), oo, o2.N)
+    g, o = codes("C4")
+    llr, _ = o.channel(1.5, seed=13, frame_begin=0, frames=4)
+    oo = o.decode(llr, 20, oracle.STOP_SYNDROME, oracle.MINSUM, want_omega=True, alpha=0.75)
+    assert_same(gpu_decode(g, llr, 20, oracle.STOP_SYNDROME, alpha=0.75, **MS), oo, o.N, omega=False)
 
 
 @pytest.mark.parametrize("name,ebn0,frames,llr_mode", [("C2", 2.0, 2000, 0), ("C2", 2.5, 1000, 1),
@@ -303,7 +320,7 @@ def test_minsum_ber_sim_parity(codes, name, ebn0, frames, llr_mode):
     assert list(got) == list(want), dict(zip(oracle.COUNT_NAMES, zip(got, want)))
 
 
-def test_minsum_rejects_bad_options(codes):
+def test_minsum_rejects_bad_options(codes, fpl):
     g, o = codes("C2")
     x = torch.zeros((2, 648), dtype=torch.float32, device="cuda")
     for a in (0.0, -0.5, 1.5, float("nan")):
@@ -313,7 +330,7 @@ def test_minsum_rejects_bad_options(codes):
         g.decode(x, 5, algorithm=7)
     # a degree-1 check row has no leave-one-out minimum: min-sum is refused, log-tanh decodes
     base = np.array([[0, 1, -1, 2], [-1, 2, 0, -1], [-1, -1, 3, -1]], np.int16)   # last base row: degree 1
-    g1 = cbp.Code(base, 8)
+    g1 = make_code(base, 8, fpl)
     y = torch.zeros((2, 32), dtype=torch.float32, device="cuda")
     g1.decode(y, 5)
     with pytest.raises(RuntimeError):

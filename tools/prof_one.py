@@ -25,11 +25,12 @@ ap.add_argument("--mode", default="ber", choices=["ber", "decode"])
 ap.add_argument("--rule", type=int, default=0)
 ap.add_argument("--alg", type=int, default=0, help="0 log-tanh, 1 normalized min-sum")
 ap.add_argument("--alpha", type=float, default=0.75)
+ap.add_argument("--fpl", type=int, default=0, help="frames per lane: 0 auto, 1, 2")
 a = ap.parse_args()
 ALG = dict(algorithm=a.alg, alpha=a.alpha)
 cfg = inputs.CONFIGS[a.config]
 base, Z = inputs.config_base(a.config)
-g = cbp.Code(base, Z)
+g = cbp.Code(base, Z, frames_per_lane=a.fpl)
 print(g.launch_info())
 if a.mode == "decode":
     llr, _ = g.channel(a.ebn0, 1, 0, a.frames, want_cw=False)
@@ -40,11 +41,13 @@ while time.perf_counter() < t_end:
     g.ber_sim(a.ebn0, 1, 0, a.frames, cfg.max_iter, stop_rule=a.rule, **ALG)
     torch.cuda.synchronize()
 best = None
+cnt = torch.zeros(8, dtype=torch.int64, device="cuda")
 for _ in range(a.reps):
+    cnt.zero_()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     if a.mode == "ber":
-        c = g.ber_sim(a.ebn0, 1, 0, a.frames, cfg.max_iter, stop_rule=a.rule, **ALG)
+        c = g.ber_sim(a.ebn0, 1, 0, a.frames, cfg.max_iter, stop_rule=a.rule, counts=cnt, **ALG)
     else:
         out = g.decode(llr, cfg.max_iter, a.rule, ev=True, **ALG)
     e1.record()
