@@ -52,12 +52,16 @@ struct DeviceGuard {
 // phi contract v2 table, built once per device by phi_table_kernel
 std::mutex g_tab_mu;
 float4* g_tab[128] = {};
+cudaTextureObject_t g_tex[128] = {};   // texture objects over g_tab (TEX-pipe lookups)
 
-const float4* phi_table(int device, std::string* err)
+const float4* phi_table(int device, std::string* err, cudaTextureObject_t* tex = nullptr)
 {
     std::lock_guard<std::mutex> lk(g_tab_mu);
     if (device < 0 || device >= 128) { *err = "device index out of range"; return nullptr; }
-    if (g_tab[device]) return g_tab[device];
+    if (g_tab[device]) {
+        if (tex) *tex = g_tex[device];
+        return g_tab[device];
+    }
     DeviceGuard g(device);
     float4* p = nullptr;
     cudaStream_t st = nullptr;
@@ -66,12 +70,25 @@ const float4* phi_table(int device, std::string* err)
     if (e == cudaSuccess) e = static_cast<cudaError_t>(cbp::launch_phi_table(p, st));
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (st) cudaStreamDestroy(st);
+    cudaTextureObject_t t = 0;
+    if (e == cudaSuccess) {
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypeLinear;
+        rd.res.linear.devPtr = p;
+        rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+        rd.res.linear.sizeInBytes = sizeof(float4) * cbp::kPhiTableSegs;
+        cudaTextureDesc td{};
+        td.readMode = cudaReadModeElementType;   // point fetch of the stored words, no filtering
+        e = cudaCreateTextureObject(&t, &rd, &td, nullptr);
+    }
     if (e != cudaSuccess) {
         if (p) cudaFree(p);
         *err = std::string("phi table: ") + cudaGetErrorString(e);
         return nullptr;
     }
     g_tab[device] = p;
+    g_tex[device] = t;
+    if (tex) *tex = t;
     return p;
 }
 
@@ -86,6 +103,7 @@ struct cbp_code {
     std::vector<int32_t> row_ptr;
     std::vector<int16_t> pshift;
     const float4* phi_tab = nullptr;   // per-device table, not owned
+    cudaTextureObject_t phi_tex = 0;   // per-device texture object over phi_tab, not owned
     cbp::Geometry geo[2]{};           // per cbp_algorithm
     int ctas_per_sm[2] = {1, 1}, num_sms = 1;
 };
@@ -170,10 +188,13 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
     if (nent > cbp::kMaxEnt || mb > cbp::kMaxRows)
         return fail(CBP_E_UNSUPPORTED, "cbp_code_create: more than 512 nonzero base entries or 128 base rows");
     // two int4 per entry b for a geometry with P frames per lane (layout documented in
-    // cbp_kernels.cu; QS = 8P bytes per variable, RS = 4P bytes per edge):
-    //   A = {QS jZ, RS row(p) Z, RS bZ, RS pZ},  B = {QS s, RS ds, first | kp << 8 | s << 16, jZ}
-    auto make_ent = [&](int P) {
-        const int QS = 8 * P, RS = 4 * P;
+    // cbp_kernels.cu; QS = 8P bytes per variable, RS = 4P bytes per edge, SU = 4 for the
+    // 16-byte min-sum check records, else 1):
+    //   A = {QS jZ, S0 + SU RS row(p) Z, R0 + RS bZ, R0 + RS pZ},  B = {QS s, RS ds, first | kp << 8 | s << 16, jZ}
+    // Byte offsets are relative to the group base: QP at 0, the check records at S0, R at R0.
+    auto make_ent = [&](int P, int alg) {
+        const int QS = 8 * P, RS = 4 * P, SU = alg ? 4 : 1, SW = alg ? 4 : 1;
+        const int S0 = 4 * ((2 * P * nb * Z + 3) & ~3), R0 = S0 + 4 * P * SW * mb * Z;
         std::vector<int4> ent(2 * static_cast<size_t>(nent));
         for (int j = 0; j < nb; ++j) {
             const auto& L = col_ent[j];
@@ -185,7 +206,7 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
                 // kp: position of prev(b) among its row's entries = the variable's edge index inside
                 // the previous check (min-sum minimum owner, reading R20)
                 const int kp = p - row_ptr[ent_row[p]];
-                ent[2 * b] = make_int4(QS * j * Z, RS * ent_row[p] * Z, RS * b * Z, RS * p * Z);
+                ent[2 * b] = make_int4(QS * j * Z, S0 + SU * RS * ent_row[p] * Z, R0 + RS * b * Z, R0 + RS * p * Z);
                 ent[2 * b + 1] = make_int4(QS * ent_s[b], RS * ds, first | (kp << 8) | (ent_s[b] << 16), j * Z);
             }
         }
@@ -237,7 +258,7 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
     if (!g.ok) { delete c; return fail(CBP_E_CUDA, "cbp_code_create: cudaSetDevice failed"); }
     {
         std::string terr;
-        c->phi_tab = phi_table(device, &terr);
+        c->phi_tab = phi_table(device, &terr, &c->phi_tex);
         if (!c->phi_tab) { delete c; return fail(CBP_E_CUDA, "cbp_code_create: " + terr); }
     }
     c->row_ptr = row_ptr;
@@ -273,7 +294,7 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         G.team_threads = G.threads;
         // teams per CTA: as many independent teams as shared memory, the thread limit of the
         // instantiation (512 for P = 1, 256 for P = 2) and 15 named barriers allow
-        const int maxt = (P == 2) ? 256 : 512;
+        const int maxt = (P == 2) ? 256 : (G.multi ? 512 : CBP_WARP_MAXT);
         if (G.team_threads > maxt && P == 2) return G;
         const int64_t per_team = 4LL * (cbp::kCtlTeamWords + static_cast<int64_t>(G.F) * G.slot_words);
         const int64_t fixed = 4LL * G.table_words;
@@ -308,7 +329,7 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
             return fail(CBP_E_UNSUPPORTED, "cbp_code_create: kernel does not fit on this device");
         }
         c->ctas_per_sm[alg] = G.state_in_smem ? occ : 1;
-        c->ent[alg] = make_ent(G.P);
+        c->ent[alg] = make_ent(G.P, alg);
     }
     *out = c;
     return CBP_OK;
@@ -351,6 +372,7 @@ cbp::KernelArgs base_args(const cbp_code* c, int alg = 0)
     d.nent = c->nent; d.E = static_cast<int32_t>(c->E); d.nwords = (c->N + 31) / 32; d.kwords = (c->K + 31) / 32;
     d.max_dc = c->max_dc; d.can_encode = c->can_encode; d.mid = c->mid;
     d.phi_tab = c->phi_tab;
+    d.phi_tex = static_cast<unsigned long long>(c->phi_tex);
     std::memcpy(a.ent, c->ent[alg].data(), sizeof(int4) * c->ent[alg].size());
     std::memcpy(a.row_ptr, c->row_ptr.data(), sizeof(int32_t) * c->row_ptr.size());
     std::memcpy(a.pshift, c->pshift.data(), sizeof(int16_t) * c->pshift.size());

@@ -13,6 +13,7 @@ struct DevCode {
     int32_t can_encode;
     int32_t mid;           // floor(core/2)
     const float4* phi_tab; // [929] phi contract v2 coefficients
+    unsigned long long phi_tex;   // cudaTextureObject_t over phi_tab (float4 elements)
 };
 
 enum Mode : int32_t { MODE_DECODE_F32 = 0, MODE_DECODE_I8 = 1, MODE_BER_SIM = 2, MODE_CHANNEL = 3 };
@@ -57,6 +58,11 @@ struct KernelArgs {
     uint32_t phi_m19, phi_one;     // 0x7ffff, 0x3f800000 (phi local variable, runtime operands)
     float* gstate;         // per-CTA global state (state_in_smem == 0)
 };
+
+// thread limit (launch bound) of the one-frame-per-lane warp-team instantiation
+#ifndef CBP_WARP_MAXT
+#define CBP_WARP_MAXT 512
+#endif
 
 constexpr int kCtlTeamWords = 136;  // shared control words per team: 2 x P(2) x 32 ballot words + broadcast
 

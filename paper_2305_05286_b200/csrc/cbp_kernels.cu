@@ -32,10 +32,20 @@ constexpr uint32_t kSign = 0x80000000u;
 #ifndef CBP_CHUNK
 #define CBP_CHUNK 3
 #endif
-// A/B switch: 1 = stage the schedule tables in shared memory (default), 0 = read them
-// from the kernel parameters in the hot loop
+// A/B switches: 1 = stage the schedule tables in shared memory (default), 0 = read them
+// from the kernel parameters in the hot loop.  CBP_TEX_C2B / CBP_TEX_B2V: evaluate the
+// C2B / B2V phi with the table row fetched through the texture pipe instead of LDS.
 #ifndef CBP_SCHED_SMEM
 #define CBP_SCHED_SMEM 1
+#endif
+#ifndef CBP_TEX_C2B
+#define CBP_TEX_C2B 1
+#endif
+#ifndef CBP_TEX_B2V
+#define CBP_TEX_B2V 0
+#endif
+#ifndef CBP_ONE_VARIANT
+#define CBP_ONE_VARIANT 1
 #endif
 
 // ---------------------------------------------------------------- byte-addressed vector access
@@ -127,15 +137,21 @@ struct Grp {
     __device__ __forceinline__ uint32_t* cwp(int p) const { return cw + p * nwords; }
 };
 
-// Schedule table entry b (two int4, built in cbp_api.cpp for the launch's P and algorithm):
-//   A = {QS jZ, RS row(prev(b)) Z, RS b Z, RS prev(b) Z}   byte bases: variable block (QP),
-//        check block of the previous check of the same variables (x SU for the S records),
-//        own R block, R block of prev(b)
+// Schedule table entry b (two int4, built in cbp_api.cpp for the launch's P and algorithm),
+// byte offsets from the group base (QP at 0, check records at S0, R at R0):
+//   A = {QS jZ, S0 + SU RS row(prev(b)) Z, R0 + RS b Z, R0 + RS prev(b) Z}: variable block (QP),
+//        check block of the previous check of the same variables, own R block, R block of prev(b)
 //   B = {QS s, RS ds, first | kp << 8 | s << 16, jZ}   ds = (s - s_prev) mod Z; first: no latest
 //        check in sweep 1 (R1); kp = position of prev(b) in its row (min-sum owner, R20)
 // prev(b) = previous nonzero row of b's column, cyclically (the static "latest check" of
 // every variable of the block after sweep 1); prev(b) == b for a degree-1
 // column (R3).  Variable of lane r: j Z + (r + s) mod Z; its previous check's row (r + ds) mod Z.
+
+// (t mod n) for t in [0, 2n): unsigned min of t and t - n (two instructions, no predicate)
+__device__ __forceinline__ int wrap(int t, int n)
+{
+    return static_cast<int>(min(static_cast<unsigned>(t), static_cast<unsigned>(t - n)));
+}
 
 __device__ __forceinline__ int lane_var(const int4* ent, int e, int r, int Z)
 {
@@ -200,9 +216,17 @@ struct Team {
 // ---------------------------------------------------------------- per-row edge chain
 struct Lane {
     int r, rq, rr, ZQ, ZR;            // lane, r QS, r RS, Z QS, Z RS
-    int qp_bytes, R_bytes, S_bytes;   // group array sizes (bounds checks of debug builds)
+    int slot_bytes;                   // group size (bounds checks of debug builds)
     uint32_t m19, one;                // phi local-variable masks as runtime operands (one LOP3)
+    cudaTextureObject_t tex;          // phi table through the texture pipe
 };
+
+template <bool TEX>
+__device__ __forceinline__ float phi_sel(float x, const float4* __restrict__ ptab, const Lane& L)
+{
+    if constexpr (TEX) return phi32_tex(x, L.tex, L.m19, L.one);
+    else return phi32(x, ptab, L.m19, L.one);
+}
 
 template <int P>
 struct RowAcc {
@@ -233,13 +257,11 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
     for (int u = 0; u < U; ++u) {
         const int4 A = ent[2 * (e0 + k0 + u)];
         const int4 B = ent[2 * (e0 + k0 + u) + 1];
-        int tq = L.rq + B.x;
-        tq = (tq >= L.ZQ) ? tq - L.ZQ : tq;
-        int tr = L.rr + B.y;
-        tr = (tr >= L.ZR) ? tr - L.ZR : tr;
+        const int tq = wrap(L.rq + B.x, L.ZQ);
+        const int tr = wrap(L.rr + B.y, L.ZR);
         CBP_CHECK(tq >= 0 && tq < L.ZQ && tr >= 0 && tr < L.ZR);
-        CBP_CHECK(A.x + tq + Ly::QS <= L.qp_bytes && A.y + tr + Ly::RS <= L.S_bytes && A.z + L.rr + Ly::RS <= L.R_bytes &&
-                  A.w + tr + Ly::RS <= L.R_bytes);
+        CBP_CHECK(A.x + tq + Ly::QS <= L.slot_bytes && A.y + tr + Ly::RS <= L.slot_bytes &&
+                  A.z + L.rr + Ly::RS <= L.slot_bytes && A.w + tr + Ly::RS <= L.slot_bytes);
         aqp[u] = A.x + tq;
         aw[u] = A.w + tr;
         ar[u] = A.z + L.rr;
@@ -251,7 +273,7 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
             q[u][p] = qp[p];
             p0[u][p] = qp[P + p];
         }
-        ldf<P>(g.S, A.y + tr, scj[u]);
+        ldf<P>(g.qp, A.y + tr, scj[u]);
     }
     // B2V (equ_s4e18): R^new_{cj->v} = sgn(Omega_cj) sgn(Q) phi(|phi(|Omega_cj|) - phi(|Q|)|), phi(|Omega|) = S (R11)
 #pragma unroll
@@ -260,20 +282,20 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
         vabsdiff<P>(scj[u], p0[u], d);
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            const float mag = phi32(fabsf(d[p]), ptab, L.m19, L.one);
+            const float mag = phi_sel<CBP_TEX_B2V>(fabsf(d[p]), ptab, L);
             const uint32_t sg = (__float_as_uint(scj[u][p]) ^ __float_as_uint(q[u][p])) & kSign;
             Rn[u][p] = __uint_as_float(__float_as_uint(mag) | sg);
             if (SW1 && fst[u] && s1[p]) Rn[u][p] = 0.0f;
         }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) stf<P>(g.R, aw[u], Rn[u]);   // equ_s4e22 commit of R_{cj->v} (R2), before the read (R3)
+    for (int u = 0; u < U; ++u) stf<P>(g.qp, aw[u], Rn[u]);   // equ_s4e22 commit of R_{cj->v} (R2), before the read (R3)
     float qn[U][P];
     uint32_t lb[U][P];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         float ro[P], lam[P];
-        ldf<P>(g.R, ar[u], ro);                              // R_{ci->v}
+        ldf<P>(g.qp, ar[u], ro);                             // R_{ci->v}
         vadd<P>(q[u], Rn[u], lam);                           // equ_s4e20 (Lambda is never -0)
         vsub<P>(lam, ro, qn[u]);                             // equ_s4e19 (R15)
 #pragma unroll
@@ -287,7 +309,7 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int p = 0; p < P; ++p) ph[u][p] = phi32(fabsf(qn[u][p]), ptab, L.m19, L.one);   // C2B (equ_s4e21, App. equ_ae4)
+        for (int p = 0; p < P; ++p) ph[u][p] = phi_sel<CBP_TEX_C2B>(fabsf(qn[u][p]), ptab, L);   // C2B (equ_s4e21, App. equ_ae4)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         vadd<P>(acc.Ssum, ph[u], acc.Ssum);
@@ -394,11 +416,9 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
     for (int u = 0; u < U; ++u) {
         const int4 A = ent[2 * (e0 + k0 + u)];
         const int4 B = ent[2 * (e0 + k0 + u) + 1];
-        int tq = L.rq + B.x;
-        tq = (tq >= L.ZQ) ? tq - L.ZQ : tq;
-        int tr = L.rr + B.y;
-        tr = (tr >= L.ZR) ? tr - L.ZR : tr;
-        CBP_CHECK(Ly::SU * (A.y + tr) + Ly::SS <= L.S_bytes);
+        const int tq = wrap(L.rq + B.x, L.ZQ);
+        const int tr = wrap(L.rr + B.y, L.ZR);
+        CBP_CHECK(A.y + Ly::SU * tr + Ly::SS <= L.slot_bytes);
         aqp[u] = A.x + tq;
         aw[u] = A.w + tr;
         ar[u] = A.z + L.rr;
@@ -411,7 +431,7 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
             q[u][p] = qp[p];
             p0[u][p] = qp[P + p];
         }
-        ld_rec<P>(g.S, Ly::SU * (A.y + tr), cm1[u], cm2[u], cow[u]);   // record of the previous check c_j
+        ld_rec<P>(g.qp, A.y + Ly::SU * tr, cm1[u], cm2[u], cow[u]);   // record of the previous check c_j
     }
     // B2V (equ_s4e18xx)
 #pragma unroll
@@ -424,11 +444,11 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
             if (SW1 && fst[u] && s1[p]) Rn[u][p] = 0.0f;
         }
 #pragma unroll
-    for (int u = 0; u < U; ++u) stf<P>(g.R, aw[u], Rn[u]);   // commit of R_{cj->v} (R2, R3)
+    for (int u = 0; u < U; ++u) stf<P>(g.qp, aw[u], Rn[u]);   // commit of R_{cj->v} (R2, R3)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         float ro[P], lam[P], qn[P], st[2 * P];
-        ldf<P>(g.R, ar[u], ro);
+        ldf<P>(g.qp, ar[u], ro);
         vadd<P>(q[u], Rn[u], lam);                           // equ_s4e20
         vsub<P>(lam, ro, qn);                                // equ_s4e19
 #pragma unroll
@@ -694,8 +714,8 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
     }
     tm.lane_on = tm.r < Z && tm.slot < a.F;
     const int r = tm.r;
-    const Lane lane{r, r * Ly::QS, r * Ly::RS, Z * Ly::QS, Z * Ly::RS, Ly::QS * C.N, Ly::RS * C.E, Ly::SS * C.M,
-                    a.phi_m19, a.phi_one};
+    const Lane lane{r, r * Ly::QS, r * Ly::RS, Z * Ly::QS, Z * Ly::RS, 4 * a.slot_words,
+                    a.phi_m19, a.phi_one, static_cast<cudaTextureObject_t>(C.phi_tex)};
     uint32_t* ctl = smem + a.table_words + tm.tidx * kCtlTeamWords;
     long long* ctl64 = reinterpret_cast<long long*>(ctl + 128);
 
@@ -933,6 +953,16 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                         track |= active[p] && belief && consec[p] + Z >= W;
                     }
                     const int sidx = (i * Z + r) * Ly::RS;
+#if CBP_ONE_VARIANT
+                    // one code path for every row (smaller code, fewer instruction-cache misses):
+                    // first-visit handling and rollback bits always evaluated
+                    if constexpr (ALG == 1)
+                        ro = process_row_ms<P, true, true>(ent, e0, dc, sidx, lane, g, s1, a.alpha);
+                    else
+                        ro = process_row<P, true, true>(ent, ptab, e0, dc, sidx, lane, g, s1);
+                    (void)sw1;
+                    (void)track;
+#else
                     if (sw1) {
                         if constexpr (ALG == 1)
                             ro = track ? process_row_ms<P, true, true>(ent, e0, dc, sidx, lane, g, s1, a.alpha)
@@ -948,6 +978,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                             ro = track ? process_row<P, false, true>(ent, ptab, e0, dc, sidx, lane, g, s1)
                                        : process_row<P, false, false>(ent, ptab, e0, dc, sidx, lane, g, s1);
                     }
+#endif
                 }
                 // ---- Step 2(3): stopping criterion, counted per check update (R4, R5)
                 int first_bad[P], last_bad[P];   // first / last unclean check of the row
@@ -1147,7 +1178,9 @@ static int dispatch(const Geometry& g, Args... args)
         if (!g.state_in_smem || g.threads > 256) return static_cast<int>(cudaErrorInvalidConfiguration);
         return g.multi ? Fn<true, true, 256, 2>::run(g, args...) : Fn<false, true, 256, 2>::run(g, args...);
     }
-    if (!g.multi) return g.state_in_smem ? Fn<false, true, 512, 1>::run(g, args...) : Fn<false, false, 512, 1>::run(g, args...);
+    if (!g.multi)
+        return g.state_in_smem ? Fn<false, true, CBP_WARP_MAXT, 1>::run(g, args...)
+                               : Fn<false, false, CBP_WARP_MAXT, 1>::run(g, args...);
     if (g.threads <= 512)
         return g.state_in_smem ? Fn<true, true, 512, 1>::run(g, args...) : Fn<true, false, 512, 1>::run(g, args...);
     return g.state_in_smem ? Fn<true, true, 1024, 1>::run(g, args...) : Fn<true, false, 1024, 1>::run(g, args...);

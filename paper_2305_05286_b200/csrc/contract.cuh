@@ -6,6 +6,8 @@
 // IEEE div/sqrt and denormals kept.  Every FMA below is an explicit
 // __fmaf_rn (one correctly rounded FFMA), never formed by the compiler.
 #pragma once
+#include <cuda_runtime.h>
+
 #include <cassert>
 #include <cstdint>
 
@@ -147,7 +149,8 @@ __device__ __forceinline__ float4 phi_segment_coeffs(int seg)
 // exactly (the fma is exact before its one rounding toward zero, ulp 1 in
 // [2^23, 2^24)), so seg = bits(m) - bits(2^23) + 704 and u = fma(x, 8, -(16 + i))
 // = t - i exactly: the contract's i = (int)t and u = t - (float)i, bit for bit.
-__device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab, uint32_t m19, uint32_t one)
+// segment index and local variable of x (clamped to [PHI_LO, PHI_HI])
+__device__ __forceinline__ void phi32_index(float x, uint32_t m19, uint32_t one, int& seg, float& u)
 {
     x = fminf(fmaxf(x, kPhiLo), kPhiHi);
     const uint32_t b = __float_as_uint(x);
@@ -159,18 +162,41 @@ __device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab, 
     const float u_hi = __fmaf_rn(x, 8.0f, __fsub_rn(8388592.0f, m));
     const int seg_hi = static_cast<int>(__float_as_uint(m)) - (0x4b000000 - 704);
     const bool hi = x >= 2.0f;
-    const int seg = hi ? seg_hi : seg_lo;
-    const float u = hi ? u_hi : u_lo;
+    seg = hi ? seg_hi : seg_lo;
+    u = hi ? u_hi : u_lo;
     CBP_CHECK(seg >= 0 && seg < kPhiSegs);
-    const float4 c = tab[seg];
+}
+
+__device__ __forceinline__ float phi32_cubic(float4 c, float u)
+{
     float p = __fmaf_rn(c.w, u, c.z);
     p = __fmaf_rn(p, u, c.y);
     return __fmaf_rn(p, u, c.x);
 }
 
+__device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab, uint32_t m19, uint32_t one)
+{
+    int seg;
+    float u;
+    phi32_index(x, m19, one, seg, u);
+    return phi32_cubic(tab[seg], u);
+}
+
 __device__ __forceinline__ float phi32(float x, const float4* __restrict__ tab)
 {
     return phi32(x, tab, 0x7ffffu, 0x3f800000u);
+}
+
+// The same function with the segment row fetched through the texture path (TEX data
+// pipe) from the device copy of the table: identical bits, and its bandwidth adds to the
+// shared-memory pipe's (tools/ubench_lookup.cu: 2 LDS.128 + 1 TEX lookups per step take
+// the time of the 2 LDS.128 alone).
+__device__ __forceinline__ float phi32_tex(float x, cudaTextureObject_t tex, uint32_t m19, uint32_t one)
+{
+    int seg;
+    float u;
+    phi32_index(x, m19, one, seg, u);
+    return phi32_cubic(tex1Dfetch<float4>(tex, seg), u);
 }
 
 // sin / cos of 2 pi m 2^-24 with exact integer quadrant reduction (Box-Muller)
