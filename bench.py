@@ -26,14 +26,17 @@ sys.path.insert(0, str(ROOT))
 METRIC = "CBP info Gbit/s and frames/s per GPU and 8×B200 at Eb/N0, % of roofline"
 UNIT = "info Gbit/s"
 I_EDGE = 38            # algorithmic fp32/int ops per edge visit of the arithmetic contract v2
+B_EDGE = 60            # algorithmic on-chip bytes per edge visit: QP r/w 8+8, S_cj 4, R_ci 4, R_cj 4, 2 phi rows 2x16
 
 
 def kernel_traffic():
-    """DRAM bytes per launch of the dominant kernel from the committed ncu capture (profiles/)."""
+    """DRAM bytes per launch and pipe utilisation of the dominant kernel from the
+    latest committed ncu capture (profiles/*_kernel_traffic.json, tools/profile_summary.py)."""
     caps = sorted((ROOT / "profiles").glob("r*_kernel_traffic.json"))
     if not caps:
         return None, None
     d = json.loads(caps[-1].read_text())
+    d["file"] = caps[-1].name
     return d["dram_bytes_read"] + d["dram_bytes_write"], d
 
 
@@ -239,10 +242,24 @@ def main():
     roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Top/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "note": f"I_edge={I_EDGE} contract ops/edge-visit x exact edge visits / mean launch time; peak = "
-                        f"{li['num_sms']} SM x 128 lanes x {f_sm:.0f} MHz (sm_max, MEASURED_PEAKS.json); traffic = "
-                        f"DRAM bytes/launch from {traffic_src.get('source', 'n/a') if traffic_src else 'n/a'} "
-                        f"(algorithmic HBM bytes of ber_sim: 0 in, 64 out); shared-memory wavefronts/SM-cycle "
-                        f"{traffic_src.get('smem_wavefronts_per_sm_cycle') if traffic_src else None}"}
+                        f"{li['num_sms']} SM x 128 lanes x {f_sm:.0f} MHz (sm_max, MEASURED_PEAKS.json, derived "
+                        f"issue peak); traffic = DRAM bytes/launch from "
+                        f"{traffic_src.get('file', 'n/a') if traffic_src else 'n/a'} (algorithmic HBM bytes of "
+                        f"ber_sim: 0 in, 64 out)"}
+    # the resources that actually bind: the on-chip data pipes and the issue slots,
+    # measured by ncu on the same kernel (C2, 2 dB, 1e5 frames) and committed under profiles/
+    on_chip = float(np.array(ev_local, dtype=np.float64).sum() * B_EDGE / dur.sum())
+    onchip_peak = li["num_sms"] * 128 * f_sm * 1e6
+    roofline_onchip = {"bound": "smem+tex data pipes", "achieved": on_chip / 1e12, "peak": onchip_peak / 1e12,
+                       "unit": "TB/s", "frac": on_chip / onchip_peak,
+                       "note": f"B_edge={B_EDGE} algorithmic on-chip bytes/edge-visit (no bank conflicts) x edge "
+                               f"visits / mean launch time; peak = 128 B/clk/SM x {li['num_sms']} SM x {f_sm:.0f} MHz "
+                               f"(one shared-memory wavefront per clock)"}
+    if traffic_src:
+        roofline_onchip["ncu_pipe_utilisation_pct"] = {k: traffic_src.get(k) for k in (
+            "smem_pipe_pct", "tex_pipe_pct", "issue_active_pct", "alu_pipe_pct", "fma_pipe_pct")}
+        roofline_onchip["ncu_lane_slots_per_edge_visit"] = traffic_src.get("lane_slots_per_edge_visit")
+        roofline_onchip["ncu_source"] = traffic_src.get("file")
 
     # end-to-end: host LLRs -> cbp_decode (pipelined H2D / decode / D2H) -> host outputs
     e2e = None
@@ -278,19 +295,24 @@ def main():
     # C5 = C3a @ 2.5 dB with the fp32 and the int8 LLR stream
     others = {}
     if not args.no_suite:
-        suite = [("C1", 2.0, 1_000_000, 0, 0), ("C3a", 2.5, 300_000, 0, 0), ("C5", 2.5, 300_000, 0, 1),
-                 ("C3b", 4.0, 300_000, 0, 0), ("C4", 1.5, 3_000, 2, 0)]
-        for name, eb, nf, rule, lm in suite:
+        # (config, Eb/N0, frames, stop rule, llr mode, algorithm): the other BASELINE configs, the C2 stop-rule
+        # variants (W=N, syndrome per sweep) and normalized min-sum CBP (NEXT-1) on the same frames
+        suite = [("C1", 2.0, 1_000_000, 0, 0, 0), ("C3a", 2.5, 300_000, 0, 0, 0), ("C5", 2.5, 300_000, 0, 1, 0),
+                 ("C3b", 4.0, 300_000, 0, 0, 0), ("C4", 1.5, 3_000, 2, 0, 0), ("C2", 2.0, 1_000_000, 1, 0, 0),
+                 ("C2", 2.0, 1_000_000, 2, 0, 0), ("C2", 2.0, 1_000_000, 0, 0, 1)]
+        for name, eb, nf, rule, lm, alg in suite:
             ocfg = inputs.CONFIGS[name]
             ob, oz = inputs.config_base(name)
             oc = cbp.Code(ob, oz, device=local)
             c = torch.zeros(8, dtype=torch.int64, device=dev)
-            oc.ber_sim(eb, args.seed, 0, min(nf, 20_000), ocfg.max_iter, rule, lm, counts=c, stream=stream)
+            oc.ber_sim(eb, args.seed, 0, min(nf, 20_000), ocfg.max_iter, rule, lm, counts=c, stream=stream,
+                       algorithm=alg)
             c.zero_()
             barrier()
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
-            oc.ber_sim(eb, args.seed, rank * nf, nf, ocfg.max_iter, rule, lm, counts=c, stream=stream)
+            oc.ber_sim(eb, args.seed, rank * nf, nf, ocfg.max_iter, rule, lm, counts=c, stream=stream,
+                       algorithm=alg)
             a1.record(stream)
             allreduce_counts(c)
             torch.cuda.synchronize()
@@ -298,12 +320,15 @@ def main():
             if world > 1:
                 dist.all_reduce(ms, op=dist.ReduceOp.MAX)
             t = c.cpu().numpy()
-            others[f"{name}@{eb}dB" + ("/int8" if lm else "")] = {
+            key = f"{name}@{eb}dB" + ("/int8" if lm else "") + ("/min-sum" if alg else "") + \
+                ("" if rule == 0 or name == "C4" else ["", "/W=N", "/syndrome", "/none"][rule])
+            others[key] = {
                 "N": oc.N, "K": oc.K, "frames": int(t[0]), "ms": ms.item(),
                 "frames_per_s": t[0] / ms.item() * 1e3, "info_gbps": t[0] * oc.K / ms.item() / 1e6,
                 "edge_visits_per_s": t[5] / ms.item() * 1e3, "ber": t[1] / max(1, t[0] * oc.K),
                 "fer": t[2] / max(1, t[0]), "avg_iters": t[4] / max(1, t[0]),
                 "stop_rule": ["belief W=M", "belief W=N", "syndrome", "none"][rule],
+                "algorithm": ["log-tanh", "normalized min-sum (alpha 0.75)"][alg],
                 "launch": oc.launch_info()}
 
     cpu = None
@@ -334,7 +359,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_block(cfg, ebn0s, frames, args, world),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "roofline": roofline, "roofline_onchip": roofline_onchip, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clocks,
             "gpu_launches": args.steps * len(ebn0s), "launch": li, "results": results,
             "other_configs": others,
         }
