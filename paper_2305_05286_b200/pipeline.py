@@ -1,6 +1,8 @@
-"""Host-buffer decoding: chunked, double-buffered H2D -> cbp_decode -> D2H on
-two CUDA streams so PCIe transfers overlap the decode kernel (the end-to-end
-call a user with LLRs in host memory makes)."""
+"""Host-buffer decoding: chunked H2D -> cbp_decode -> D2H round-robin over four
+CUDA streams so PCIe transfers overlap the decode kernels (the end-to-end call a
+user with LLRs in host memory makes).  Chunks of 2^15 frames on 4 streams keep
+the pipeline at 98% of the device-resident decode rate on C2 at 2 dB
+(tools/e2e_sweep.py: 1.26e7 vs 1.28e7 frames/s; 2^17 x 2 streams: 1.0e7)."""
 from __future__ import annotations
 
 import torch
@@ -15,17 +17,17 @@ def alloc_host_outputs(code: Code, frames: int) -> dict:
 
 
 def decode_host(code: Code, llr_host: torch.Tensor, max_iter: int, stop_rule: int = CBP_STOP_BELIEF_M,
-                out: dict | None = None, chunk: int = 1 << 17, streams=None) -> dict:
+                out: dict | None = None, chunk: int = 1 << 15, streams=None, nstreams: int = 4) -> dict:
     """Decode float32 LLRs [frames, ld] held in (pinned) host memory; returns pinned host outputs.
 
-    The copies and launches are enqueued on two streams; the call returns after
-    synchronising them, so the outputs are ready."""
+    The copies and launches are enqueued on `nstreams` streams (each with its own
+    device buffers); the call returns after synchronising them, so the outputs are ready."""
     frames, ld = llr_host.shape
     out = out if out is not None else alloc_host_outputs(code, frames)
     if frames == 0:
         return out
     dev = code.device
-    streams = streams or [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+    streams = streams or [torch.cuda.Stream(device=dev) for _ in range(nstreams)]
     n = min(chunk, frames)
     bufs = [(torch.empty((n, ld), dtype=torch.float32, device=dev), code.alloc_outputs(n)) for _ in streams]
     cur = torch.cuda.current_stream(dev)

@@ -335,3 +335,25 @@ def test_minsum_rejects_bad_options(codes, fpl):
     g1.decode(y, 5)
     with pytest.raises(RuntimeError):
         g1.decode(y, 5, **MS)
+
+
+def test_decode_host_pipeline(codes):
+    """The end-to-end path of bench.py's e2e (pinned host LLRs -> chunked H2D / cbp_decode
+    / D2H over several streams) returns exactly the device-resident decode's outputs,
+    for a frame count that leaves a ragged last chunk; a sample equals the oracle."""
+    from paper_2305_05286_b200 import pipeline
+    g, o = codes("C2")
+    F = 3 * (1 << 15) + 777
+    llr, _ = g.channel(2.0, 17, 0, F, want_cw=False)
+    host = torch.empty(tuple(llr.shape), dtype=torch.float32, pin_memory=True)
+    host.copy_(llr)
+    out = pipeline.decode_host(g, host, 30)
+    ref = g.decode(llr, 30)
+    torch.cuda.synchronize()
+    for k in ("bits", "iters", "flags"):
+        assert torch.equal(out[k], ref[k].cpu()), k
+    idx = np.array([0, 1, F // 2, F - 1])
+    l_o = llr[idx].cpu().numpy()[:, :o.N]
+    oo = o.decode(np.ascontiguousarray(l_o), 30)
+    assert (out["bits"].numpy()[idx].view(np.uint32)[:, :oo["bits"].shape[1]] == oo["bits"]).all()
+    assert (out["iters"].numpy()[idx] == oo["iters"]).all()
