@@ -141,8 +141,9 @@ struct Grp {
 // byte offsets from the group base (QP at 0, check records at S0, R at R0):
 //   A = {QS jZ, S0 + SU RS row(prev(b)) Z, R0 + RS b Z, R0 + RS prev(b) Z}: variable block (QP),
 //        check block of the previous check of the same variables, own R block, R block of prev(b)
-//   B = {QS s, RS ds, first | kp << 8 | s << 16, jZ}   ds = (s - s_prev) mod Z; first: no latest
-//        check in sweep 1 (R1); kp = position of prev(b) in its row (min-sum owner, R20)
+//   B = {QS s, RS ds, first | kp << 8 | s << 16, first ? ~0 : 0}   ds = (s - s_prev) mod Z; first: no
+//        latest check in sweep 1 (R1), as a bit and as a kill mask; kp = position of prev(b) in its row
+//        (min-sum owner, R20)
 // prev(b) = previous nonzero row of b's column, cyclically (the static "latest check" of
 // every variable of the block after sweep 1); prev(b) == b for a degree-1
 // column (R3).  Variable of lane r: j Z + (r + s) mod Z; its previous check's row (r + ds) mod Z.
@@ -153,12 +154,13 @@ __device__ __forceinline__ int wrap(int t, int n)
     return static_cast<int>(min(static_cast<unsigned>(t), static_cast<unsigned>(t - n)));
 }
 
+// variable of lane r in entry e: j Z + (r + s) mod Z, j Z = A.x / QS
+template <int QS>
 __device__ __forceinline__ int lane_var(const int4* ent, int e, int r, int Z)
 {
-    const int4 B = ent[2 * e + 1];
-    int t = r + (B.z >> 16);
+    int t = r + (ent[2 * e + 1].z >> 16);
     t = (t >= Z) ? t - Z : t;
-    return B.w + t;
+    return ent[2 * e].x / QS + t;
 }
 
 // ---------------------------------------------------------------- team helpers
@@ -247,12 +249,12 @@ struct RowAcc {
 // the same slot, which realises "commit before read" (R3) through memory order.
 template <int U, int P, bool SW1, bool TRACK>
 __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int k0,
-                                           const Lane& L, const Grp<P, 0>& g, const bool (&s1)[P], RowAcc<P>& acc)
+                                           const Lane& L, const Grp<P, 0>& g, const uint32_t (&s1m)[P], RowAcc<P>& acc)
 {
     using Ly = Lay<P, 0>;
     int aqp[U], aw[U], ar[U];
     float q[U][P], p0[U][P], scj[U][P], Rn[U][P];
-    bool fst[U];
+    uint32_t fkill[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int4 A = ent[2 * (e0 + k0 + u)];
@@ -265,7 +267,7 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
         aqp[u] = A.x + tq;
         aw[u] = A.w + tr;
         ar[u] = A.z + L.rr;
-        fst[u] = SW1 && (B.z & 1) != 0;
+        fkill[u] = SW1 ? static_cast<uint32_t>(B.w) : 0u;
         float qp[2 * P];
         ldf<2 * P>(g.qp, aqp[u], qp);
 #pragma unroll
@@ -284,8 +286,8 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
         for (int p = 0; p < P; ++p) {
             const float mag = phi_sel<CBP_TEX_B2V>(fabsf(d[p]), ptab, L);
             const uint32_t sg = (__float_as_uint(scj[u][p]) ^ __float_as_uint(q[u][p])) & kSign;
-            Rn[u][p] = __uint_as_float(__float_as_uint(mag) | sg);
-            if (SW1 && fst[u] && s1[p]) Rn[u][p] = 0.0f;
+            // first visit of a frame in sweep 1 (R1): R^new = +0 (kill mask, one LOP3)
+            Rn[u][p] = __uint_as_float((__float_as_uint(mag) | sg) & ~(fkill[u] & s1m[p]));
         }
     }
 #pragma unroll
@@ -302,7 +304,8 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
         for (int p = 0; p < P; ++p) {
             lb[u][p] = __float_as_uint(lam[p]) & kSign;      // hard decision, equ_s2e7
             acc.flipw[p] |= __float_as_uint(lam[p]) ^ __float_as_uint(p0[u][p]);   // equ_s4e24 (R7), bit 31
-            if (TRACK) acc.oldbits[p] |= (__float_as_uint(p0[u][p]) >> 31) << (k0 + u);
+            // previous hard bit, edge k at bit dc-1-k (one funnel shift)
+            if (TRACK) acc.oldbits[p] = __funnelshift_l(__float_as_uint(p0[u][p]), acc.oldbits[p], 1);
         }
     }
     float ph[U][P];
@@ -335,7 +338,7 @@ struct RowOut {
 template <int P, bool SW1, bool TRACK>
 __device__ __forceinline__ RowOut<P> process_row(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
                                                  int dc, int sidx, const Lane& L, const Grp<P, 0>& g,
-                                                 const bool (&s1)[P])
+                                                 const uint32_t (&s1)[P])
 {
     RowAcc<P> acc;
     float Sold[P];
@@ -404,14 +407,13 @@ __device__ __forceinline__ void st_rec(char* S, int off, const float (&m1)[P], c
 
 template <int U, int P, bool SW1, bool TRACK>
 __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int e0, int k0, const Lane& L,
-                                              const Grp<P, 1>& g, const bool (&s1)[P], float alpha, MsAcc<P>& acc)
+                                              const Grp<P, 1>& g, const uint32_t (&s1m)[P], float alpha, MsAcc<P>& acc)
 {
     using Ly = Lay<P, 1>;
     int aqp[U], aw[U], ar[U], kp[U];
     float q[U][P], p0[U][P], Rn[U][P];
     float cm1[U][P], cm2[U][P];
-    uint32_t cow[U][P];
-    bool fst[U];
+    uint32_t cow[U][P], fkill[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int4 A = ent[2 * (e0 + k0 + u)];
@@ -422,7 +424,7 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
         aqp[u] = A.x + tq;
         aw[u] = A.w + tr;
         ar[u] = A.z + L.rr;
-        fst[u] = SW1 && (B.z & 1) != 0;
+        fkill[u] = SW1 ? static_cast<uint32_t>(B.w) : 0u;
         kp[u] = (B.z >> 8) & 0xff;
         float qp[2 * P];
         ldf<2 * P>(g.qp, aqp[u], qp);
@@ -440,8 +442,8 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
         for (int p = 0; p < P; ++p) {
             const uint32_t ow = cow[u][p];
             const float mag = (static_cast<int>(ow & 0xffu) == kp[u]) ? cm2[u][p] : cm1[u][p];
-            Rn[u][p] = __uint_as_float(__float_as_uint(mag) | ((ow ^ __float_as_uint(q[u][p])) & kSign));
-            if (SW1 && fst[u] && s1[p]) Rn[u][p] = 0.0f;
+            Rn[u][p] = __uint_as_float((__float_as_uint(mag) | ((ow ^ __float_as_uint(q[u][p])) & kSign)) &
+                                       ~(fkill[u] & s1m[p]));
         }
 #pragma unroll
     for (int u = 0; u < U; ++u) stf<P>(g.qp, aw[u], Rn[u]);   // commit of R_{cj->v} (R2, R3)
@@ -455,7 +457,8 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
         for (int p = 0; p < P; ++p) {
             const uint32_t lb = __float_as_uint(lam[p]) & kSign;
             acc.flipw[p] |= __float_as_uint(lam[p]) ^ __float_as_uint(p0[u][p]);
-            if (TRACK) acc.oldbits[p] |= (__float_as_uint(p0[u][p]) >> 31) << (k0 + u);
+            // previous hard bit, edge k at bit dc-1-k (one funnel shift)
+            if (TRACK) acc.oldbits[p] = __funnelshift_l(__float_as_uint(p0[u][p]), acc.oldbits[p], 1);
             // C2B (equ_s4e21xx), in ascending edge order, branch-free:
             // m < m1: (m1, m2, own) <- (m, m1, k); else m2 <- min(m2, m).  m1 <= m2 always.
             const float m = __fmul_rn(alpha, fabsf(qn[p]));
@@ -473,7 +476,8 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
 
 template <int P, bool SW1, bool TRACK>
 __device__ __forceinline__ RowOut<P> process_row_ms(const int4* __restrict__ ent, int e0, int dc, int sidx,
-                                                    const Lane& L, const Grp<P, 1>& g, const bool (&s1)[P], float alpha)
+                                                    const Lane& L, const Grp<P, 1>& g, const uint32_t (&s1)[P],
+                                                    float alpha)
 {
     using Ly = Lay<P, 1>;
     const float inf = __uint_as_float(0x7f800000u);
@@ -512,12 +516,13 @@ template <int P, int ALG>
 __device__ __forceinline__ uint32_t swap_row_bits(const int4* __restrict__ ent, int e0, int dc, int r, int Z, int p,
                                                   uint32_t bits, const Grp<P, ALG>& g)
 {
+    // bit of edge k at position dc-1-k (the order edge_chunk accumulates them in)
     uint32_t prev = 0;
     for (int k = 0; k < dc; ++k) {
-        const int v = lane_var(ent, e0 + k, r, Z);
+        const int v = lane_var<8 * P>(ent, e0 + k, r, Z);
         const uint32_t w = __float_as_uint(g.PH(v, p));
-        prev |= (w >> 31) << k;
-        g.PH(v, p) = __uint_as_float((w & ~kSign) | (((bits >> k) & 1u) << 31));
+        prev = (prev << 1) | (w >> 31);
+        g.PH(v, p) = __uint_as_float((w & ~kSign) | (((bits >> (dc - 1 - k)) & 1u) << 31));
     }
     return prev;
 }
@@ -530,20 +535,21 @@ __device__ __forceinline__ bool lane_syndrome(const int4* __restrict__ ent, cons
     uint32_t nz = 0;
     for (int i = 0; i < mb; ++i) {
         uint32_t par = 0;
-        for (int k = row_ptr[i]; k < row_ptr[i + 1]; ++k) par ^= __float_as_uint(g.PH(lane_var(ent, k, r, Z), p)) >> 31;
+        for (int k = row_ptr[i]; k < row_ptr[i + 1]; ++k) par ^= __float_as_uint(g.PH(lane_var<8 * P>(ent, k, r, Z), p)) >> 31;
         nz |= par;
     }
     return nz != 0u;
 }
 
 // lambda_i[r] = XOR of the info bits of lifted check i*Z + r (encoder)
+template <int QS>
 __device__ __forceinline__ uint32_t info_parity(const int4* __restrict__ ent, const int32_t* row_ptr, int i, int r,
                                                 int Z, int K, const uint32_t* cw)
 {
     uint32_t par = 0;
     for (int k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
-        if (ent[2 * k + 1].w >= K) continue;
-        const int v = lane_var(ent, k, r, Z);
+        if (ent[2 * k].x / QS >= K) continue;                   // parity column
+        const int v = lane_var<QS>(ent, k, r, Z);
         par ^= (cw[v >> 5] >> (v & 31)) & 1u;
     }
     return par;
@@ -592,7 +598,7 @@ __device__ void channel_frames(const KernelArgs& a, const Team<MULTI>& tm, const
         for (int v = r; v < C.K; v += Z) g.Q(v, p) = ((cw[v >> 5] >> (v & 31)) & 1u) ? -1.0f : 1.0f;
         uint32_t p0 = 0;
         for (int i = 0; i < C.core; ++i) {
-            const uint32_t lam = info_parity(ent, row_ptr, i, r, Z, C.K, cw);
+            const uint32_t lam = info_parity<8 * P>(ent, row_ptr, i, r, Z, C.K, cw);
             g.Sw(i * Z + r, 0, p) = __uint_as_float(lam);   // lambda_i[r] kept for the next pass (S is free here)
             p0 ^= lam;
         }
@@ -617,7 +623,7 @@ __device__ void channel_frames(const KernelArgs& a, const Team<MULTI>& tm, const
             pprev = pt;
         }
         for (int k = 0; k < C.mb - C.core; ++k) {
-            const uint32_t pe = info_parity(ent, row_ptr, C.core + k, r, Z, C.K, g.cwp(p));
+            const uint32_t pe = info_parity<8 * P>(ent, row_ptr, C.core + k, r, Z, C.K, g.cwp(p));
             g.Q((C.kb + C.core + k) * Z + r, p) = pe ? -1.0f : 1.0f;
         }
     }
@@ -945,11 +951,13 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                 if (live && tm.lane_on) {
                     // the window can only fill in this row if consec + Z >= W (R4); otherwise
                     // no rollback information is needed
-                    bool s1[P], sw1 = false, track = false;
+                    bool sw1 = false, track = false;
+                    uint32_t s1[P];   // all ones for a frame in sweep 1 (first-visit kill mask)
 #pragma unroll
                     for (int p = 0; p < P; ++p) {
-                        s1[p] = active[p] && sweep[p] == 1;
-                        sw1 |= s1[p];
+                        const bool f1 = active[p] && sweep[p] == 1;
+                        s1[p] = f1 ? kFull : 0u;
+                        sw1 |= f1;
                         track |= active[p] && belief && consec[p] + Z >= W;
                     }
                     const int sidx = (i * Z + r) * Ly::RS;
