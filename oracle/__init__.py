@@ -15,7 +15,7 @@ _HERE = Path(__file__).resolve().parent
 _LIB = None
 
 STOP_BELIEF_M, STOP_BELIEF_N, STOP_SYNDROME, STOP_NONE = 0, 1, 2, 3
-FP32_CONTRACT, FP64, FP64_LITERAL, MINSUM = 0, 1, 2, 3
+FP32_CONTRACT, FP64, FP64_LITERAL, MINSUM, LBP, FBP = 0, 1, 2, 3, 4, 5
 ALPHA_DEFAULT = 0.75   # normalized min-sum parameter (reading R20; the paper leaves alpha open)
 PHI_LO = float.fromhex("0x1.a56e0cp-43")
 PHI_HI = 30.0

@@ -502,10 +502,115 @@ static FrameResult minsum_frame(const or_code* c, const float* L, const or_opts*
     return res;
 }
 
+// ---------------------------------------------------------------- comparison schedules (NEXT-3)
+// Layered BP, in fp32 under the arithmetic contract (reading R22):
+// checks ascending; for c and every v in N(c) (ascending): Q_{v->c} = Lambda_v - R_{c->v}
+// (equ_s2e10); the C2V rule equ_s2e4 in the phi domain with the leave-one-out sum as
+// S - phi(|Q_v|), S = sum of phi(|Q|) over N(c) in ascending order (as CBP's R11) and the
+// sign product as the XOR of all signs with v's own; Lambda^new_v = Q + R^new (equ_s2e12).
+// Decision equ_s2e7; stop: syndrome after every sweep (the hidden stop rule, l.157-160) or none.
+static FrameResult lbp_frame(const or_code* c, const float* L, const or_opts* o, std::vector<uint8_t>& xhat)
+{
+    const int32_t N = c->N, M = c->M;
+    std::vector<float> Lam(N), R(c->E, 0.0f);    // equ_s2e2: R = 0
+    xhat.assign(N, 0);
+    for (int32_t v = 0; v < N; ++v) {
+        Lam[v] = L[v];
+        xhat[v] = Lam[v] < 0.0f;
+    }
+    FrameResult res;
+    bool converged = false;
+    for (int32_t sweep = 1; sweep <= o->max_iter && !converged; ++sweep) {
+        for (int32_t ci = 0; ci < M; ++ci) {
+            const int32_t b = c->chk_ptr[ci], d = c->chk_ptr[ci + 1] - b;
+            std::vector<float> Qe(d), Ph(d);
+            float S = 0.0f;
+            bool ng = false;
+            for (int32_t k = 0; k < d; ++k) {
+                Qe[k] = Lam[c->e_var[b + k]] - R[b + k];          // equ_s2e10
+                Ph[k] = oracle_phi32(std::fabs(Qe[k]));
+                S += Ph[k];
+                ng = ng != (Qe[k] < 0.0f);
+            }
+            for (int32_t k = 0; k < d; ++k) {
+                const float mag = oracle_phi32(std::fabs(S - Ph[k]));   // equ_s2e4, leave-one-out
+                const bool sg = ng != (Qe[k] < 0.0f);
+                const float Rn = sg ? -mag : mag;
+                const int32_t v = c->e_var[b + k];
+                Lam[v] = Qe[k] + Rn;                              // equ_s2e12
+                R[b + k] = Rn;
+                xhat[v] = Lam[v] < 0.0f;                          // equ_s2e7
+            }
+            res.edge_visits += d;
+        }
+        if (o->stop_rule == OR_STOP_SYNDROME && syndrome_weight_bits(c, xhat) == 0) {
+            converged = true;
+            res.iters = sweep;
+        }
+    }
+    if (!converged) res.iters = o->max_iter;
+    res.flags = (uint8_t)((converged ? 1 : 0) | (syndrome_weight_bits(c, xhat) == 0 ? 2 : 0));
+    return res;
+}
+
+// Flooding BP, fp32 under the contract (reading R22): every iteration
+// computes all V2C messages from the previous posterior, Q_{v->c} = Lambda_v - R_{c->v}
+// (equ_s2e3 written as Lambda minus the own message), then all C2V messages by the phi-domain
+// leave-one-out rule (equ_s2e4, as lbp_frame), then Lambda_v = L_v + sum_c R_{c->v}
+// (equ_s2e6) summed from L_v in ascending check order; decision equ_s2e7; stop as lbp_frame.
+static FrameResult fbp_frame(const or_code* c, const float* L, const or_opts* o, std::vector<uint8_t>& xhat)
+{
+    const int32_t N = c->N, M = c->M;
+    std::vector<float> Lam(N), Rn(c->E, 0.0f);
+    xhat.assign(N, 0);
+    for (int32_t v = 0; v < N; ++v) {
+        Lam[v] = L[v];
+        xhat[v] = Lam[v] < 0.0f;
+    }
+    FrameResult res;
+    bool converged = false;
+    for (int32_t it = 1; it <= o->max_iter && !converged; ++it) {
+        std::vector<float> Rold = Rn;
+        for (int32_t ci = 0; ci < M; ++ci) {
+            const int32_t b = c->chk_ptr[ci], d = c->chk_ptr[ci + 1] - b;
+            std::vector<float> Qe(d), Ph(d);
+            float S = 0.0f;
+            bool ng = false;
+            for (int32_t k = 0; k < d; ++k) {
+                Qe[k] = Lam[c->e_var[b + k]] - Rold[b + k];       // equ_s2e3
+                Ph[k] = oracle_phi32(std::fabs(Qe[k]));
+                S += Ph[k];
+                ng = ng != (Qe[k] < 0.0f);
+            }
+            for (int32_t k = 0; k < d; ++k) {
+                const float mag = oracle_phi32(std::fabs(S - Ph[k]));   // equ_s2e4
+                Rn[b + k] = (ng != (Qe[k] < 0.0f)) ? -mag : mag;
+            }
+            res.edge_visits += d;
+        }
+        for (int32_t v = 0; v < N; ++v) Lam[v] = L[v];
+        for (int32_t ci = 0; ci < M; ++ci)                          // equ_s2e6, ascending checks
+            for (int32_t e = c->chk_ptr[ci]; e < c->chk_ptr[ci + 1]; ++e) Lam[c->e_var[e]] += Rn[e];
+        for (int32_t v = 0; v < N; ++v) xhat[v] = Lam[v] < 0.0f;    // equ_s2e7
+        if (o->stop_rule == OR_STOP_SYNDROME && syndrome_weight_bits(c, xhat) == 0) {
+            converged = true;
+            res.iters = it;
+        }
+    }
+    if (!converged) res.iters = o->max_iter;
+    res.flags = (uint8_t)((converged ? 1 : 0) | (syndrome_weight_bits(c, xhat) == 0 ? 2 : 0));
+    return res;
+}
+
 static bool opts_ok(const or_opts* o)
 {
-    return o && o->max_iter >= 1 && o->max_iter <= 65535 && o->stop_rule >= 0 && o->stop_rule <= 3 &&
-           o->arith >= 0 && o->arith <= 3 && (o->arith != OR_MINSUM || (o->alpha > 0.0f && o->alpha <= 1.0f));
+    if (!o || o->max_iter < 1 || o->max_iter > 65535 || o->stop_rule < 0 || o->stop_rule > 3 || o->arith < 0 ||
+        o->arith > 5)
+        return false;
+    if (o->arith == OR_MINSUM && !(o->alpha > 0.0f && o->alpha <= 1.0f)) return false;
+    if ((o->arith == OR_LBP || o->arith == OR_FBP) && o->stop_rule != OR_STOP_SYNDROME && o->stop_rule != OR_STOP_NONE)
+        return false;
+    return true;
 }
 
 int oracle_decode(const or_code* c, const float* llr, int64_t ld, int64_t frames, const or_opts* o,
@@ -517,7 +622,10 @@ int oracle_decode(const or_code* c, const float* llr, int64_t ld, int64_t frames
     for (int64_t f = 0; f < frames; ++f) {
         const float* L = llr + f * ld;
         FrameResult r;
-        if (o->arith == OR_MINSUM) {
+        if (o->arith == OR_LBP || o->arith == OR_FBP) {
+            r = (o->arith == OR_LBP) ? lbp_frame(c, L, o, xhat) : fbp_frame(c, L, o, xhat);
+            if (omega) std::fill(omega + f * c->M, omega + (f + 1) * c->M, 0.0f);
+        } else if (o->arith == OR_MINSUM) {
             std::vector<float> om;
             r = minsum_frame(c, L, o, xhat, omega ? &om : nullptr, nullptr);
             if (omega) std::copy(om.begin(), om.end(), omega + f * c->M);

@@ -38,7 +38,9 @@ enum { OR_STOP_BELIEF_M = 0, OR_STOP_BELIEF_N = 1, OR_STOP_SYNDROME = 2, OR_STOP
 enum { OR_FP32_CONTRACT = 0,   /* fp32, phi from the arithmetic contract (parity reference) */
        OR_FP64 = 1,            /* fp64, phi = log1p(2/expm1(x)) (= -log tanh(x/2)), phi-domain C2B */
        OR_FP64_LITERAL = 2,    /* fp64, literal psi+ recursion of equ_s4e5/equ_s4e6 (test variant) */
-       OR_MINSUM = 3 };        /* fp32 normalized min-sum CBP (equ_s4e18xx / equ_s4e21xx, reading R20) */
+       OR_MINSUM = 3,          /* fp32 normalized min-sum CBP (equ_s4e18xx / equ_s4e21xx, reading R20) */
+       OR_LBP = 4,             /* fp32 layered BP, the paper's comparison schedule (l.171-197, equ_s2e10/e12; R22) */
+       OR_FBP = 5 };           /* fp32 flooding BP, the paper's comparison schedule (l.102-169, equ_s2e3-e7; R22) */
 
 typedef struct {
     int32_t max_iter;
@@ -48,6 +50,8 @@ typedef struct {
 } or_opts;
 
 /* Decode `frames` LLR vectors (row f at llr + f*ld, N floats).
+ * OR_LBP / OR_FBP take only the stop rules OR_STOP_SYNDROME and OR_STOP_NONE
+ * (the belief window is CBP's); their omega output is all zeros (no check-beliefs).
  * bits: packed hard decisions, bit v%32 of word v/32 (LSB first), ld_words per frame.
  * iters: 1-based sweep in which the stop fired, max_iter if it never did.
  * flags: bit0 converged (stop rule fired and, for belief rules, syndrome verified),
