@@ -296,10 +296,12 @@ def main():
     others = {}
     if not args.no_suite:
         # (config, Eb/N0, frames, stop rule, llr mode, algorithm): the other BASELINE configs, the C2 stop-rule
-        # variants (W=N, syndrome per sweep) and normalized min-sum CBP (NEXT-1) on the same frames
+        # variants (W=N, syndrome per sweep), normalized min-sum CBP (NEXT-1) and the paper's comparison
+        # schedules LBP / FBP (NEXT-3) on the same frames
         suite = [("C1", 2.0, 1_000_000, 0, 0, 0), ("C3a", 2.5, 300_000, 0, 0, 0), ("C5", 2.5, 300_000, 0, 1, 0),
                  ("C3b", 4.0, 300_000, 0, 0, 0), ("C4", 1.5, 3_000, 2, 0, 0), ("C2", 2.0, 1_000_000, 1, 0, 0),
-                 ("C2", 2.0, 1_000_000, 2, 0, 0), ("C2", 2.0, 1_000_000, 0, 0, 1)]
+                 ("C2", 2.0, 1_000_000, 2, 0, 0), ("C2", 2.0, 1_000_000, 0, 0, 1),
+                 ("C2", 2.0, 1_000_000, 2, 0, 2), ("C2", 2.0, 1_000_000, 2, 0, 3)]
         for name, eb, nf, rule, lm, alg in suite:
             ocfg = inputs.CONFIGS[name]
             ob, oz = inputs.config_base(name)
@@ -320,7 +322,7 @@ def main():
             if world > 1:
                 dist.all_reduce(ms, op=dist.ReduceOp.MAX)
             t = c.cpu().numpy()
-            key = f"{name}@{eb}dB" + ("/int8" if lm else "") + ("/min-sum" if alg else "") + \
+            key = f"{name}@{eb}dB" + ("/int8" if lm else "") + ["", "/min-sum", "/LBP", "/FBP"][alg] + \
                 ("" if rule == 0 or name == "C4" else ["", "/W=N", "/syndrome", "/none"][rule])
             others[key] = {
                 "N": oc.N, "K": oc.K, "frames": int(t[0]), "ms": ms.item(),
@@ -328,7 +330,8 @@ def main():
                 "edge_visits_per_s": t[5] / ms.item() * 1e3, "ber": t[1] / max(1, t[0] * oc.K),
                 "fer": t[2] / max(1, t[0]), "avg_iters": t[4] / max(1, t[0]),
                 "stop_rule": ["belief W=M", "belief W=N", "syndrome", "none"][rule],
-                "algorithm": ["log-tanh", "normalized min-sum (alpha 0.75)"][alg],
+                "algorithm": ["CBP log-tanh", "CBP normalized min-sum (alpha 0.75)", "layered BP (comparison)",
+                              "flooding BP (comparison)"][alg],
                 "launch": oc.launch_info()}
 
     cpu = None

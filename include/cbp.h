@@ -98,10 +98,18 @@ typedef enum {
     CBP_STOP_NONE = 3       /* always run max_iter sweeps                              */
 } cbp_stop_rule;
 
-/* Check-belief update rules. */
+/* Decoding algorithms: the two CBP check-belief update rules, and the paper's two
+ * comparison schedules (reading R22) on the same
+ * code graph, channel and counters -- for the CBP vs LBP vs FBP convergence and
+ * error-rate comparisons of the paper (Fig. 6-9, l.613-724).  All four run in fp32
+ * under the arithmetic contract.  LBP / FBP take only CBP_STOP_SYNDROME or
+ * CBP_STOP_NONE (the belief window is CBP's), always run one frame per lane, and
+ * leave d_omega zero (no check-beliefs). */
 typedef enum {
-    CBP_ALG_LOG_TANH = 0,   /* phi-domain psi+/psi- (equ_s4e18, equ_s4e21), fp32 arithmetic contract */
-    CBP_ALG_MIN_SUM = 1     /* normalized min-sum (equ_s4e18xx, equ_s4e21xx, reading R20); needs row degree >= 2 */
+    CBP_ALG_LOG_TANH = 0,   /* CBP, phi-domain psi+/psi- (equ_s4e18, equ_s4e21), fp32 arithmetic contract */
+    CBP_ALG_MIN_SUM = 1,    /* CBP, normalized min-sum (equ_s4e18xx, equ_s4e21xx, reading R20); row degree >= 2 */
+    CBP_ALG_LBP = 2,        /* layered BP (equ_s2e10, equ_s2e4, equ_s2e12), checks in ascending order */
+    CBP_ALG_FBP = 3         /* flooding BP (equ_s2e3, equ_s2e4, equ_s2e6) */
 } cbp_algorithm;
 
 typedef struct {

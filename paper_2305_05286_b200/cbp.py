@@ -38,7 +38,7 @@ class _Opts(ctypes.Structure):
     _fields_ = [("max_iter", _i32), ("stop_rule", _i32), ("algorithm", _i32), ("alpha", _f32)]
 
 
-CBP_ALG_LOG_TANH, CBP_ALG_MIN_SUM = 0, 1
+CBP_ALG_LOG_TANH, CBP_ALG_MIN_SUM, CBP_ALG_LBP, CBP_ALG_FBP = 0, 1, 2, 3
 ALPHA_DEFAULT = 0.75
 
 

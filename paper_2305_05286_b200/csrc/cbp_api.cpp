@@ -99,13 +99,13 @@ struct cbp_code {
     int32_t mb = 0, nb = 0, Z = 0, N = 0, K = 0, M = 0, kb = 0, core = 0, mid = 0, nent = 0, max_dc = 0, min_dc = 0;
     int64_t E = 0;
     bool can_encode = false;
-    std::vector<int4> ent[2];             // schedule tables scaled for geo[alg] (kernel parameters)
+    std::vector<int4> ent[4];             // schedule tables scaled for geo[alg] (kernel parameters)
     std::vector<int32_t> row_ptr;
     std::vector<int16_t> pshift;
     const float4* phi_tab = nullptr;   // per-device table, not owned
     cudaTextureObject_t phi_tex = 0;   // per-device texture object over phi_tab, not owned
-    cbp::Geometry geo[2]{};           // per cbp_algorithm
-    int ctas_per_sm[2] = {1, 1}, num_sms = 1;
+    cbp::Geometry geo[4]{};           // per cbp_algorithm
+    int ctas_per_sm[4] = {1, 1, 1, 1}, num_sms = 1;
 };
 
 extern "C" {
@@ -194,7 +194,7 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
     //   B = {QS s, RS ds, first | kp << 8 | s << 16, first ? ~0 : 0}
     // Byte offsets are relative to the group base: QP at 0, the check records at S0, R at R0.
     auto make_ent = [&](int P, int alg) {
-        const int QS = 8 * P, RS = 4 * P, SU = alg ? 4 : 1, SW = alg ? 4 : 1;
+        const int QS = 8 * P, RS = 4 * P, SU = (alg == 1) ? 4 : 1, SW = (alg == 1) ? 4 : 1;
         const int S0 = 4 * ((2 * P * nb * Z + 3) & ~3), R0 = S0 + 4 * P * SW * mb * Z;
         std::vector<int4> ent(2 * static_cast<size_t>(nent));
         for (int j = 0; j < nb; ++j) {
@@ -289,7 +289,9 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         // group of P frames: QP (2P words per variable), pad to 4 words, check records
         // (P words, or 4P for min-sum's 16-byte records), R (P words per edge), P codewords;
         // groups 16-byte aligned, F > 1 groups staggered by max(Zp, 4) words across banks
-        const int64_t raw = (2LL * P * c->N + 3) / 4 * 4 + P * ((alg ? 4LL : 1LL) * c->M + c->E + nwords);
+        // (flooding BP adds its channel LLRs, P words per variable, after the codewords)
+        const int64_t raw = (2LL * P * c->N + 3) / 4 * 4 +
+                            P * ((alg == 1 ? 4LL : 1LL) * c->M + c->E + nwords + (alg == 3 ? c->N : 0));
         G.slot_words = static_cast<int32_t>(G.F > 1 ? (raw + 31) / 32 * 32 + std::max(G.Zp, 4) : (raw + 3) / 4 * 4);
         G.table_words = 4 * cbp::kPhiTableSegs + (CBP_SCHED_SMEM ? (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4 : 0);
         G.team_threads = G.threads;
@@ -310,12 +312,13 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
                                                             : fixed + 4LL * cbp::kCtlTeamWords * G.teams);
         return G;
     };
-    for (int alg = 0; alg < 2; ++alg) {
-        const cbp::Geometry g1 = make_geo(alg, 1), g2 = make_geo(alg, 2);
+    for (int alg = 0; alg < 4; ++alg) {
+        const cbp::Geometry g1 = make_geo(alg, 1), g2 = alg <= 1 ? make_geo(alg, 2) : cbp::Geometry{};
         // automatic: one frame per lane.  Two interleaved frames per lane halve the warps
         // per SM at the same shared memory and measured slower on every config (C2
         // ber_sim 12.0 vs 7.65 ms); they remain a selectable geometry.
-        const int P = want_P ? want_P : 1;
+        // (the comparison schedules LBP / FBP always run one frame per lane)
+        const int P = (alg >= 2) ? 1 : (want_P ? want_P : 1);
         if (P == 2 && g2.teams == 0) {
             cbp_code_destroy(c);
             return fail(CBP_E_UNSUPPORTED, "cbp_code_create: two frames per lane need the state in shared memory "
@@ -391,8 +394,11 @@ cbp_status check_opts(const cbp_code* c, const cbp_opts* o)
     if (!o) return fail(CBP_E_INVALID, "null opts");
     if (o->max_iter < 1 || o->max_iter > 65535) return fail(CBP_E_INVALID, "opts.max_iter must be in [1, 65535]");
     if (o->stop_rule < 0 || o->stop_rule > 3) return fail(CBP_E_INVALID, "opts.stop_rule must be in [0, 3]");
-    if (o->algorithm != CBP_ALG_LOG_TANH && o->algorithm != CBP_ALG_MIN_SUM)
-        return fail(CBP_E_INVALID, "opts.algorithm must be CBP_ALG_LOG_TANH or CBP_ALG_MIN_SUM");
+    if (o->algorithm < CBP_ALG_LOG_TANH || o->algorithm > CBP_ALG_FBP)
+        return fail(CBP_E_INVALID, "opts.algorithm must be a cbp_algorithm (0..3)");
+    if ((o->algorithm == CBP_ALG_LBP || o->algorithm == CBP_ALG_FBP) && o->stop_rule != CBP_STOP_SYNDROME &&
+        o->stop_rule != CBP_STOP_NONE)
+        return fail(CBP_E_INVALID, "layered / flooding BP take the stop rules CBP_STOP_SYNDROME or CBP_STOP_NONE");
     if (o->algorithm == CBP_ALG_MIN_SUM) {
         if (!(o->alpha > 0.0f && o->alpha <= 1.0f)) return fail(CBP_E_INVALID, "opts.alpha must be in (0, 1]");
         if (c->min_dc < 2) return fail(CBP_E_UNSUPPORTED, "min-sum needs every base row degree >= 2");

@@ -112,9 +112,9 @@ template <int P, int ALG>
 struct Lay {
     static constexpr int QS = 8 * P;
     static constexpr int RS = 4 * P;
-    static constexpr int SU = ALG ? 4 : 1;   // check-record stride in units of RS
+    static constexpr int SU = (ALG == 1) ? 4 : 1;   // check-record stride in units of RS
     static constexpr int SS = RS * SU;
-    static constexpr int SW = ALG ? 4 : 1;   // words per frame in a check record
+    static constexpr int SW = (ALG == 1) ? 4 : 1;   // words per frame in a check record
 };
 
 // A group of P frames.  Record word k of frame p at byte 4 (k P + p) of the record
@@ -135,6 +135,11 @@ struct Grp {
         return reinterpret_cast<float*>(S + c * Ly::SS)[k * P + p];
     }
     __device__ __forceinline__ uint32_t* cwp(int p) const { return cw + p * nwords; }
+    // flooding BP (ALG 3): channel LLRs L_v, after the codewords
+    __device__ __forceinline__ float& Lv(int v, int p) const
+    {
+        return reinterpret_cast<float*>(cw + P * nwords)[v * P + p];
+    }
 };
 
 // Schedule table entry b (two int4, built in cbp_api.cpp for the launch's P and algorithm),
@@ -511,6 +516,217 @@ __device__ __forceinline__ RowOut<P> process_row_ms(const int4* __restrict__ ent
     return o;
 }
 
+// ---------------------------------------------------------------- comparison schedules (NEXT-3)
+// Layered BP (ALG 2, reading R22), one check per lane, two passes over its
+// edges.  Pass 1: Q = Lambda - R_{c->v} (equ_s2e10), Phi = phi(|Q|), S += Phi in ascending order;
+// {Q, Phi} parked in the variable's QP slot (only this lane touches the variable in this row).
+// Pass 2: R^new = sgn phi(|S - Phi|) (equ_s2e4, leave-one-out in the phi domain),
+// Lambda = Q + R^new (equ_s2e12); QP = {Lambda, Lambda} (the sign of .y is the hard bit).
+template <int U, int P>
+__device__ __forceinline__ void lbp_pass1(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
+                                          int k0, const Lane& L, const Grp<P, 2>& g, float (&S)[P], uint32_t (&negw)[P])
+{
+    using Ly = Lay<P, 2>;
+    int aqp[U];
+    float q[U][P], ph[U][P];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int4 A = ent[2 * (e0 + k0 + u)];
+        const int4 B = ent[2 * (e0 + k0 + u) + 1];
+        aqp[u] = A.x + wrap(L.rq + B.x, L.ZQ);
+        float qp[2 * P], ro[P];
+        ldf<2 * P>(g.qp, aqp[u], qp);
+        ldf<P>(g.qp, A.z + L.rr, ro);
+        float lam[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) lam[p] = qp[p];
+        vsub<P>(lam, ro, q[u]);                                  // equ_s2e10
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int p = 0; p < P; ++p) ph[u][p] = phi_sel<CBP_TEX_C2B>(fabsf(q[u][p]), ptab, L);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        vadd<P>(S, ph[u], S);
+        float st[2 * P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            negw[p] ^= __float_as_uint(q[u][p]);
+            st[p] = q[u][p];
+            st[P + p] = ph[u][p];
+        }
+        stf<2 * P>(g.qp, aqp[u], st);
+        (void)Ly::QS;
+    }
+}
+
+template <int U, int P>
+__device__ __forceinline__ void lbp_pass2(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
+                                          int k0, const Lane& L, const Grp<P, 2>& g, const float (&S)[P],
+                                          const uint32_t (&negw)[P])
+{
+    int aqp[U];
+    float q[U][P], ph[U][P], Rn[U][P];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int4 A = ent[2 * (e0 + k0 + u)];
+        const int4 B = ent[2 * (e0 + k0 + u) + 1];
+        aqp[u] = A.x + wrap(L.rq + B.x, L.ZQ);
+        float qp[2 * P];
+        ldf<2 * P>(g.qp, aqp[u], qp);
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            q[u][p] = qp[p];
+            ph[u][p] = qp[P + p];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        float d[P];
+        vsub<P>(S, ph[u], d);
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const float mag = phi_sel<CBP_TEX_B2V>(fabsf(d[p]), ptab, L);   // equ_s2e4
+            Rn[u][p] = __uint_as_float(__float_as_uint(mag) | ((negw[p] ^ __float_as_uint(q[u][p])) & kSign));
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int4 A = ent[2 * (e0 + k0 + u)];
+        float lam[P], st[2 * P];
+        vadd<P>(q[u], Rn[u], lam);                               // equ_s2e12
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            st[p] = lam[p];
+            st[P + p] = lam[p];
+        }
+        stf<P>(g.qp, A.z + L.rr, Rn[u]);
+        stf<2 * P>(g.qp, aqp[u], st);
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void process_row_lbp(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
+                                                int dc, const Lane& L, const Grp<P, 2>& g)
+{
+    float S[P];
+    uint32_t negw[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        S[p] = 0.0f;
+        negw[p] = 0u;
+    }
+    int k0 = 0;
+    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) lbp_pass1<CBP_CHUNK, P>(ent, ptab, e0, k0, L, g, S, negw);
+    for (; k0 < dc; ++k0) lbp_pass1<1, P>(ent, ptab, e0, k0, L, g, S, negw);
+    k0 = 0;
+    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) lbp_pass2<CBP_CHUNK, P>(ent, ptab, e0, k0, L, g, S, negw);
+    for (; k0 < dc; ++k0) lbp_pass2<1, P>(ent, ptab, e0, k0, L, g, S, negw);
+}
+
+// Flooding BP (ALG 3, reading R22).  QP = {Lambda_acc, Lambda_old}: all
+// checks read Lambda_old (the previous iteration's posterior, .y, whose sign is the hard bit)
+// and add their new messages into Lambda_acc (.x, started at L_v) in ascending row order
+// (equ_s2e6); after the last row the variable pass makes Lambda_acc the new Lambda_old.
+// Pass 1: Q = Lambda_old - R (equ_s2e3), Phi = phi(|Q|), S += Phi; the R slot (own edge) parks
+// Phi with the sign of Q.  Pass 2: R^new = sgn phi(|S - Phi|) (equ_s2e4), Lambda_acc += R^new.
+template <int U, int P>
+__device__ __forceinline__ void fbp_pass1(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
+                                          int k0, const Lane& L, const Grp<P, 3>& g, float (&S)[P], uint32_t (&negw)[P])
+{
+    int ar[U];
+    float q[U][P], ph[U][P];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int4 A = ent[2 * (e0 + k0 + u)];
+        const int4 B = ent[2 * (e0 + k0 + u) + 1];
+        const int aqp = A.x + wrap(L.rq + B.x, L.ZQ);
+        ar[u] = A.z + L.rr;
+        float qp[2 * P], ro[P], lo[P];
+        ldf<2 * P>(g.qp, aqp, qp);
+        ldf<P>(g.qp, ar[u], ro);
+#pragma unroll
+        for (int p = 0; p < P; ++p) lo[p] = qp[P + p];
+        vsub<P>(lo, ro, q[u]);                                   // equ_s2e3 (Lambda_old - R)
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int p = 0; p < P; ++p) ph[u][p] = phi_sel<CBP_TEX_C2B>(fabsf(q[u][p]), ptab, L);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        vadd<P>(S, ph[u], S);
+        float st[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            negw[p] ^= __float_as_uint(q[u][p]);
+            st[p] = __uint_as_float(__float_as_uint(ph[u][p]) | (__float_as_uint(q[u][p]) & kSign));
+        }
+        stf<P>(g.qp, ar[u], st);
+    }
+}
+
+template <int U, int P>
+__device__ __forceinline__ void fbp_pass2(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
+                                          int k0, const Lane& L, const Grp<P, 3>& g, const float (&S)[P],
+                                          const uint32_t (&negw)[P])
+{
+    int aqp[U], ar[U];
+    float w[U][P], acc[U][P], Rn[U][P];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int4 A = ent[2 * (e0 + k0 + u)];
+        const int4 B = ent[2 * (e0 + k0 + u) + 1];
+        aqp[u] = A.x + wrap(L.rq + B.x, L.ZQ);
+        ar[u] = A.z + L.rr;
+        ldf<P>(g.qp, ar[u], w[u]);
+        float qp[2 * P];
+        ldf<2 * P>(g.qp, aqp[u], qp);
+#pragma unroll
+        for (int p = 0; p < P; ++p) acc[u][p] = qp[p];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        float ph[P], d[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) ph[p] = fabsf(w[u][p]);
+        vsub<P>(S, ph, d);
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const float mag = phi_sel<CBP_TEX_B2V>(fabsf(d[p]), ptab, L);   // equ_s2e4
+            Rn[u][p] = __uint_as_float(__float_as_uint(mag) | ((negw[p] ^ __float_as_uint(w[u][p])) & kSign));
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        float na[P];
+        vadd<P>(acc[u], Rn[u], na);                              // equ_s2e6, ascending checks
+        stf<P>(g.qp, ar[u], Rn[u]);
+#pragma unroll
+        for (int p = 0; p < P; ++p) reinterpret_cast<float*>(g.qp + aqp[u])[p] = na[p];
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void process_row_fbp(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
+                                                int dc, const Lane& L, const Grp<P, 3>& g)
+{
+    float S[P];
+    uint32_t negw[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        S[p] = 0.0f;
+        negw[p] = 0u;
+    }
+    int k0 = 0;
+    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) fbp_pass1<CBP_CHUNK, P>(ent, ptab, e0, k0, L, g, S, negw);
+    for (; k0 < dc; ++k0) fbp_pass1<1, P>(ent, ptab, e0, k0, L, g, S, negw);
+    k0 = 0;
+    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) fbp_pass2<CBP_CHUNK, P>(ent, ptab, e0, k0, L, g, S, negw);
+    for (; k0 < dc; ++k0) fbp_pass2<1, P>(ent, ptab, e0, k0, L, g, S, negw);
+}
+
 // write hard bits (sign of Phi) of lane r's variables of frame p in row (e0, dc); returns the previous ones
 template <int P, int ALG>
 __device__ __forceinline__ uint32_t swap_row_bits(const int4* __restrict__ ent, int e0, int dc, int r, int Z, int p,
@@ -666,7 +882,8 @@ __device__ void channel_frames(const KernelArgs& a, const Team<MULTI>& tm, const
                     Lv = __fmul_rn(qq, 0.25f);
                 }
                 g.Q(v, p) = Lv;
-                g.PH(v, p) = Lv < 0.0f ? -0.0f : 0.0f;
+                g.PH(v, p) = (ALG >= 2) ? Lv : (Lv < 0.0f ? -0.0f : 0.0f);   // LBP / FBP: Lambda (old) = L
+                if constexpr (ALG == 3) g.Lv(v, p) = Lv;
             }
         }
         for (int e = r; e < C.E; e += Z) g.Rw(e, p) = 0.0f;
@@ -799,7 +1016,10 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                         float* om = a.omega + static_cast<size_t>(fidx[p]) * C.M;
                         for (int c = r; c < C.M; c += Z) {
                             float Sv, m;
-                            if constexpr (ALG == 1) {
+                            if constexpr (ALG >= 2) {
+                                Sv = 0.0f;                               // LBP / FBP: no check-beliefs
+                                m = 0.0f;
+                            } else if constexpr (ALG == 1) {
                                 Sv = g.Sw(c, 2, p);                      // sign bit = sign of Omega
                                 m = g.Sw(c, 0, p);                       // Omega = sgn * min (reading R20)
                             } else {
@@ -917,7 +1137,8 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                     const float Lv = (a.mode == MODE_DECODE_I8) ? __fmul_rn(static_cast<float>(a.q[base + v]), a.qscale)
                                                                 : a.llr[base + v];
                     g.Q(v, p) = Lv;                                  // equ_s4e15
-                    g.PH(v, p) = Lv < 0.0f ? -0.0f : 0.0f;           // hard bit from L (R7)
+                    g.PH(v, p) = (ALG >= 2) ? Lv : (Lv < 0.0f ? -0.0f : 0.0f);   // hard bit from L (R7)
+                    if constexpr (ALG == 3) g.Lv(v, p) = Lv;          // flooding BP keeps L_v
                 }
                 for (int e = r; e < C.E; e += Z) g.Rw(e, p) = 0.0f;   // equ_s4e17
                 for (int c = r; c < C.M; c += Z)                      // equ_s4e16: Omega = inf <=> S = 0
@@ -966,12 +1187,20 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                     // first-visit handling and rollback bits always evaluated
                     if constexpr (ALG == 1)
                         ro = process_row_ms<P, true, true>(ent, e0, dc, sidx, lane, g, s1, a.alpha);
+                    else if constexpr (ALG == 2)
+                        process_row_lbp<P>(ent, ptab, e0, dc, lane, g);
+                    else if constexpr (ALG == 3)
+                        process_row_fbp<P>(ent, ptab, e0, dc, lane, g);
                     else
                         ro = process_row<P, true, true>(ent, ptab, e0, dc, sidx, lane, g, s1);
                     (void)sw1;
                     (void)track;
 #else
-                    if (sw1) {
+                    if constexpr (ALG == 2) {
+                        process_row_lbp<P>(ent, ptab, e0, dc, lane, g);
+                    } else if constexpr (ALG == 3) {
+                        process_row_fbp<P>(ent, ptab, e0, dc, lane, g);
+                    } else if (sw1) {
                         if constexpr (ALG == 1)
                             ro = track ? process_row_ms<P, true, true>(ent, e0, dc, sidx, lane, g, s1, a.alpha)
                                        : process_row_ms<P, true, false>(ent, e0, dc, sidx, lane, g, s1, a.alpha);
@@ -988,14 +1217,18 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                     }
 #endif
                 }
-                // ---- Step 2(3): stopping criterion, counted per check update (R4, R5)
+                // ---- Step 2(3): stopping criterion, counted per check update (R4, R5).  The
+                // ballots double as the team's row barrier; without a belief rule a plain
+                // barrier orders the rows.
                 int first_bad[P], last_bad[P];   // first / last unclean check of the row
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
                     first_bad[p] = Z;
                     last_bad[p] = -1;
                 }
-                if (MULTI) {
+                if (!belief) {
+                    tm.sync();
+                } else if (MULTI) {
                     const int buf = (i & 1) * 64;
                     const int nw = tm.nthreads >> 5;
 #pragma unroll
@@ -1004,16 +1237,15 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                         if ((tm.tl & 31) == 0) ctl[buf + 32 * p + (tm.tl >> 5)] = m;
                     }
                     tm.sync();
-                    if (belief)
 #pragma unroll
-                        for (int p = 0; p < P; ++p)
-                            for (int w = 0; w < nw; ++w) {
-                                const unsigned mw = ctl[buf + 32 * p + w];
-                                if (mw) {
-                                    first_bad[p] = min(first_bad[p], 32 * w + __ffs(mw) - 1);
-                                    last_bad[p] = max(last_bad[p], 32 * w + 31 - __clz(mw));
-                                }
+                    for (int p = 0; p < P; ++p)
+                        for (int w = 0; w < nw; ++w) {
+                            const unsigned mw = ctl[buf + 32 * p + w];
+                            if (mw) {
+                                first_bad[p] = min(first_bad[p], 32 * w + __ffs(mw) - 1);
+                                last_bad[p] = max(last_bad[p], 32 * w + 31 - __clz(mw));
                             }
+                        }
                 } else {
                     __syncwarp();
 #pragma unroll
@@ -1079,6 +1311,19 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                 }
             }
             // ---- end of sweep
+            if constexpr (ALG == 3) {
+                // flooding BP variable pass (equ_s2e6): the accumulated posterior becomes
+                // Lambda_old (sign = hard bit, equ_s2e7); the accumulator restarts at L_v
+                tm.sync();
+#pragma unroll
+                for (int p = 0; p < P; ++p)
+                    if (active[p] && tm.lane_on)
+                        for (int v = r; v < C.N; v += Z) {
+                            g.PH(v, p) = g.Q(v, p);
+                            g.Q(v, p) = g.Lv(v, p);
+                        }
+                tm.sync();
+            }
             bool done[P];
 #pragma unroll
             for (int p = 0; p < P; ++p) {
@@ -1160,10 +1405,26 @@ int launch_phi_table(float4* out, void* stream)
 // ---------------------------------------------------------------- host-side launch
 // Instantiations: P = 1 for every geometry (state in smem or global, warp or multi-warp
 // teams up to 1024 threads); P = 2 only with state in smem and at most 256 threads.
+// the kernel of algorithm g.alg (P = 2 exists for the CBP rules 0 and 1 only)
+template <bool MULTI, bool SMEM, int MAXT, int P>
+static auto kernel_of(const Geometry& g)
+{
+    if constexpr (P == 1) {
+        switch (g.alg) {
+        case 1: return cbp_kernel<MULTI, SMEM, MAXT, 1, P>;
+        case 2: return cbp_kernel<MULTI, SMEM, MAXT, 2, P>;
+        case 3: return cbp_kernel<MULTI, SMEM, MAXT, 3, P>;
+        default: return cbp_kernel<MULTI, SMEM, MAXT, 0, P>;
+        }
+    } else {
+        return (g.alg == 1) ? cbp_kernel<MULTI, SMEM, MAXT, 1, P> : cbp_kernel<MULTI, SMEM, MAXT, 0, P>;
+    }
+}
+
 template <bool MULTI, bool SMEM, int MAXT, int P>
 static int launch_t(const KernelArgs& a, const Geometry& g, int grid, cudaStream_t st)
 {
-    auto k = (g.alg == 1) ? cbp_kernel<MULTI, SMEM, MAXT, 1, P> : cbp_kernel<MULTI, SMEM, MAXT, 0, P>;
+    auto k = kernel_of<MULTI, SMEM, MAXT, P>(g);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
     k<<<grid, g.threads, g.smem_bytes, st>>>(a);
@@ -1173,7 +1434,7 @@ static int launch_t(const KernelArgs& a, const Geometry& g, int grid, cudaStream
 template <bool MULTI, bool SMEM, int MAXT, int P>
 static int occ_t(const Geometry& g, int* out)
 {
-    auto k = (g.alg == 1) ? cbp_kernel<MULTI, SMEM, MAXT, 1, P> : cbp_kernel<MULTI, SMEM, MAXT, 0, P>;
+    auto k = kernel_of<MULTI, SMEM, MAXT, P>(g);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
     return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, g.threads, g.smem_bytes));
@@ -1183,7 +1444,7 @@ template <template <bool, bool, int, int> class Fn, typename... Args>
 static int dispatch(const Geometry& g, Args... args)
 {
     if (g.P == 2) {
-        if (!g.state_in_smem || g.threads > 256) return static_cast<int>(cudaErrorInvalidConfiguration);
+        if (!g.state_in_smem || g.threads > 256 || g.alg > 1) return static_cast<int>(cudaErrorInvalidConfiguration);
         return g.multi ? Fn<true, true, 256, 2>::run(g, args...) : Fn<false, true, 256, 2>::run(g, args...);
     }
     if (!g.multi)

@@ -357,3 +357,57 @@ def test_decode_host_pipeline(codes):
     oo = o.decode(np.ascontiguousarray(l_o), 30)
     assert (out["bits"].numpy()[idx].view(np.uint32)[:, :oo["bits"].shape[1]] == oo["bits"]).all()
     assert (out["iters"].numpy()[idx] == oo["iters"]).all()
+
+
+# ---------------------------------------------------------------- NEXT-3: comparison schedules
+BP_ALGS = [(2, oracle.LBP), (3, oracle.FBP)]
+
+
+@pytest.mark.parametrize("alg,arith", BP_ALGS, ids=["LBP", "FBP"])
+@pytest.mark.parametrize("name,ebn0,frames", [("C1", 2.0, 2000), ("C2", 2.0, 600), ("C2", 1.0, 200),
+                                              ("C3a", 2.0, 100), ("C3b", 3.5, 100), ("T24", 4.0, 500)])
+def test_bp_schedule_decode_parity(codes, alg, arith, name, ebn0, frames):
+    """Layered and flooding BP (the paper's comparison schedules, reading R22) on the
+    GPU equal the oracle's fp32 LBP / FBP bit for bit: decisions, iterations, flags,
+    edge visits, for the syndrome stop and for a fixed number of sweeps."""
+    g, o = codes(name)
+    mi = inputs.CONFIGS[name].max_iter
+    llr, _ = o.channel(ebn0, seed=41, frame_begin=0, frames=frames)
+    for rule, m in ((oracle.STOP_SYNDROME, mi), (oracle.STOP_NONE, 3)):
+        oo = o.decode(llr, m, rule, arith)
+        go = gpu_decode(g, llr, m, rule, algorithm=alg)
+        assert_same(go, oo, o.N, omega=False)
+
+
+@pytest.mark.parametrize("alg,arith", BP_ALGS, ids=["LBP", "FBP"])
+def test_bp_schedule_degree_one_and_global_state(codes, fpl, alg, arith):
+    base = inputs.construct_base((8, 14, 8, 4, 0, 3, 3), 1)
+    g, o = make_code(base, 8, fpl), oracle.OracleCode(base, 8)
+    llr, _ = o.channel(3.0, seed=42, frame_begin=0, frames=400)
+    assert_same(gpu_decode(g, llr, 25, oracle.STOP_SYNDROME, algorithm=alg),
+                o.decode(llr, 25, oracle.STOP_SYNDROME, arith), o.N, omega=False)
+    g, o = codes("C4")
+    llr, _ = o.channel(1.5, seed=43, frame_begin=0, frames=4)
+    assert_same(gpu_decode(g, llr, 10, oracle.STOP_SYNDROME, algorithm=alg),
+                o.decode(llr, 10, oracle.STOP_SYNDROME, arith), o.N, omega=False)
+
+
+@pytest.mark.parametrize("alg,arith", BP_ALGS, ids=["LBP", "FBP"])
+@pytest.mark.parametrize("name,ebn0,frames,llr_mode", [("C2", 2.0, 1500, 0), ("C2", 2.5, 800, 1), ("C3a", 2.5, 100, 0)])
+def test_bp_schedule_ber_sim_parity(codes, alg, arith, name, ebn0, frames, llr_mode):
+    g, o = codes(name)
+    mi = inputs.CONFIGS[name].max_iter
+    want = o.ber_sim(ebn0, 44, 100, frames, mi, oracle.STOP_SYNDROME, llr_mode, arith=arith)
+    got = g.ber_sim(ebn0, 44, 100, frames, mi, oracle.STOP_SYNDROME, llr_mode, algorithm=alg).cpu().numpy()
+    assert list(got) == list(want), dict(zip(oracle.COUNT_NAMES, zip(got, want)))
+
+
+def test_bp_schedule_rejects_belief_rules(codes):
+    g, o = codes("C2")
+    x = torch.zeros((2, 648), dtype=torch.float32, device="cuda")
+    for alg in (2, 3):
+        for rule in (0, 1):
+            with pytest.raises(RuntimeError):
+                g.decode(x, 5, rule, algorithm=alg)
+    with pytest.raises(RuntimeError):
+        g.decode(x, 5, 2, algorithm=4)
