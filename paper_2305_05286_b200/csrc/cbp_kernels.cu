@@ -355,10 +355,8 @@ __device__ __forceinline__ RowOut<P> process_row(const int4* __restrict__ ent, c
     ldf<P>(g.S, sidx, Sold);
     int k0 = 0;
     for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) edge_chunk<CBP_CHUNK, P, SW1, TRACK>(ent, ptab, e0, k0, L, g, s1, acc);
-    if (CBP_CHUNK > 2 && k0 + 2 <= dc) {
-        edge_chunk<2, P, SW1, TRACK>(ent, ptab, e0, k0, L, g, s1, acc);
-        k0 += 2;
-    }
+    if (CBP_CHUNK > 2)
+        for (; k0 + 2 <= dc; k0 += 2) edge_chunk<2, P, SW1, TRACK>(ent, ptab, e0, k0, L, g, s1, acc);
     if (k0 < dc) edge_chunk<1, P, SW1, TRACK>(ent, ptab, e0, k0, L, g, s1, acc);
     RowOut<P> o;
     float Snew[P];
@@ -497,10 +495,8 @@ __device__ __forceinline__ RowOut<P> process_row_ms(const int4* __restrict__ ent
     ld_rec<P>(g.S, Ly::SU * sidx, om1, om2, oow);
     int k0 = 0;
     for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) edge_chunk_ms<CBP_CHUNK, P, SW1, TRACK>(ent, e0, k0, L, g, s1, alpha, acc);
-    if (CBP_CHUNK > 2 && k0 + 2 <= dc) {
-        edge_chunk_ms<2, P, SW1, TRACK>(ent, e0, k0, L, g, s1, alpha, acc);
-        k0 += 2;
-    }
+    if (CBP_CHUNK > 2)
+        for (; k0 + 2 <= dc; k0 += 2) edge_chunk_ms<2, P, SW1, TRACK>(ent, e0, k0, L, g, s1, alpha, acc);
     if (k0 < dc) edge_chunk_ms<1, P, SW1, TRACK>(ent, e0, k0, L, g, s1, alpha, acc);
     uint32_t nw[P];
     RowOut<P> o;
@@ -534,6 +530,7 @@ __device__ __forceinline__ void lbp_pass1(const int4* __restrict__ ent, const fl
         const int4 A = ent[2 * (e0 + k0 + u)];
         const int4 B = ent[2 * (e0 + k0 + u) + 1];
         aqp[u] = A.x + wrap(L.rq + B.x, L.ZQ);
+        CBP_CHECK(aqp[u] >= 0 && aqp[u] + Ly::QS <= L.slot_bytes && A.z + L.rr + Ly::RS <= L.slot_bytes);
         float qp[2 * P], ro[P];
         ldf<2 * P>(g.qp, aqp[u], qp);
         ldf<P>(g.qp, A.z + L.rr, ro);
@@ -643,6 +640,7 @@ __device__ __forceinline__ void fbp_pass1(const int4* __restrict__ ent, const fl
         const int4 B = ent[2 * (e0 + k0 + u) + 1];
         const int aqp = A.x + wrap(L.rq + B.x, L.ZQ);
         ar[u] = A.z + L.rr;
+        CBP_CHECK(aqp >= 0 && aqp + 8 * P <= L.slot_bytes && ar[u] + 4 * P <= L.slot_bytes);
         float qp[2 * P], ro[P], lo[P];
         ldf<2 * P>(g.qp, aqp, qp);
         ldf<P>(g.qp, ar[u], ro);
