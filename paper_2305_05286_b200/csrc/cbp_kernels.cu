@@ -32,20 +32,13 @@ constexpr uint32_t kSign = 0x80000000u;
 #ifndef CBP_CHUNK
 #define CBP_CHUNK 3
 #endif
-// A/B switches: 1 = stage the schedule tables in shared memory (default), 0 = read them
-// from the kernel parameters in the hot loop.  CBP_TEX_C2B / CBP_TEX_B2V: evaluate the
-// C2B / B2V phi with the table row fetched through the texture pipe instead of LDS.
-#ifndef CBP_SCHED_SMEM
-#define CBP_SCHED_SMEM 1
-#endif
+// A/B switches CBP_TEX_C2B / CBP_TEX_B2V: evaluate the C2B / B2V phi with the table row
+// fetched through the texture pipe instead of LDS (default: C2B through TEX).
 #ifndef CBP_TEX_C2B
 #define CBP_TEX_C2B 1
 #endif
 #ifndef CBP_TEX_B2V
 #define CBP_TEX_B2V 0
-#endif
-#ifndef CBP_ONE_VARIANT
-#define CBP_ONE_VARIANT 1
 #endif
 
 // ---------------------------------------------------------------- byte-addressed vector access
@@ -903,21 +896,15 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
 
     // ---- stage the phi table and the schedule tables (a1).  The tables travel in the
     // kernel parameters; reading them in the hot loop straight from the constant bank
-    // (CBP_SCHED_SMEM=0) measured 20% slower on C2 than from shared memory.
+    // measured 20% slower on C2 than from shared memory (constant-cache misses).
     float4* ptab = reinterpret_cast<float4*>(smem);
     for (int k = threadIdx.x; k < kPhiSegs; k += blockDim.x) ptab[k] = C.phi_tab[k];
-#if CBP_SCHED_SMEM
     int4* ent = reinterpret_cast<int4*>(smem + 4 * kPhiSegs);
     int32_t* row_ptr = reinterpret_cast<int32_t*>(smem + 4 * kPhiSegs + 8 * C.nent);
     int16_t* pshift = reinterpret_cast<int16_t*>(row_ptr + mb + 1);
     for (int k = threadIdx.x; k < 2 * C.nent; k += blockDim.x) ent[k] = a.ent[k];
     for (int k = threadIdx.x; k <= mb; k += blockDim.x) row_ptr[k] = a.row_ptr[k];
     for (int k = threadIdx.x; k < mb; k += blockDim.x) pshift[k] = a.pshift[k];
-#else
-    const int4* ent = a.ent;
-    const int32_t* row_ptr = a.row_ptr;
-    const int16_t* pshift = a.pshift;
-#endif
     Team<MULTI> tm;
     tm.nthreads = a.team_threads;
     tm.tidx = threadIdx.x / a.team_threads;
@@ -1168,19 +1155,10 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                     ro.Snew[p] = ro.Sold[p] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                 }
                 if (live && tm.lane_on) {
-                    // the window can only fill in this row if consec + Z >= W (R4); otherwise
-                    // no rollback information is needed
-                    bool sw1 = false, track = false;
-                    uint32_t s1[P];   // all ones for a frame in sweep 1 (first-visit kill mask)
+                    uint32_t s1[P];   // all ones for a frame in sweep 1 (first-visit kill mask, R1)
 #pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        const bool f1 = active[p] && sweep[p] == 1;
-                        s1[p] = f1 ? kFull : 0u;
-                        sw1 |= f1;
-                        track |= active[p] && belief && consec[p] + Z >= W;
-                    }
+                    for (int p = 0; p < P; ++p) s1[p] = (active[p] && sweep[p] == 1) ? kFull : 0u;
                     const int sidx = (i * Z + r) * Ly::RS;
-#if CBP_ONE_VARIANT
                     // one code path for every row (smaller code, fewer instruction-cache misses):
                     // first-visit handling and rollback bits always evaluated
                     if constexpr (ALG == 1)
@@ -1191,29 +1169,6 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                         process_row_fbp<P>(ent, ptab, e0, dc, lane, g);
                     else
                         ro = process_row<P, true, true>(ent, ptab, e0, dc, sidx, lane, g, s1);
-                    (void)sw1;
-                    (void)track;
-#else
-                    if constexpr (ALG == 2) {
-                        process_row_lbp<P>(ent, ptab, e0, dc, lane, g);
-                    } else if constexpr (ALG == 3) {
-                        process_row_fbp<P>(ent, ptab, e0, dc, lane, g);
-                    } else if (sw1) {
-                        if constexpr (ALG == 1)
-                            ro = track ? process_row_ms<P, true, true>(ent, e0, dc, sidx, lane, g, s1, a.alpha)
-                                       : process_row_ms<P, true, false>(ent, e0, dc, sidx, lane, g, s1, a.alpha);
-                        else
-                            ro = track ? process_row<P, true, true>(ent, ptab, e0, dc, sidx, lane, g, s1)
-                                       : process_row<P, true, false>(ent, ptab, e0, dc, sidx, lane, g, s1);
-                    } else {
-                        if constexpr (ALG == 1)
-                            ro = track ? process_row_ms<P, false, true>(ent, e0, dc, sidx, lane, g, s1, a.alpha)
-                                       : process_row_ms<P, false, false>(ent, e0, dc, sidx, lane, g, s1, a.alpha);
-                        else
-                            ro = track ? process_row<P, false, true>(ent, ptab, e0, dc, sidx, lane, g, s1)
-                                       : process_row<P, false, false>(ent, ptab, e0, dc, sidx, lane, g, s1);
-                    }
-#endif
                 }
                 // ---- Step 2(3): stopping criterion, counted per check update (R4, R5).  The
                 // ballots double as the team's row barrier; without a belief rule a plain

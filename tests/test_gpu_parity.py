@@ -411,3 +411,21 @@ def test_bp_schedule_rejects_belief_rules(codes):
                 g.decode(x, 5, rule, algorithm=alg)
     with pytest.raises(RuntimeError):
         g.decode(x, 5, 2, algorithm=4)
+
+
+def test_sweep_gpu_runner_resume(codes, tmp_path):
+    """paper_2305_05286_b200.sweep with the product runner (cbp_ber_sim): chunked and
+    resumed totals equal one fused launch over the whole frame range."""
+    from paper_2305_05286_b200.sweep import gpu_runner, run_sweep
+    g, o = codes("C2")
+    run = gpu_runner(g, 30, 5)
+    hdr = {"config": "C2", "seed": 5}
+    out = tmp_path / "s.jsonl"
+    run_sweep(run, [2.0], 150_000, 40_000, hdr, out)
+    lines = out.read_text().splitlines()
+    out.write_text("\n".join(lines[:-2]) + "\n")                 # drop the last two chunks: resume redoes them
+    res = run_sweep(run, [2.0, 2.5], 150_000, 40_000, hdr, out)
+    for eb in (2.0, 2.5):
+        want = g.ber_sim(eb, 5, 0, 150_000, 30).cpu().numpy()
+        c = res[eb]["counts"]
+        assert [c[k] for k in cbp.COUNT_NAMES] == list(want)
