@@ -429,3 +429,54 @@ def test_sweep_gpu_runner_resume(codes, tmp_path):
         want = g.ber_sim(eb, 5, 0, 150_000, 30).cpu().numpy()
         c = res[eb]["counts"]
         assert [c[k] for k in cbp.COUNT_NAMES] == list(want)
+
+
+def _fused_vs_unfused(g, eb, seed, begin, frames, mi, chunk, llr_mode=0):
+    """channel -> (int8) decode -> compare on the GPU, chunk by chunk: the counters the fused
+    ber_sim must reproduce, plus the indices of the frames with errors / no convergence."""
+    tot = np.zeros(8, np.int64)
+    bad = []
+    for b in range(begin, begin + frames, chunk):
+        n = min(chunk, begin + frames - b)
+        llr, cw = g.channel(eb, seed, b, n, llr_mode=llr_mode)
+        if llr_mode:
+            q = torch.zeros((n, (g.N + 15) // 16 * 16), dtype=torch.int8, device=llr.device)
+            q[:, :g.N] = torch.round(llr[:, :g.N] * 4).to(torch.int8)
+            out = g.decode_i8(q, 0.25, mi, ev=True)
+        else:
+            out = g.decode(llr, mi, ev=True)
+        d = cbp.unpack_bits(out["bits"], g.N) != cbp.unpack_bits(cw, g.N)
+        info = d[:, :g.K].sum(1)
+        tot += np.array([n, info.sum().item(), (info > 0).sum().item(), d.any(1).sum().item(),
+                         out["iters"].sum().item(), out["ev"].sum().item(),
+                         ((out["flags"] & 1) == 0).sum().item(), 0], np.int64)
+        bad += (b + torch.nonzero((info > 0) | ((out["flags"] & 1) == 0)).flatten().cpu().numpy()).tolist()
+    return tot, bad
+
+
+@pytest.mark.parametrize("name,eb,begin,frames,llr_mode", [
+    ("C3a", 1.5, 0, 10_000_000, 0),                       # BASELINE configs[2]: 10^7 frames per point
+    ("C5", 2.5, 1_000_000_000 - 20_000_000, 20_000_000, 1)])   # configs[4]: the top slice of 10^9, int8 stream
+def test_ber_sim_full_size_sampled_c3(codes, name, eb, begin, frames, llr_mode):
+    """Full-size fused ber_sim in the bench launch configuration for the N=1944 code:
+    shard invariance, the fused counters reproduced by channel -> decode -> compare on
+    the GPU (first 10^6 frames of the range), and sampled plus error frames equal the
+    oracle frame by frame."""
+    g, o = codes("C3a")
+    mi = 30
+    full = g.ber_sim(eb, 1, begin, frames, mi, llr_mode=llr_mode).cpu().numpy()
+    cut = frames // 3
+    parts = (g.ber_sim(eb, 1, begin, cut, mi, llr_mode=llr_mode) +
+             g.ber_sim(eb, 1, begin + cut, frames - cut, mi, llr_mode=llr_mode)).cpu().numpy()
+    assert (full == parts).all() and full[0] == frames
+    sub = 1_000_000
+    want = g.ber_sim(eb, 1, begin, sub, mi, llr_mode=llr_mode).cpu().numpy()
+    tot, bad = _fused_vs_unfused(g, eb, 1, begin, sub, mi, 250_000, llr_mode)
+    assert (tot[:7] == want[:7]).all(), (tot, want)
+    rng = np.random.default_rng(4)
+    sample = sorted(set((begin + rng.integers(0, sub, 40)).tolist() + bad[:40]))
+    for fidx in sample:
+        llr_o, _ = o.channel(eb, 1, fidx, 1, llr_mode=llr_mode)
+        llr_g, _ = g.channel(eb, 1, fidx, 1, llr_mode=llr_mode)
+        assert (llr_g[:, :o.N].cpu().numpy() == llr_o).all()
+        assert_same(gpu_decode(g, llr_o, mi), o.decode(llr_o, mi, want_omega=True), o.N)
