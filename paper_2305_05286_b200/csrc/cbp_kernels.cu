@@ -240,14 +240,14 @@ struct RowAcc {
 
 // U consecutive edges of lane r's check for the P frames.  Loads first, then U x P
 // independent B2V phi chains, commits / V2C, U x P independent C2B phi chains and
-// the ordered S accumulation (reading R12).  SW1: some frame of the group is in
-// sweep 1 (s1[p]); its first visits get R^new = 0 (reading R1) -- the commit then
-// writes that 0 into an R slot that still holds its initial 0 (no edge of the
-// column has been processed yet in sweep 1), identical to not writing.  TRACK
-// records the previous hard bits (only rows where the belief window can fire).
+// the ordered S accumulation (reading R12).  A frame in sweep 1 (s1m[p] all ones)
+// gets R^new = 0 on the first visits of a column (reading R1; kill mask B.w) -- the
+// commit then writes that 0 into an R slot that still holds its initial 0 (no edge
+// of the column has been processed yet in sweep 1), identical to not writing.  The
+// previous hard bits are recorded for the rollback of a mid-row stop (R5).
 // R_{ci->v} is read after the commit of R_{cj->v}: for a degree-1 column both are
 // the same slot, which realises "commit before read" (R3) through memory order.
-template <int U, int P, bool SW1, bool TRACK>
+template <int U, int P>
 __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int k0,
                                            const Lane& L, const Grp<P, 0>& g, const uint32_t (&s1m)[P], RowAcc<P>& acc)
 {
@@ -267,7 +267,7 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
         aqp[u] = A.x + tq;
         aw[u] = A.w + tr;
         ar[u] = A.z + L.rr;
-        fkill[u] = SW1 ? static_cast<uint32_t>(B.w) : 0u;
+        fkill[u] = static_cast<uint32_t>(B.w);
         float qp[2 * P];
         ldf<2 * P>(g.qp, aqp[u], qp);
 #pragma unroll
@@ -305,7 +305,7 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
             lb[u][p] = __float_as_uint(lam[p]) & kSign;      // hard decision, equ_s2e7
             acc.flipw[p] |= __float_as_uint(lam[p]) ^ __float_as_uint(p0[u][p]);   // equ_s4e24 (R7), bit 31
             // previous hard bit, edge k at bit dc-1-k (one funnel shift)
-            if (TRACK) acc.oldbits[p] = __funnelshift_l(__float_as_uint(p0[u][p]), acc.oldbits[p], 1);
+            acc.oldbits[p] = __funnelshift_l(__float_as_uint(p0[u][p]), acc.oldbits[p], 1);
         }
     }
     float ph[U][P];
@@ -335,7 +335,7 @@ struct RowOut {
     bool ok[P];
 };
 
-template <int P, bool SW1, bool TRACK>
+template <int P>
 __device__ __forceinline__ RowOut<P> process_row(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
                                                  int dc, int sidx, const Lane& L, const Grp<P, 0>& g,
                                                  const uint32_t (&s1)[P])
@@ -349,10 +349,10 @@ __device__ __forceinline__ RowOut<P> process_row(const int4* __restrict__ ent, c
     }
     ldf<P>(g.S, sidx, Sold);
     int k0 = 0;
-    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) edge_chunk<CBP_CHUNK, P, SW1, TRACK>(ent, ptab, e0, k0, L, g, s1, acc);
+    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) edge_chunk<CBP_CHUNK, P>(ent, ptab, e0, k0, L, g, s1, acc);
     if (CBP_CHUNK > 2)
-        for (; k0 + 2 <= dc; k0 += 2) edge_chunk<2, P, SW1, TRACK>(ent, ptab, e0, k0, L, g, s1, acc);
-    if (k0 < dc) edge_chunk<1, P, SW1, TRACK>(ent, ptab, e0, k0, L, g, s1, acc);
+        for (; k0 + 2 <= dc; k0 += 2) edge_chunk<2, P>(ent, ptab, e0, k0, L, g, s1, acc);
+    if (k0 < dc) edge_chunk<1, P>(ent, ptab, e0, k0, L, g, s1, acc);
     RowOut<P> o;
     float Snew[P];
 #pragma unroll
@@ -403,7 +403,7 @@ __device__ __forceinline__ void st_rec(char* S, int off, const float (&m1)[P], c
     }
 }
 
-template <int U, int P, bool SW1, bool TRACK>
+template <int U, int P>
 __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int e0, int k0, const Lane& L,
                                               const Grp<P, 1>& g, const uint32_t (&s1m)[P], float alpha, MsAcc<P>& acc)
 {
@@ -422,7 +422,7 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
         aqp[u] = A.x + tq;
         aw[u] = A.w + tr;
         ar[u] = A.z + L.rr;
-        fkill[u] = SW1 ? static_cast<uint32_t>(B.w) : 0u;
+        fkill[u] = static_cast<uint32_t>(B.w);
         kp[u] = (B.z >> 8) & 0xff;
         float qp[2 * P];
         ldf<2 * P>(g.qp, aqp[u], qp);
@@ -456,7 +456,7 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
             const uint32_t lb = __float_as_uint(lam[p]) & kSign;
             acc.flipw[p] |= __float_as_uint(lam[p]) ^ __float_as_uint(p0[u][p]);
             // previous hard bit, edge k at bit dc-1-k (one funnel shift)
-            if (TRACK) acc.oldbits[p] = __funnelshift_l(__float_as_uint(p0[u][p]), acc.oldbits[p], 1);
+            acc.oldbits[p] = __funnelshift_l(__float_as_uint(p0[u][p]), acc.oldbits[p], 1);
             // C2B (equ_s4e21xx), in ascending edge order, branch-free:
             // m < m1: (m1, m2, own) <- (m, m1, k); else m2 <- min(m2, m).  m1 <= m2 always.
             const float m = __fmul_rn(alpha, fabsf(qn[p]));
@@ -472,7 +472,7 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
     }
 }
 
-template <int P, bool SW1, bool TRACK>
+template <int P>
 __device__ __forceinline__ RowOut<P> process_row_ms(const int4* __restrict__ ent, int e0, int dc, int sidx,
                                                     const Lane& L, const Grp<P, 1>& g, const uint32_t (&s1)[P],
                                                     float alpha)
@@ -489,10 +489,10 @@ __device__ __forceinline__ RowOut<P> process_row_ms(const int4* __restrict__ ent
     uint32_t oow[P];
     ld_rec<P>(g.S, Ly::SU * sidx, om1, om2, oow);
     int k0 = 0;
-    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) edge_chunk_ms<CBP_CHUNK, P, SW1, TRACK>(ent, e0, k0, L, g, s1, alpha, acc);
+    for (; k0 + CBP_CHUNK <= dc; k0 += CBP_CHUNK) edge_chunk_ms<CBP_CHUNK, P>(ent, e0, k0, L, g, s1, alpha, acc);
     if (CBP_CHUNK > 2)
-        for (; k0 + 2 <= dc; k0 += 2) edge_chunk_ms<2, P, SW1, TRACK>(ent, e0, k0, L, g, s1, alpha, acc);
-    if (k0 < dc) edge_chunk_ms<1, P, SW1, TRACK>(ent, e0, k0, L, g, s1, alpha, acc);
+        for (; k0 + 2 <= dc; k0 += 2) edge_chunk_ms<2, P>(ent, e0, k0, L, g, s1, alpha, acc);
+    if (k0 < dc) edge_chunk_ms<1, P>(ent, e0, k0, L, g, s1, alpha, acc);
     uint32_t nw[P];
     RowOut<P> o;
 #pragma unroll
@@ -1164,13 +1164,13 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                     // one code path for every row (smaller code, fewer instruction-cache misses):
                     // first-visit handling and rollback bits always evaluated
                     if constexpr (ALG == 1)
-                        ro = process_row_ms<P, true, true>(ent, e0, dc, sidx, lane, g, s1, a.alpha);
+                        ro = process_row_ms<P>(ent, e0, dc, sidx, lane, g, s1, a.alpha);
                     else if constexpr (ALG == 2)
                         process_row_lbp<P>(ent, ptab, e0, dc, lane, g);
                     else if constexpr (ALG == 3)
                         process_row_fbp<P>(ent, ptab, e0, dc, lane, g);
                     else
-                        ro = process_row<P, true, true>(ent, ptab, e0, dc, sidx, lane, g, s1);
+                        ro = process_row<P>(ent, ptab, e0, dc, sidx, lane, g, s1);
                 }
                 // ---- Step 2(3): stopping criterion, counted per check update (R4, R5).  The
                 // ballots double as the team's row barrier; without a belief rule a plain
