@@ -480,3 +480,64 @@ def test_ber_sim_full_size_sampled_c3(codes, name, eb, begin, frames, llr_mode):
         llr_g, _ = g.channel(eb, 1, fidx, 1, llr_mode=llr_mode)
         assert (llr_g[:, :o.N].cpu().numpy() == llr_o).all()
         assert_same(gpu_decode(g, llr_o, mi), o.decode(llr_o, mi, want_omega=True), o.N)
+
+
+def test_abi_error_paths(codes):
+    """The documented error behaviour of include/cbp.h: every invalid argument returns
+    CBP_E_INVALID (1) / CBP_E_UNSUPPORTED (2) with a message and launches nothing."""
+    import ctypes
+    L = cbp.lib()
+    g, o = codes("C2")
+    h = g.handle
+    dev = torch.device("cuda", 0)
+    x = torch.zeros((4, 648), dtype=torch.float32, device=dev)
+    bits = torch.zeros((4, 21), dtype=torch.int32, device=dev)
+    it = torch.zeros(4, dtype=torch.int32, device=dev)
+    fl = torch.zeros(4, dtype=torch.uint8, device=dev)
+    ok = cbp.cbp._Opts(30, 0, 0, 0.75)
+
+    def dec(ptr=None, ld=648, frames=4, opts=ok, lw=21, b=bits):
+        return L.cbp_decode(h, x.data_ptr() if ptr is None else ptr, ld, frames, ctypes.byref(opts),
+                            b.data_ptr() if b is not None else None, lw, it.data_ptr(), fl.data_ptr(), None, None,
+                            None)
+    assert dec() == 0
+    assert dec(ld=640) == 1                                    # ld < N
+    assert dec(ld=650) == 1                                    # ld * 4 not a multiple of 16
+    assert dec(ptr=x.data_ptr() + 4) == 1                      # misaligned input
+    assert dec(frames=-1) == 1
+    assert dec(lw=20) == 1                                     # ld_words < ceil(N/32)
+    assert dec(b=None) == 1                                    # null output
+    assert dec(frames=0, b=None) == 0                          # empty batch is a no-op
+    for bad in ((0, 0, 0, 0.75), (70000, 0, 0, 0.75), (5, 4, 0, 0.75), (5, 0, 4, 0.75), (5, 0, 1, 0.0),
+                (5, 0, 2, 0.75), (5, 1, 3, 0.75)):
+        assert dec(opts=cbp.cbp._Opts(*bad)) == 1, bad
+    assert b"opts" in L.cbp_last_error() or b"stop" in L.cbp_last_error()
+    cnt = torch.zeros(8, dtype=torch.int64, device=dev)
+    assert L.cbp_ber_sim(h, 2.0, 1, 0, 10, ctypes.byref(ok), 2, cnt.data_ptr(), None) == 1   # llr_mode
+    assert L.cbp_ber_sim(h, float("nan"), 1, 0, 10, ctypes.byref(ok), 0, cnt.data_ptr(), None) == 1
+    assert L.cbp_ber_sim(h, 2.0, 1, -1, 10, ctypes.byref(ok), 0, cnt.data_ptr(), None) == 1
+    assert L.cbp_ber_sim(h, 2.0, 1, 0, 10, ctypes.byref(ok), 0, None, None) == 1
+    assert int(cnt.sum()) == 0                                 # nothing ran
+
+    def create(base, Z, fpl=0):
+        hh = ctypes.c_void_p()
+        b = np.ascontiguousarray(base, np.int16)
+        cfg = cbp.cbp._CodeConfig(fpl)
+        rc = L.cbp_code_create_ex(b.ctypes.data, b.shape[0], b.shape[1], Z, 0, ctypes.byref(cfg), ctypes.byref(hh))
+        if rc == 0:
+            L.cbp_code_destroy(hh)
+        return rc
+    good = np.array([[0, 1, 0, -1], [2, -1, 0, 0]], np.int16)
+    assert create(good, 4) == 0
+    assert create(good, 0) == 1 and create(good, 1025) == 1  # Z range
+    assert create(np.array([[0, 5, 0, -1], [2, -1, 0, 0]]), 4) == 1       # shift >= Z
+    assert create(np.array([[0, -1, 0, -1], [2, -1, 0, 0]]), 4) == 1      # empty column
+    assert create(np.array([[-1, -1, -1, -1], [2, 1, 0, 0]]), 4) == 1     # empty row
+    assert create(good, 4, fpl=3) == 1                                    # frames_per_lane
+    assert create(np.zeros((2, 70), np.int16), 1000) == 2                 # N >= 65536: unsupported
+    assert create(np.zeros((1, 40), np.int16), 4) == 2                    # base row degree > 32
+    # encoding needs the dual-diagonal structure: this base decodes but cannot simulate
+    gg = cbp.Code(good, 4)
+    with pytest.raises(cbp.CbpError):
+        gg.ber_sim(2.0, 1, 0, 10, 5)
+    gg.decode(torch.zeros((2, 16), dtype=torch.float32, device=dev), 5)
