@@ -55,7 +55,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-suite", action="store_true", help="skip the other-config measurements")
     ap.add_argument("--e2e-frames", type=int, default=200_000)
-    ap.add_argument("--cpu-frames", type=int, default=400, help="oracle frames per Eb/N0 point (cpu_baseline)")
+    ap.add_argument("--cpu-frames", type=int, default=400,
+                    help="oracle frames per Eb/N0 point and core (cpu_baseline, reference arm)")
+    ap.add_argument("--cpu-cores", type=int, default=0, help="oracle processes (default: all host cores)")
     return ap.parse_args()
 
 
@@ -106,6 +108,37 @@ def measured_peaks():
 
 
 # ------------------------------------------------------------------ reference arm (CPU oracle)
+def _oracle_slice(job):
+    """worker: the unmodified single-threaded oracle on one frame range (one process per core)"""
+    name, eb, seed, begin, n, max_iter, llr_mode = job
+    import inputs
+    import oracle
+    base, Z = inputs.config_base(name)
+    return oracle.OracleCode(base, Z).ber_sim(eb, seed, begin, n, max_iter, llr_mode=llr_mode)
+
+
+def oracle_timed(name, ebn0s, seed, begin, frames, max_iter, llr_mode, cores):
+    """Time the oracle over `frames` frames per Eb/N0 point, split into `cores` independent
+    frame ranges run by `cores` processes (the oracle itself is untouched and single-threaded).
+    Returns (counts int64[8], seconds)."""
+    import multiprocessing as mpr
+    import numpy as np
+    jobs = []
+    for eb in ebn0s:
+        per = (frames + cores - 1) // cores
+        for k in range(cores):
+            b = begin + k * per
+            n = max(0, min(per, begin + frames - b))
+            if n:
+                jobs.append((name, eb, seed, b, n, max_iter, llr_mode))
+    ctx = mpr.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        pool.map(_oracle_slice, jobs[:cores])              # warm the workers (library load)
+        t0 = time.perf_counter()
+        res = pool.map(_oracle_slice, jobs, chunksize=1)
+        dt = time.perf_counter() - t0
+    return np.sum(res, axis=0), dt
+
 def run_reference(args, cfg, ebn0s):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -115,26 +148,27 @@ def run_reference(args, cfg, ebn0s):
     import oracle
     base, Z = inputs.config_base(cfg.name)
     o = oracle.OracleCode(base, Z)
-    frames = args.cpu_frames
+    cores = args.cpu_cores or os.cpu_count() or 1
+    frames = args.cpu_frames * cores
     for _ in range(args.warmup):
         o.ber_sim(ebn0s[0], args.seed, 0, 8, cfg.max_iter)
     times = []
     tot = np.zeros(8, np.int64)
     for s in range(args.steps):
-        t0 = time.perf_counter()
-        for eb in ebn0s:
-            tot += o.ber_sim(eb, args.seed, s * frames, frames, cfg.max_iter, llr_mode=args.llr_mode)
-        times.append(time.perf_counter() - t0)
+        c, dt = oracle_timed(cfg.name, ebn0s, args.seed, s * frames, frames, cfg.max_iter, args.llr_mode, cores)
+        tot += c
+        times.append(dt)
     T = sum(times)
     fps = tot[0] / T
     gbps = fps * o.K / 1e9
-    sample = f"{frames} frames x {len(ebn0s)} Eb/N0 points per step ({cfg.name}), single-threaded oracle"
+    sample = (f"{frames} frames x {len(ebn0s)} Eb/N0 points per step ({cfg.name}): the single-threaded oracle in "
+              f"{cores} processes on disjoint frame ranges")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": gbps, "unit": UNIT, "frames_per_s": fps,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": config_block(cfg, ebn0s, frames, args, n_gpus=1),
-        "cpu_baseline": {"value": gbps, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": gbps, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": gbps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -340,13 +374,19 @@ def main():
             import oracle
             o = oracle.OracleCode(base, Z)
             t0 = time.perf_counter()
-            c = np.zeros(8, np.int64)
+            c1 = np.zeros(8, np.int64)
             for p, eb in enumerate(ebn0s):
-                c += o.ber_sim(eb, args.seed, 0, args.cpu_frames, cfg.max_iter, llr_mode=args.llr_mode)
-            tc = time.perf_counter() - t0
-            cpu = {"value": c[0] * o.K / tc / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-                   "sample": f"{args.cpu_frames} frames x {len(ebn0s)} Eb/N0 points of the same workload, "
-                             f"single-threaded C++ oracle, {tc:.1f} s", "frames_per_s": c[0] / tc}
+                c1 += o.ber_sim(eb, args.seed, 0, args.cpu_frames, cfg.max_iter, llr_mode=args.llr_mode)
+            t1 = time.perf_counter() - t0
+            cores = args.cpu_cores or os.cpu_count() or 1
+            cN, tN = oracle_timed(cfg.name, ebn0s, args.seed, 0, args.cpu_frames * cores, cfg.max_iter,
+                                  args.llr_mode, cores)
+            cpu = {"value": cN[0] * o.K / tN / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+                   "sample": f"{args.cpu_frames * cores} frames x {len(ebn0s)} Eb/N0 points of the same workload: "
+                             f"the single-threaded C++ oracle in {cores} processes on disjoint frame ranges, "
+                             f"{tN:.1f} s", "frames_per_s": cN[0] / tN,
+                   "single_core": {"value": c1[0] * o.K / t1 / 1e9, "frames_per_s": c1[0] / t1,
+                                   "sample": f"{args.cpu_frames} frames x {len(ebn0s)} points, {t1:.1f} s"}}
         except Exception as ex:   # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {ex}"}
 
