@@ -296,7 +296,8 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         // instantiation (512 for P = 1, 256 for P = 2) and 15 named barriers allow
         const int maxt = (P == 2) ? 256 : (G.multi ? 512 : CBP_WARP_MAXT);
         if (G.team_threads > maxt && P == 2) return G;
-        const int64_t per_team = 4LL * (cbp::kCtlTeamWords + static_cast<int64_t>(G.F) * G.slot_words);
+        const int64_t ctl = G.multi ? cbp::kCtlTeamWords : 0;     // warp teams use no shared control words
+        const int64_t per_team = 4LL * (ctl + static_cast<int64_t>(G.F) * G.slot_words);
         const int64_t fixed = 4LL * G.table_words;
         int nt = static_cast<int>((smem_optin - fixed) / per_team);
         nt = std::min(nt, std::max(1, maxt / G.team_threads));
@@ -306,7 +307,7 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         G.teams = std::max(nt, 1);
         G.threads = G.teams * G.team_threads;
         G.smem_bytes = static_cast<int32_t>(G.state_in_smem ? fixed + G.teams * per_team
-                                                            : fixed + 4LL * cbp::kCtlTeamWords * G.teams);
+                                                            : fixed + 4LL * ctl * G.teams);
         return G;
     };
     for (int alg = 0; alg < 4; ++alg) {

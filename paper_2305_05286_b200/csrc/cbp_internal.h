@@ -64,7 +64,7 @@ struct KernelArgs {
 #define CBP_WARP_MAXT 512
 #endif
 
-constexpr int kCtlTeamWords = 136;  // shared control words per team: 2 x P(2) x 32 ballot words + broadcast
+constexpr int kCtlTeamWords = 136;  // shared control words per multi-warp team: 2 x P(2) x 32 ballots + broadcast
 
 struct Geometry {
     int32_t threads, F, Zp, slot_words, table_words, smem_bytes, state_in_smem, multi;

@@ -926,11 +926,13 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
     const int r = tm.r;
     const Lane lane{r, r * Ly::QS, r * Ly::RS, Z * Ly::QS, Z * Ly::RS, 4 * a.slot_words,
                     a.phi_m19, a.phi_one, static_cast<cudaTextureObject_t>(C.phi_tex)};
-    uint32_t* ctl = smem + a.table_words + tm.tidx * kCtlTeamWords;
+    // shared control words: only multi-warp teams exchange ballots / queue indices through them
+    constexpr int kCtl = MULTI ? kCtlTeamWords : 0;
+    uint32_t* ctl = smem + a.table_words + tm.tidx * kCtl;
     long long* ctl64 = reinterpret_cast<long long*>(ctl + 128);
 
     const int nteams = blockDim.x / a.team_threads;
-    float* sbase = SMEM ? reinterpret_cast<float*>(smem + a.table_words + nteams * kCtlTeamWords)
+    float* sbase = SMEM ? reinterpret_cast<float*>(smem + a.table_words + nteams * kCtl)
                         : a.gstate + static_cast<size_t>(blockIdx.x) * nteams * a.F * a.slot_words;
     float* grp0 = sbase + static_cast<size_t>(tm.tidx * a.F + (tm.slot < a.F ? tm.slot : 0)) * a.slot_words;
     // group layout (word offsets; slot_words % 4 == 0): QP [2PN] | pad to 4 | S [P SW M] | R [P E] | cw [P nwords]
