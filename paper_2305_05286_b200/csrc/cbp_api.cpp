@@ -290,7 +290,8 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         const int64_t raw = (2LL * P * c->N + 3) / 4 * 4 +
                             P * ((alg == 1 ? 4LL : 1LL) * c->M + c->E + nwords + (alg == 3 ? c->N : 0));
         G.slot_words = static_cast<int32_t>(G.F > 1 ? (raw + 31) / 32 * 32 + std::max(G.Zp, 4) : (raw + 3) / 4 * 4);
-        G.table_words = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4;
+        G.table_words = ((CBP_TEX_B2V && CBP_TEX_C2B) ? 0 : 4 * cbp::kPhiTableSegs) +
+                        (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4;
         G.team_threads = G.threads;
         // teams per CTA: as many independent teams as shared memory, the thread limit of the
         // instantiation (512 for P = 1, 256 for P = 2) and 15 named barriers allow

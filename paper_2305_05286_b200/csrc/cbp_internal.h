@@ -59,6 +59,14 @@ struct KernelArgs {
     float* gstate;         // per-CTA global state (state_in_smem == 0)
 };
 
+// phi lookups through the texture pipe (C2B default on, B2V default off)
+#ifndef CBP_TEX_C2B
+#define CBP_TEX_C2B 1
+#endif
+#ifndef CBP_TEX_B2V
+#define CBP_TEX_B2V 0
+#endif
+
 // thread limit (launch bound) of the one-frame-per-lane warp-team instantiation
 #ifndef CBP_WARP_MAXT
 #define CBP_WARP_MAXT 512

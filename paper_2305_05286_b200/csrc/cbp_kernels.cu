@@ -35,12 +35,6 @@ constexpr uint32_t kSign = 0x80000000u;
 // A/B switches CBP_TEX_C2B / CBP_TEX_B2V: evaluate the C2B / B2V phi with the table row
 // fetched through the texture pipe instead of LDS (default: C2B through TEX, DESIGN.md §5;
 // B2V through TEX as well, or one B2V lookup per chunk, measured 4-10% slower).
-#ifndef CBP_TEX_C2B
-#define CBP_TEX_C2B 1
-#endif
-#ifndef CBP_TEX_B2V
-#define CBP_TEX_B2V 0
-#endif
 
 
 // ---------------------------------------------------------------- byte-addressed vector access
@@ -899,10 +893,12 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
     // ---- stage the phi table and the schedule tables (a1).  The tables travel in the
     // kernel parameters; reading them in the hot loop straight from the constant bank
     // measured 20% slower on C2 than from shared memory (constant-cache misses).
+    // (with both phi lookups on the texture pipe the table is not staged at all)
+    constexpr int kTabWords = (CBP_TEX_B2V && CBP_TEX_C2B) ? 0 : 4 * kPhiSegs;
     float4* ptab = reinterpret_cast<float4*>(smem);
-    for (int k = threadIdx.x; k < kPhiSegs; k += blockDim.x) ptab[k] = C.phi_tab[k];
-    int4* ent = reinterpret_cast<int4*>(smem + 4 * kPhiSegs);
-    int32_t* row_ptr = reinterpret_cast<int32_t*>(smem + 4 * kPhiSegs + 8 * C.nent);
+    for (int k = threadIdx.x; k < kTabWords / 4; k += blockDim.x) ptab[k] = C.phi_tab[k];
+    int4* ent = reinterpret_cast<int4*>(smem + kTabWords);
+    int32_t* row_ptr = reinterpret_cast<int32_t*>(smem + kTabWords + 8 * C.nent);
     int16_t* pshift = reinterpret_cast<int16_t*>(row_ptr + mb + 1);
     for (int k = threadIdx.x; k < 2 * C.nent; k += blockDim.x) ent[k] = a.ent[k];
     for (int k = threadIdx.x; k <= mb; k += blockDim.x) row_ptr[k] = a.row_ptr[k];
@@ -1013,7 +1009,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                                 m = g.Sw(c, 0, p);                       // Omega = sgn * min (reading R20)
                             } else {
                                 Sv = g.Sw(c, 0, p);
-                                m = phi32(fabsf(Sv), ptab);              // Omega = sgn * phi(S)
+                                m = phi_sel<CBP_TEX_B2V && CBP_TEX_C2B>(fabsf(Sv), ptab, lane);   // Omega = sgn phi(S)
                             }
                             om[c] = (__float_as_uint(Sv) >> 31) ? -m : m;
                         }
