@@ -541,3 +541,18 @@ def test_abi_error_paths(codes):
     with pytest.raises(cbp.CbpError):
         gg.ber_sim(2.0, 1, 0, 10, 5)
     gg.decode(torch.zeros((2, 16), dtype=torch.float32, device=dev), 5)
+
+
+def test_ber_sim_all_frames_equal_oracle_counts(codes):
+    """BASELINE configs[1] exactly as bench.py runs it (C2, 1.0..3.0 dB, 10^6 frames per
+    point, seed 1, max_iter 30): the fused GPU counters over EVERY frame equal the CPU
+    oracle's (tests/golden/oracle_counts_C2.json, written by tools/write_oracle_counts.py
+    from oracle/ alone) -- bit errors, frame errors, iteration and edge-visit sums."""
+    import json
+    from pathlib import Path
+    gold = json.loads((Path(__file__).parent / "golden" / "oracle_counts_C2.json").read_text())
+    g, o = codes("C2")
+    F = gold["frames_per_point"]
+    for eb, want in gold["counts"].items():
+        got = g.ber_sim(float(eb), gold["seed"], 0, F, gold["max_iter"]).cpu().numpy()
+        assert list(got) == want, (eb, dict(zip(oracle.COUNT_NAMES, zip(got, want))))

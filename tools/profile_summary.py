@@ -25,13 +25,16 @@ def ncu(*args):
 
 raw = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv"))))
 R = dict(zip(raw[0], raw[2]))
+U = dict(zip(raw[0], raw[1]))
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}   # ncu's decimal byte units
 
 
 def f(k):
     try:
-        return float(R[k].replace(",", ""))
+        x = float(R[k].replace(",", ""))
     except (KeyError, ValueError):
         return None
+    return x * SCALE.get(U.get(k, ""), 1.0)
 
 
 M = {
