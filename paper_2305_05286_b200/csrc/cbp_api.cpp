@@ -89,6 +89,33 @@ const float4* phi_table(int device, std::string* err, cudaTextureObject_t* tex =
     return p;
 }
 
+// Per-device memory pool for the launch workspace (work-queue counter, global frame state):
+// stream-ordered allocations that stay cached across launches.  The default pool of the
+// device returns freed memory at every synchronisation (release threshold 0), which made
+// each launch re-map memory -- measured as intermittent 2-20x slower launches.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[128] = {};
+
+cudaMemPool_t work_pool(int device)
+{
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (device < 0 || device >= 128) return nullptr;
+    if (g_pool[device]) return g_pool[device];
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    uint64_t keep = UINT64_MAX;   // never trim: the workspace is reused launch after launch
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+    g_pool[device] = p;
+    return p;
+}
+
 }  // namespace
 
 struct cbp_code {
@@ -418,12 +445,16 @@ cbp_status run(const cbp_code* c, cbp::KernelArgs& a, int64_t frames, void* stre
         1, std::min<int64_t>(static_cast<int64_t>(c->num_sms) * c->ctas_per_sm[a.algorithm], ctas_needed)));
     cudaError_t e;
     unsigned long long* q = nullptr;
-    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&q), sizeof(unsigned long long), st)) != cudaSuccess)
+    cudaMemPool_t pool = work_pool(c->device);
+    auto alloc = [&](void** p, size_t bytes) {
+        return pool ? cudaMallocFromPoolAsync(p, bytes, pool, st) : cudaMallocAsync(p, bytes, st);
+    };
+    if ((e = alloc(reinterpret_cast<void**>(&q), sizeof(unsigned long long))) != cudaSuccess)
         return fail(CBP_E_NOMEM, std::string(who) + ": " + cudaGetErrorString(e));
     float* gs = nullptr;
     if (!G.state_in_smem) {
         const size_t bytes = sizeof(float) * static_cast<size_t>(grid) * G.F * G.teams * G.slot_words;
-        if ((e = cudaMallocAsync(reinterpret_cast<void**>(&gs), bytes, st)) != cudaSuccess) {
+        if ((e = alloc(reinterpret_cast<void**>(&gs), bytes)) != cudaSuccess) {
             cudaFreeAsync(q, st);
             return fail(CBP_E_NOMEM, std::string(who) + ": " + cudaGetErrorString(e));
         }

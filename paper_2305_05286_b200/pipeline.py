@@ -10,6 +10,9 @@ import torch
 from .cbp import CBP_STOP_BELIEF_M, Code
 
 
+_CACHE: dict = {}
+
+
 def alloc_host_outputs(code: Code, frames: int) -> dict:
     return {"bits": torch.empty((frames, code.words), dtype=torch.int32, pin_memory=True),
             "iters": torch.empty(frames, dtype=torch.int32, pin_memory=True),
@@ -17,7 +20,7 @@ def alloc_host_outputs(code: Code, frames: int) -> dict:
 
 
 def decode_host(code: Code, llr_host: torch.Tensor, max_iter: int, stop_rule: int = CBP_STOP_BELIEF_M,
-                out: dict | None = None, chunk: int = 1 << 15, streams=None, nstreams: int = 4) -> dict:
+                out: dict | None = None, chunk: int = 1 << 14, streams=None, nstreams: int = 4) -> dict:
     """Decode float32 LLRs [frames, ld] held in (pinned) host memory; returns pinned host outputs.
 
     The copies and launches are enqueued on `nstreams` streams (each with its own
@@ -27,9 +30,18 @@ def decode_host(code: Code, llr_host: torch.Tensor, max_iter: int, stop_rule: in
     if frames == 0:
         return out
     dev = code.device
-    streams = streams or [torch.cuda.Stream(device=dev) for _ in range(nstreams)]
     n = min(chunk, frames)
-    bufs = [(torch.empty((n, ld), dtype=torch.float32, device=dev), code.alloc_outputs(n)) for _ in streams]
+    key = (id(code), dev.index, nstreams, n, ld)
+    if streams is None:
+        # streams and device buffers persist across calls (no per-call stream creation / frees)
+        if key not in _CACHE:
+            ss = [torch.cuda.Stream(device=dev) for _ in range(nstreams)]
+            _CACHE.clear()
+            _CACHE[key] = (ss, [(torch.empty((n, ld), dtype=torch.float32, device=dev), code.alloc_outputs(n))
+                                for _ in ss])
+        streams, bufs = _CACHE[key]
+    else:
+        bufs = [(torch.empty((n, ld), dtype=torch.float32, device=dev), code.alloc_outputs(n)) for _ in streams]
     cur = torch.cuda.current_stream(dev)
     for s in streams:
         s.wait_stream(cur)

@@ -11,6 +11,7 @@ import inputs  # noqa: E402
 import paper_2305_05286_b200 as cbp  # noqa: E402
 from paper_2305_05286_b200 import pipeline  # noqa: E402
 
+EB = float(sys.argv[1]) if len(sys.argv) > 1 else 2.0
 base, Z = inputs.config_base("C2")
 code = cbp.Code(base, Z)
 F = 200_000
@@ -18,7 +19,7 @@ ld = (code.N + 3) // 4 * 4
 host = torch.empty((F, ld), dtype=torch.float32, pin_memory=True)
 for b in range(0, F, 1 << 17):
     n = min(1 << 17, F - b)
-    llr, _ = code.channel(2.0, 2, b, n, want_cw=False)
+    llr, _ = code.channel(EB, 2, b, n, want_cw=False)
     host[b:b + n].copy_(llr)
 dev = torch.empty_like(host, device="cuda")
 for _ in range(2):
@@ -36,10 +37,17 @@ torch.cuda.synchronize()
 t1 = time.perf_counter()
 out = code.decode(dev, 30)
 torch.cuda.synchronize()
-print(f"device-resident decode {F / (time.perf_counter() - t1):.3e} frames/s")
+print(f"device-resident decode {F / (time.perf_counter() - t1):.3e} frames/s at {EB} dB")
+cnt = torch.zeros(8, dtype=torch.int64, device="cuda")
+code.ber_sim(EB, 2, 0, F, 30, counts=cnt)
+torch.cuda.synchronize()
+t1 = time.perf_counter()
+code.ber_sim(EB, 2, 0, F, 30, counts=cnt)
+torch.cuda.synchronize()
+print(f"fused ber_sim {F / (time.perf_counter() - t1):.3e} frames/s")
 hout = pipeline.alloc_host_outputs(code, F)
-for chunk in (1 << 15, 1 << 16, 1 << 17, 1 << 18):
-    for ns in (2, 3, 4):
+for chunk in (1 << 14, 1 << 15, 1 << 16):
+    for ns in (4, 6):
         streams = [torch.cuda.Stream() for _ in range(ns)]
         pipeline.decode_host(code, host, 30, out=hout, chunk=chunk, streams=streams)
         t0 = time.perf_counter()
