@@ -556,3 +556,35 @@ def test_ber_sim_all_frames_equal_oracle_counts(codes):
     for eb, want in gold["counts"].items():
         got = g.ber_sim(float(eb), gold["seed"], 0, F, gold["max_iter"]).cpu().numpy()
         assert list(got) == want, (eb, dict(zip(oracle.COUNT_NAMES, zip(got, want))))
+
+
+def test_concurrent_streams_and_threads(codes):
+    """A cbp_code is shared by several host threads and streams (include/cbp.h): concurrent
+    decodes and ber_sims on four streams from four threads give the sequential results."""
+    import threading
+    g, o = codes("C2")
+    llr, _ = g.channel(2.0, 3, 0, 20_000, want_cw=False)
+    ref = g.decode(llr, 30, ev=True)
+    ref_c = g.ber_sim(2.5, 9, 0, 30_000, 30).cpu()
+    torch.cuda.synchronize()
+    outs, cnts, errs = [None] * 4, [None] * 4, []
+
+    def work(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                outs[k] = g.decode(llr, 30, ev=True, stream=s)
+                cnts[k] = g.ber_sim(2.5, 9, 0, 30_000, 30, stream=s)
+            s.synchronize()
+        except Exception as e:   # pragma: no cover
+            errs.append(e)
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for k in range(4):
+        for key in ("bits", "iters", "flags", "ev"):
+            assert torch.equal(outs[k][key], ref[key]), (k, key)
+        assert torch.equal(cnts[k].cpu(), ref_c)
