@@ -588,3 +588,19 @@ def test_concurrent_streams_and_threads(codes):
         for key in ("bits", "iters", "flags", "ev"):
             assert torch.equal(outs[k][key], ref[key]), (k, key)
         assert torch.equal(cnts[k].cpu(), ref_c)
+
+
+@pytest.mark.parametrize("alg,arith", [(1, oracle.MINSUM), (2, oracle.LBP), (3, oracle.FBP)],
+                         ids=["min-sum", "LBP", "FBP"])
+def test_decode_i8_other_algorithms(codes, alg, arith):
+    """cbp_decode_i8 (int8 LLR stream, L = q/4) with the min-sum CBP and the comparison
+    schedules equals the oracle on the dequantised LLRs."""
+    g, o = codes("C2")
+    l8, _ = o.channel(2.0, seed=51, frame_begin=0, frames=400, llr_mode=1)
+    q = np.zeros((400, 656), np.int8)
+    q[:, :o.N] = np.rint(l8 * 4).astype(np.int8)
+    rule = oracle.STOP_BELIEF_M if alg == 1 else oracle.STOP_SYNDROME
+    out = g.decode_i8(torch.from_numpy(q).cuda(), 0.25, 30, rule, ev=True, omega=True, algorithm=alg)
+    torch.cuda.synchronize()
+    go = {k: v.cpu().numpy() for k, v in out.items()}
+    assert_same(go, o.decode(l8, 30, rule, arith, want_omega=True), o.N, omega=False)
