@@ -18,6 +18,10 @@
  *    synchronisation (reported then by the CUDA runtime, not by this ABI).
  *  - A cbp_code is immutable after creation and may be used concurrently from
  *    several host threads and streams.
+ *  - Launch workspace (the frame work-queue counter; for codes whose per-frame
+ *    state does not fit in shared memory, the global frame state: ~0.7 MB per SM
+ *    for N = 26112) is allocated stream-ordered from a library-private memory
+ *    pool per device that keeps its memory for reuse (it is never trimmed).
  *  - Bits are packed LSB first: bit v of a frame is bit (v % 32) of word v / 32.
  *  - Results depend only on (code, inputs, options) -- never on grid size,
  *    stream or GPU count.  cbp_ber_sim / cbp_channel depend only on
