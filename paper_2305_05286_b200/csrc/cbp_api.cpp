@@ -324,7 +324,11 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         // instantiation (512 for P = 1, 256 for P = 2) and 15 named barriers allow
         const int maxt = (P == 2) ? 256 : (G.multi ? 512 : CBP_WARP_MAXT);
         if (G.team_threads > maxt && P == 2) return G;
-        const int64_t ctl = G.multi ? cbp::kCtlTeamWords : 0;     // warp teams use no shared control words
+        // shared control words: multi-warp teams exchange ballots and queue indices; warp teams with
+        // one group keep nb ballot words for the packed syndrome (kernel syndrome_nz)
+        G.fast_syn = (!G.multi && G.F == 1 && Z <= 32 && mb <= 32) ? 1 : 0;
+        G.ctl_words = G.multi ? cbp::kCtlTeamWords : (G.fast_syn ? (nb + 3) / 4 * 4 : 0);
+        const int64_t ctl = G.ctl_words;
         const int64_t per_team = 4LL * (ctl + static_cast<int64_t>(G.F) * G.slot_words);
         const int64_t fixed = 4LL * G.table_words;
         int nt = static_cast<int>((smem_optin - fixed) / per_team);
@@ -407,6 +411,7 @@ cbp::KernelArgs base_args(const cbp_code* c, int alg = 0)
     std::memcpy(a.row_ptr, c->row_ptr.data(), sizeof(int32_t) * c->row_ptr.size());
     std::memcpy(a.pshift, c->pshift.data(), sizeof(int16_t) * c->pshift.size());
     a.Zp = G.Zp; a.F = G.F; a.slot_words = G.slot_words; a.table_words = G.table_words;
+    a.ctl_words = G.ctl_words; a.fast_syn = G.fast_syn;
     a.team_threads = G.team_threads;
     a.phi_m19 = 0x7ffffu;
     a.phi_one = 0x3f800000u;

@@ -55,6 +55,8 @@ struct KernelArgs {
     unsigned long long* queue;    // frame work counter (zeroed)
     // geometry
     int32_t Zp, F, slot_words, table_words, team_threads;
+    int32_t ctl_words;     // shared control words per team (multi-warp teams; warp teams: syndrome scratch)
+    int32_t fast_syn;      // warp teams with one group, Z <= 32, mb <= 32: ballot-packed syndromes
     uint32_t phi_m19, phi_one;     // 0x7ffff, 0x3f800000 (phi local variable, runtime operands)
     float* gstate;         // per-CTA global state (state_in_smem == 0)
 };
@@ -79,6 +81,7 @@ struct Geometry {
     int32_t team_threads, teams;   // threads per team, teams per CTA
     int32_t alg;                   // cbp_algorithm of this geometry
     int32_t P;                     // frames per lane (1 or 2), interleaved in a group
+    int32_t ctl_words, fast_syn;   // see KernelArgs
 };
 
 // launch (cbp_kernels.cu); returns cudaError_t as int

@@ -923,7 +923,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
     const Lane lane{r, r * Ly::QS, r * Ly::RS, Z * Ly::QS, Z * Ly::RS, 4 * a.slot_words,
                     a.phi_m19, a.phi_one, static_cast<cudaTextureObject_t>(C.phi_tex)};
     // shared control words: only multi-warp teams exchange ballots / queue indices through them
-    constexpr int kCtl = MULTI ? kCtlTeamWords : 0;
+    const int kCtl = a.ctl_words;
     uint32_t* ctl = smem + a.table_words + tm.tidx * kCtl;
     long long* ctl64 = reinterpret_cast<long long*>(ctl + 128);
 
@@ -967,6 +967,36 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
     // per-lane counters (ber_sim)
     unsigned long long cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
+    // ---- syndrome of frame p's current hard bits, team-uniform call; valid where `want`.
+    // Warp teams with one group (Z <= 32, mb <= 32): the hard bits of each column block are
+    // packed by one ballot (bit t = variable jZ + t), lane i XORs the rotated words of base
+    // row i's entries (bit r of rot_s(w_j) = bit (r+s) mod Z = the variable of check iZ+r),
+    // and one vote says whether any check is unsatisfied -- nb ballots + ~dc words per lane
+    // instead of E per-lane bit reads.  Otherwise every lane checks its own checks.
+    auto syndrome_nz = [&](int p, bool want) -> bool {
+        if (!MULTI && a.fast_syn) {
+            for (int j = 0; j < C.nb; ++j) {
+                const bool bit = want && tm.lane_on && (__float_as_uint(g.PH(j * Z + (tm.lane_on ? r : 0), p)) >> 31);
+                const unsigned w = __ballot_sync(kFull, bit);
+                if (tm.tl == 0) ctl[j] = w;
+            }
+            __syncwarp();
+            const uint32_t zmask = (Z == 32) ? kFull : ((1u << Z) - 1u);
+            uint32_t x = 0;
+            if (want && tm.tl < mb)
+                for (int k = row_ptr[tm.tl]; k < row_ptr[tm.tl + 1]; ++k) {
+                    const int j = ent[2 * k].x / (8 * P * Z);          // A.x = QS j Z
+                    const int sft = ent[2 * k + 1].z >> 16;
+                    const uint32_t w = ctl[j];
+                    x ^= sft ? (((w >> sft) | (w << (Z - sft))) & zmask) : w;
+                }
+            const bool nz = __any_sync(kFull, x != 0u);
+            __syncwarp();
+            return nz;
+        }
+        return tm.slot_any(want && tm.lane_on && lane_syndrome<P, ALG>(ent, row_ptr, mb, r, Z, p, g));
+    };
+
     // ---- Step 3: outputs of the frames with done[p] (a8); team-uniform call
     auto finish = [&](const bool (&done)[P]) {
         bool anyd = false;
@@ -979,7 +1009,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
             bool synd_zero = conv[p];
             const bool need_syn = done[p] && !conv[p] && decoding;
             if (tm.team_any(need_syn)) {
-                const bool nz = tm.slot_any(need_syn && tm.lane_on && lane_syndrome<P, ALG>(ent, row_ptr, mb, r, Z, p, g));
+                const bool nz = syndrome_nz(p, need_syn);
                 if (need_syn) synd_zero = !nz;
             }
             const int iters = conv[p] ? sweep[p] : a.max_iter;
@@ -1241,8 +1271,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                     tm.sync();
 #pragma unroll
                     for (int p = 0; p < P; ++p) {
-                        const bool nz =
-                            tm.slot_any(fire[p] && tm.lane_on && lane_syndrome<P, ALG>(ent, row_ptr, mb, r, Z, p, g));
+                        const bool nz = syndrome_nz(p, fire[p]);
                         conv_now[p] = false;
                         if (fire[p]) {
                             if (!nz) {
@@ -1283,7 +1312,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                 const bool want_syn = active[p] && a.stop_rule == 2;
                 if (tm.team_any(want_syn)) {
                     tm.sync();
-                    const bool nz = tm.slot_any(want_syn && tm.lane_on && lane_syndrome<P, ALG>(ent, row_ptr, mb, r, Z, p, g));
+                    const bool nz = syndrome_nz(p, want_syn);
                     if (want_syn && !nz) conv[p] = true;
                 }
                 done[p] = active[p] && (conv[p] || sweep[p] >= a.max_iter);
