@@ -324,9 +324,9 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         // instantiation (512 for P = 1, 256 for P = 2) and 15 named barriers allow
         const int maxt = (P == 2) ? 256 : (G.multi ? 512 : CBP_WARP_MAXT);
         if (G.team_threads > maxt && P == 2) return G;
-        // shared control words: multi-warp teams exchange ballots and queue indices; warp teams with
-        // one group keep nb ballot words for the packed syndrome (kernel syndrome_nz)
-        G.fast_syn = (!G.multi && G.F == 1 && Z <= 32 && mb <= 32) ? 1 : 0;
+        // shared control words: multi-warp teams exchange ballots and queue indices; warp teams keep
+        // nb ballot words for the packed syndrome (kernel syndrome_nz)
+        G.fast_syn = (!G.multi && Z <= 32 && mb <= G.Zp) ? 1 : 0;
         G.ctl_words = G.multi ? cbp::kCtlTeamWords : (G.fast_syn ? (nb + 3) / 4 * 4 : 0);
         const int64_t ctl = G.ctl_words;
         const int64_t per_team = 4LL * (ctl + static_cast<int64_t>(G.F) * G.slot_words);

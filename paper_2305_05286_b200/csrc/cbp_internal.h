@@ -56,7 +56,7 @@ struct KernelArgs {
     // geometry
     int32_t Zp, F, slot_words, table_words, team_threads;
     int32_t ctl_words;     // shared control words per team (multi-warp teams; warp teams: syndrome scratch)
-    int32_t fast_syn;      // warp teams with one group, Z <= 32, mb <= 32: ballot-packed syndromes
+    int32_t fast_syn;      // warp teams with Z <= 32 and mb <= Zp: ballot-packed syndromes
     uint32_t phi_m19, phi_one;     // 0x7ffff, 0x3f800000 (phi local variable, runtime operands)
     float* gstate;         // per-CTA global state (state_in_smem == 0)
 };

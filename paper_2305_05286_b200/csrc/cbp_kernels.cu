@@ -968,11 +968,12 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
     unsigned long long cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
     // ---- syndrome of frame p's current hard bits, team-uniform call; valid where `want`.
-    // Warp teams with one group (Z <= 32, mb <= 32): the hard bits of each column block are
-    // packed by one ballot (bit t = variable jZ + t), lane i XORs the rotated words of base
-    // row i's entries (bit r of rot_s(w_j) = bit (r+s) mod Z = the variable of check iZ+r),
-    // and one vote says whether any check is unsatisfied -- nb ballots + ~dc words per lane
-    // instead of E per-lane bit reads.  Otherwise every lane checks its own checks.
+    // Warp teams (Z <= 32, mb <= Zp): the hard bits of each column block are packed by one
+    // ballot (group g's lanes in bits lane_base.., bit lane_base + t = variable jZ + t); lane i
+    // of a group XORs its field of the rotated words of base row i's entries (bit r of
+    // rot_s(field) = bit (r+s) mod Z = the variable of check iZ+r), and a vote over the group
+    // says whether any check is unsatisfied -- nb ballots + ~dc words per lane instead of E
+    // per-lane bit reads.  Multi-warp teams check their own checks lane by lane.
     auto syndrome_nz = [&](int p, bool want) -> bool {
         if (!MULTI && a.fast_syn) {
             for (int j = 0; j < C.nb; ++j) {
@@ -983,14 +984,14 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
             __syncwarp();
             const uint32_t zmask = (Z == 32) ? kFull : ((1u << Z) - 1u);
             uint32_t x = 0;
-            if (want && tm.tl < mb)
-                for (int k = row_ptr[tm.tl]; k < row_ptr[tm.tl + 1]; ++k) {
+            if (want && tm.slot < a.F && r < mb)
+                for (int k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
                     const int j = ent[2 * k].x / (8 * P * Z);          // A.x = QS j Z
                     const int sft = ent[2 * k + 1].z >> 16;
-                    const uint32_t w = ctl[j];
+                    const uint32_t w = (ctl[j] >> tm.lane_base) & zmask;
                     x ^= sft ? (((w >> sft) | (w << (Z - sft))) & zmask) : w;
                 }
-            const bool nz = __any_sync(kFull, x != 0u);
+            const bool nz = (__ballot_sync(kFull, x != 0u) & tm.slot_mask) != 0u;
             __syncwarp();
             return nz;
         }
