@@ -327,9 +327,7 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         // shared control words: multi-warp teams exchange ballots and queue indices; warp teams keep
         // nb ballot words for the packed syndrome (kernel syndrome_nz)
         G.fast_syn = (!G.multi && Z <= 32 && mb <= G.Zp) ? 1 : 0;
-        // (multi-warp teams add nb x TW words of packed hard bits for their syndromes)
-        G.ctl_words = G.multi ? cbp::kCtlTeamWords + (nb * (G.Zp / 32) + 3) / 4 * 4
-                              : (G.fast_syn ? (nb + 3) / 4 * 4 : 0);
+        G.ctl_words = G.multi ? cbp::kCtlTeamWords : (G.fast_syn ? (nb + 3) / 4 * 4 : 0);
         const int64_t ctl = G.ctl_words;
         const int64_t per_team = 4LL * (ctl + static_cast<int64_t>(G.F) * G.slot_words);
         const int64_t fixed = 4LL * G.table_words;

@@ -995,33 +995,6 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
             __syncwarp();
             return nz;
         }
-        if (MULTI) {
-            // multi-warp team: the same packed hard bits (warp w of the team ballots bits
-            // 32w.. of each column block into word j*TW + w), then every lane checks its own
-            // checks from those shared words instead of the frame state (global memory for C4)
-            const int TW = tm.nthreads >> 5, wq = tm.tl >> 5;
-            uint32_t* bw = ctl + kCtlTeamWords;
-            for (int j = 0; j < C.nb; ++j) {
-                const bool bit = want && tm.lane_on && (__float_as_uint(g.PH(j * Z + (tm.lane_on ? r : 0), p)) >> 31);
-                const unsigned w = __ballot_sync(kFull, bit);
-                if ((tm.tl & 31) == 0) bw[j * TW + wq] = w;
-            }
-            tm.sync();
-            uint32_t par = 0;
-            if (want && tm.lane_on)
-                for (int i = 0; i < mb; ++i) {
-                    uint32_t x = 0;
-                    for (int k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
-                        const int j = ent[2 * k].x / (8 * P * Z);
-                        int t = r + (ent[2 * k + 1].z >> 16);
-                        t = (t >= Z) ? t - Z : t;
-                        x ^= bw[j * TW + (t >> 5)] >> (t & 31);
-                    }
-                    par |= x;
-                }
-            const bool nz = tm.slot_any((par & 1u) != 0u);
-            return nz;
-        }
         return tm.slot_any(want && tm.lane_on && lane_syndrome<P, ALG>(ent, row_ptr, mb, r, Z, p, g));
     };
 
