@@ -604,3 +604,21 @@ def test_decode_i8_other_algorithms(codes, alg, arith):
     torch.cuda.synchronize()
     go = {k: v.cpu().numpy() for k, v in out.items()}
     assert_same(go, o.decode(l8, 30, rule, arith, want_omega=True), o.N, omega=False)
+
+
+def test_decode_deterministic_under_rescheduling(codes):
+    """Race-detection substitute (compute-sanitizer is unavailable on the pool): per-frame
+    results do not depend on how the persistent grid's work queue hands frames to teams --
+    the same frames decoded in one launch, in uneven slices, and repeatedly, give
+    identical bits, iterations, flags, edge visits and check-beliefs."""
+    g, o = codes("C2")
+    llr, _ = g.channel(1.5, 77, 0, 30_000, want_cw=False)
+    full = g.decode(llr, 30, omega=True, ev=True)
+    parts = [g.decode(llr[a:b].contiguous(), 30, omega=True, ev=True)
+             for a, b in ((0, 1), (1, 4097), (4097, 4100), (4100, 30_000))]
+    again = g.decode(llr, 30, omega=True, ev=True)
+    torch.cuda.synchronize()
+    for k in ("bits", "iters", "flags", "ev", "omega"):
+        cat = torch.cat([p[k] for p in parts])
+        assert torch.equal(full[k], cat), k
+        assert torch.equal(full[k], again[k]), k
