@@ -204,7 +204,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # under torchrun the NCCL process group is set up even for one rank, so the counter
+    # all-reduce and the max-over-ranks timing run through NCCL at every N
+    distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
+    if distributed:
         dist.init_process_group("nccl", device_id=dev)
     frames = args.frames or cfg.frames
     base, Z = inputs.config_base(cfg.name)
@@ -213,7 +216,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
-        if world > 1:
+        if distributed:
             dist.barrier()
 
     def step(counts_per_point, launch_ms=None):
@@ -252,7 +255,7 @@ def main():
         barrier()
     t_ms = sum(a.elapsed_time(b) for a, b in step_ms)
     t_max = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if distributed:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     T = t_max.item() / 1e3
     tot = torch.stack(counts).cpu().numpy()                   # counts of the last step, all ranks summed
@@ -319,7 +322,7 @@ def main():
                 pipeline.decode_host(code, host, cfg.max_iter, out=hout)
             te += time.perf_counter() - t0
         tmax = torch.tensor([te], dtype=torch.float64, device=dev)
-        if world > 1:
+        if distributed:
             dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         te = tmax.item()
         e2e = {"value": reps * len(ebn0s) * Fe * world * code.K / te / 1e9, "unit": UNIT,
@@ -358,7 +361,7 @@ def main():
             allreduce_counts(c)
             torch.cuda.synchronize()
             ms = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
-            if world > 1:
+            if distributed:
                 dist.all_reduce(ms, op=dist.ReduceOp.MAX)
             t = c.cpu().numpy()
             key = f"{name}@{eb}dB" + ("/int8" if lm else "") + ["", "/min-sum", "/LBP", "/FBP"][alg] + \
@@ -413,7 +416,7 @@ def main():
             "other_configs": others,
         }
         print(json.dumps(line))
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 
