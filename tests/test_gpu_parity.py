@@ -622,3 +622,23 @@ def test_decode_deterministic_under_rescheduling(codes):
         cat = torch.cat([p[k] for p in parts])
         assert torch.equal(full[k], cat), k
         assert torch.equal(full[k], again[k]), k
+
+
+@pytest.mark.parametrize("spec,seed,Z,frames,eb", [
+    ((3, 6, 1024, 3, 0, 3, 3), 2, 1024, 6, 2.5),        # Z = 1024: 32-warp teams (the 1024-thread instantiation)
+    ((4, 36, 4, 4, 0, 3, 3), 3, 4, 200, 4.0),            # rate 8/9: base rows of degree ~28 (near max_dc = 32)
+    ((60, 120, 4, 60, 0, 3, 3), 4, 4, 100, 3.0),         # 60 base rows, 120 columns
+])
+def test_decode_parity_size_limits(fpl, spec, seed, Z, frames, eb):
+    """Codes at the ABI's limits (include/cbp.h: Z <= 1024, base row degree <= 32, many
+    rows): decode and ber_sim parity with the oracle for every algorithm that applies."""
+    base = inputs.construct_base(spec, seed)
+    g, o = make_code(base, Z, fpl), oracle.OracleCode(base, Z)
+    assert g.launch_info()["frames_per_cta"] >= 1
+    llr, _ = o.channel(eb, seed=60 + seed, frame_begin=0, frames=frames)
+    assert_same(gpu_decode(g, llr, 12), o.decode(llr, 12, want_omega=True), o.N)
+    assert_same(gpu_decode(g, llr, 12, oracle.STOP_SYNDROME, algorithm=2),
+                o.decode(llr, 12, oracle.STOP_SYNDROME, oracle.LBP), o.N, omega=False)
+    want = o.ber_sim(eb, 61, 0, frames, 12)
+    got = g.ber_sim(eb, 61, 0, frames, 12).cpu().numpy()
+    assert list(got) == list(want)
