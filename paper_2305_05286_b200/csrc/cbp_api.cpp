@@ -214,8 +214,8 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
     // two int4 per entry b for a geometry with P frames per lane (layout documented in
     // cbp_kernels.cu; QS = 8P bytes per variable, RS = 4P bytes per edge, SU = 4 for the
     // 16-byte min-sum check records, else 1):
-    //   A = {QS jZ, S0 + SU RS row(p) Z, R0 + RS bZ, R0 + RS pZ},
-    //   B = {QS s, RS ds, first | kp << 8 | s << 16, first ? ~0 : 0}
+    //   E0 = {QS jZ, S0 + SU RS row(p) Z, R0 + RS pZ, QS s},
+    //   E1 = {RS ds, first ? ~0 : 0, first | kp << 8 | s << 16, R0 + RS bZ}
     // Byte offsets are relative to the group base: QP at 0, the check records at S0, R at R0.
     auto make_ent = [&](int P, int alg) {
         const int QS = 8 * P, RS = 4 * P, SU = (alg == 1) ? 4 : 1, SW = (alg == 1) ? 4 : 1;
@@ -231,8 +231,8 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
                 // kp: position of prev(b) among its row's entries = the variable's edge index inside
                 // the previous check (min-sum minimum owner, reading R20)
                 const int kp = p - row_ptr[ent_row[p]];
-                ent[2 * b] = make_int4(QS * j * Z, S0 + SU * RS * ent_row[p] * Z, R0 + RS * b * Z, R0 + RS * p * Z);
-                ent[2 * b + 1] = make_int4(QS * ent_s[b], RS * ds, first | (kp << 8) | (ent_s[b] << 16), first ? -1 : 0);
+                ent[2 * b] = make_int4(QS * j * Z, S0 + SU * RS * ent_row[p] * Z, R0 + RS * p * Z, QS * ent_s[b]);
+                ent[2 * b + 1] = make_int4(RS * ds, first ? -1 : 0, first | (kp << 8) | (ent_s[b] << 16), R0 + RS * b * Z);
             }
         }
         return ent;

@@ -133,11 +133,13 @@ struct Grp {
 
 // Schedule table entry b (two int4, built in cbp_api.cpp for the launch's P and algorithm),
 // byte offsets from the group base (QP at 0, check records at S0, R at R0):
-//   A = {QS jZ, S0 + SU RS row(prev(b)) Z, R0 + RS b Z, R0 + RS prev(b) Z}: variable block (QP),
-//        check block of the previous check of the same variables, own R block, R block of prev(b)
-//   B = {QS s, RS ds, first | kp << 8 | s << 16, first ? ~0 : 0}   ds = (s - s_prev) mod Z; first: no
-//        latest check in sweep 1 (R1), as a bit and as a kill mask; kp = position of prev(b) in its row
-//        (min-sum owner, R20)
+//   E0 = {QS jZ, S0 + SU RS row(prev(b)) Z, R0 + RS prev(b) Z, QS s}: variable block (QP), check
+//        block of the previous check of the same variables, R block of prev(b), rotation of the block
+//   E1 = {RS ds, first ? ~0 : 0, first | kp << 8 | s << 16, R0 + RS b Z}   ds = (s - s_prev) mod Z;
+//        first: no latest check in sweep 1 (R1), as a kill mask and a bit; kp = position of prev(b)
+//        in its row (min-sum owner, R20); own R block
+// The hot loop reads E0 and E1.xy (16 + 8 bytes, 3 shared-memory wavefronts per warp instead of
+// 4) and computes the own R block as R0 + b Z RS.
 // prev(b) = previous nonzero row of b's column, cyclically (the static "latest check" of
 // every variable of the block after sweep 1); prev(b) == b for a degree-1
 // column (R3).  Variable of lane r: j Z + (r + s) mod Z; its previous check's row (r + ds) mod Z.
@@ -212,6 +214,7 @@ struct Team {
 // ---------------------------------------------------------------- per-row edge chain
 struct Lane {
     int r, rq, rr, ZQ, ZR;            // lane, r QS, r RS, Z QS, Z RS
+    int R0;                           // byte offset of the R section in a group
     int slot_bytes;                   // group size (bounds checks of debug builds)
     uint32_t m19, one;                // phi local-variable masks as runtime operands (one LOP3)
     cudaTextureObject_t tex;          // phi table through the texture pipe
@@ -251,17 +254,18 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
     uint32_t fkill[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const int4 A = ent[2 * (e0 + k0 + u)];
-        const int4 B = ent[2 * (e0 + k0 + u) + 1];
-        const int tq = wrap(L.rq + B.x, L.ZQ);
-        const int tr = wrap(L.rr + B.y, L.ZR);
-        CBP_CHECK(tq >= 0 && tq < L.ZQ && tr >= 0 && tr < L.ZR);
-        CBP_CHECK(A.x + tq + Ly::QS <= L.slot_bytes && A.y + tr + Ly::RS <= L.slot_bytes &&
-                  A.z + L.rr + Ly::RS <= L.slot_bytes && A.w + tr + Ly::RS <= L.slot_bytes);
+        const int b = e0 + k0 + u;
+        const int4 A = ent[2 * b];
+        const int2 B = *reinterpret_cast<const int2*>(ent + 2 * b + 1);
+        const int tq = wrap(L.rq + A.w, L.ZQ);
+        const int tr = wrap(L.rr + B.x, L.ZR);
         aqp[u] = A.x + tq;
-        aw[u] = A.w + tr;
-        ar[u] = A.z + L.rr;
-        fkill[u] = static_cast<uint32_t>(B.w);
+        aw[u] = A.z + tr;
+        ar[u] = L.R0 + b * L.ZR + L.rr;
+        CBP_CHECK(tq >= 0 && tq < L.ZQ && tr >= 0 && tr < L.ZR);
+        CBP_CHECK(aqp[u] + Ly::QS <= L.slot_bytes && A.y + tr + Ly::RS <= L.slot_bytes &&
+                  ar[u] + Ly::RS <= L.slot_bytes && aw[u] + Ly::RS <= L.slot_bytes);
+        fkill[u] = static_cast<uint32_t>(B.y);
         float qp[2 * P];
         ldf<2 * P>(g.qp, aqp[u], qp);
 #pragma unroll
@@ -408,15 +412,16 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
     uint32_t cow[U][P], fkill[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const int4 A = ent[2 * (e0 + k0 + u)];
-        const int4 B = ent[2 * (e0 + k0 + u) + 1];
-        const int tq = wrap(L.rq + B.x, L.ZQ);
-        const int tr = wrap(L.rr + B.y, L.ZR);
+        const int b = e0 + k0 + u;
+        const int4 A = ent[2 * b];
+        const int4 B = ent[2 * b + 1];
+        const int tq = wrap(L.rq + A.w, L.ZQ);
+        const int tr = wrap(L.rr + B.x, L.ZR);
         CBP_CHECK(A.y + Ly::SU * tr + Ly::SS <= L.slot_bytes);
         aqp[u] = A.x + tq;
-        aw[u] = A.w + tr;
-        ar[u] = A.z + L.rr;
-        fkill[u] = static_cast<uint32_t>(B.w);
+        aw[u] = A.z + tr;
+        ar[u] = L.R0 + b * L.ZR + L.rr;
+        fkill[u] = static_cast<uint32_t>(B.y);
         kp[u] = (B.z >> 8) & 0xff;
         float qp[2 * P];
         ldf<2 * P>(g.qp, aqp[u], qp);
@@ -516,13 +521,14 @@ __device__ __forceinline__ void lbp_pass1(const int4* __restrict__ ent, const fl
     float q[U][P], ph[U][P];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const int4 A = ent[2 * (e0 + k0 + u)];
-        const int4 B = ent[2 * (e0 + k0 + u) + 1];
-        aqp[u] = A.x + wrap(L.rq + B.x, L.ZQ);
-        CBP_CHECK(aqp[u] >= 0 && aqp[u] + Ly::QS <= L.slot_bytes && A.z + L.rr + Ly::RS <= L.slot_bytes);
+        const int b = e0 + k0 + u;
+        const int4 A = ent[2 * b];
+        aqp[u] = A.x + wrap(L.rq + A.w, L.ZQ);
+        const int ar = L.R0 + b * L.ZR + L.rr;
+        CBP_CHECK(aqp[u] >= 0 && aqp[u] + Ly::QS <= L.slot_bytes && ar + Ly::RS <= L.slot_bytes);
         float qp[2 * P], ro[P];
         ldf<2 * P>(g.qp, aqp[u], qp);
-        ldf<P>(g.qp, A.z + L.rr, ro);
+        ldf<P>(g.qp, ar, ro);
         float lam[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) lam[p] = qp[p];
@@ -557,8 +563,7 @@ __device__ __forceinline__ void lbp_pass2(const int4* __restrict__ ent, const fl
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int4 A = ent[2 * (e0 + k0 + u)];
-        const int4 B = ent[2 * (e0 + k0 + u) + 1];
-        aqp[u] = A.x + wrap(L.rq + B.x, L.ZQ);
+        aqp[u] = A.x + wrap(L.rq + A.w, L.ZQ);
         float qp[2 * P];
         ldf<2 * P>(g.qp, aqp[u], qp);
 #pragma unroll
@@ -579,7 +584,7 @@ __device__ __forceinline__ void lbp_pass2(const int4* __restrict__ ent, const fl
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const int4 A = ent[2 * (e0 + k0 + u)];
+        const int ar = L.R0 + (e0 + k0 + u) * L.ZR + L.rr;
         float lam[P], st[2 * P];
         vadd<P>(q[u], Rn[u], lam);                               // equ_s2e12
 #pragma unroll
@@ -587,7 +592,7 @@ __device__ __forceinline__ void lbp_pass2(const int4* __restrict__ ent, const fl
             st[p] = lam[p];
             st[P + p] = lam[p];
         }
-        stf<P>(g.qp, A.z + L.rr, Rn[u]);
+        stf<P>(g.qp, ar, Rn[u]);
         stf<2 * P>(g.qp, aqp[u], st);
     }
 }
@@ -625,10 +630,10 @@ __device__ __forceinline__ void fbp_pass1(const int4* __restrict__ ent, const fl
     float q[U][P], ph[U][P];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const int4 A = ent[2 * (e0 + k0 + u)];
-        const int4 B = ent[2 * (e0 + k0 + u) + 1];
-        const int aqp = A.x + wrap(L.rq + B.x, L.ZQ);
-        ar[u] = A.z + L.rr;
+        const int b = e0 + k0 + u;
+        const int4 A = ent[2 * b];
+        const int aqp = A.x + wrap(L.rq + A.w, L.ZQ);
+        ar[u] = L.R0 + b * L.ZR + L.rr;
         CBP_CHECK(aqp >= 0 && aqp + 8 * P <= L.slot_bytes && ar[u] + 4 * P <= L.slot_bytes);
         float qp[2 * P], ro[P], lo[P];
         ldf<2 * P>(g.qp, aqp, qp);
@@ -663,10 +668,10 @@ __device__ __forceinline__ void fbp_pass2(const int4* __restrict__ ent, const fl
     float w[U][P], acc[U][P], Rn[U][P];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const int4 A = ent[2 * (e0 + k0 + u)];
-        const int4 B = ent[2 * (e0 + k0 + u) + 1];
-        aqp[u] = A.x + wrap(L.rq + B.x, L.ZQ);
-        ar[u] = A.z + L.rr;
+        const int b = e0 + k0 + u;
+        const int4 A = ent[2 * b];
+        aqp[u] = A.x + wrap(L.rq + A.w, L.ZQ);
+        ar[u] = L.R0 + b * L.ZR + L.rr;
         ldf<P>(g.qp, ar[u], w[u]);
         float qp[2 * P];
         ldf<2 * P>(g.qp, aqp[u], qp);
@@ -920,7 +925,8 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
     }
     tm.lane_on = tm.r < Z && tm.slot < a.F;
     const int r = tm.r;
-    const Lane lane{r, r * Ly::QS, r * Ly::RS, Z * Ly::QS, Z * Ly::RS, 4 * a.slot_words,
+    const Lane lane{r, r * Ly::QS, r * Ly::RS, Z * Ly::QS, Z * Ly::RS,
+                    4 * (((2 * P * C.N + 3) & ~3) + P * Ly::SW * C.M), 4 * a.slot_words,
                     a.phi_m19, a.phi_one, static_cast<cudaTextureObject_t>(C.phi_tex)};
     // shared control words: only multi-warp teams exchange ballots / queue indices through them
     const int kCtl = a.ctl_words;
