@@ -72,7 +72,7 @@ cbp_status cbp_construct_base(const cbp_construct_spec* spec, uint64_t seed, int
  *   every base row and column must be non-empty.
  * Encoding (cbp_channel, cbp_ber_sim) additionally needs the dual-diagonal
  * parity structure of SURVEY Appendix B; otherwise those return
- * CBP_E_UNSUPPORTED while decoding still works. */
+ * CBP_E_UNSUPPORTED (unless CBP_TX_ZERO is set) while decoding still works. */
 typedef struct cbp_code cbp_code;
 cbp_status cbp_code_create(const int16_t* base, int32_t mb, int32_t nb, int32_t Z, int32_t device, cbp_code** out);
 void       cbp_code_destroy(cbp_code* code);
@@ -146,10 +146,21 @@ cbp_status cbp_decode_i8(const cbp_code* code, const int8_t* d_q, int64_t ld, fl
 
 /* ---------------------------------------------------------------- channel */
 
+/* llr_mode flags of cbp_channel / cbp_ber_sim (OR-ed; 0..3 valid). */
+enum {
+    CBP_LLR_INT8 = 1,   /* int8 stream: q = sat(rint(4L), +-127), L = q/4 (BASELINE config 5) */
+    CBP_TX_ZERO = 2     /* transmit the all-zero codeword instead of encoded random info bits
+                           (reading R23).  Needs no encoder, so it works for every
+                           code (e.g. the PEG codes of PAPER.md l.608); the noise is the same
+                           Philox stream, so L equals the encoded run's L wherever c_v = 0. */
+};
+
 /* BPSK/AWGN channel of DESIGN.md §4 on device for global frames
  * [frame_begin, frame_begin + frames): uniform info bits (Philox4x32-10 keyed by
  * seed), systematic encoding, y = (1-2c) + sigma n, L = 2y/sigma^2 with
- * sigma^2 = 1/(2 (K/N) 10^(ebn0_db/10)); llr_mode 0 fp32, 1 int8 stream (L = q/4).
+ * sigma^2 = 1/(2 (K/N) 10^(ebn0_db/10)); llr_mode: OR of the flags above (0 = fp32,
+ * encoded random info bits).  Without CBP_TX_ZERO the code needs the dual-diagonal
+ * encoder structure, else CBP_E_UNSUPPORTED.
  *   d_llr : device float[frames][ld] (ld >= N) or NULL
  *   d_cw  : device uint32[frames][ld_words] transmitted codewords or NULL */
 cbp_status cbp_channel(const cbp_code* code, double ebn0_db, uint64_t seed, int64_t frame_begin, int64_t frames,
@@ -170,7 +181,9 @@ typedef struct {
 } cbp_counts;
 
 /* Fused channel + CBP decode + error counting for one Eb/N0 point (no LLR
- * traffic through HBM).  Equivalent to cbp_channel -> cbp_decode -> compare. */
+ * traffic through HBM).  Equivalent to cbp_channel -> cbp_decode -> compare
+ * (llr_mode as for cbp_channel; bit errors count over variables 0..K-1, the
+ * systematic part for encoded codes). */
 cbp_status cbp_ber_sim(const cbp_code* code, double ebn0_db, uint64_t seed, int64_t frame_begin, int64_t frames,
                        const cbp_opts* opts, int32_t llr_mode, cbp_counts* d_counts, void* stream);
 

@@ -2,7 +2,8 @@
 
 Holds none of the method's arithmetic (DESIGN.md §5 "input recipe"):
   * the QC base-matrix constructor (C, inputs/qc_construct.c) for the
-    BASELINE.json configs, and
+    BASELINE.json configs,
+  * the QC-PEG constructor (inputs/peg.py) for the paper's own code families, and
   * numpy LLR generators for decode-only tests (all-zero codeword over BPSK/AWGN,
     which is a codeword of every linear code, or raw random LLR vectors).
 """
@@ -14,6 +15,8 @@ from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
+
+from .peg import PEG_CONFIGS, PegConfig, peg_base, qc_peg  # noqa: F401  (the paper's own code families)
 
 _HERE = Path(__file__).resolve().parent
 _LIB = None
@@ -79,8 +82,21 @@ def construct_base(spec, seed: int) -> np.ndarray:
 
 
 def config_base(name: str) -> tuple[np.ndarray, int]:
+    """(base, Z) of a BASELINE config (CONFIGS) or of one of the paper's PEG families (PEG_CONFIGS)."""
+    if name in PEG_CONFIGS:
+        return peg_base(name)
     cfg = CONFIGS[name]
     return construct_base(cfg.spec, cfg.code_seed), cfg.spec[2]
+
+
+def get_config(name: str):
+    """CodeConfig or PegConfig by name (both carry name, code_seed, ebn0_db, frames, max_iter)."""
+    return PEG_CONFIGS[name] if name in PEG_CONFIGS else CONFIGS[name]
+
+
+def is_peg(name: str) -> bool:
+    """PEG codes have no encoder structure: channels send the all-zero codeword (TX_ZERO)."""
+    return name in PEG_CONFIGS
 
 
 def base_sha256(base: np.ndarray, Z: int) -> str:

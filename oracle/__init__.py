@@ -16,6 +16,7 @@ _LIB = None
 
 STOP_BELIEF_M, STOP_BELIEF_N, STOP_SYNDROME, STOP_NONE = 0, 1, 2, 3
 FP32_CONTRACT, FP64, FP64_LITERAL, MINSUM, LBP, FBP = 0, 1, 2, 3, 4, 5
+LLR_INT8, TX_ZERO = 1, 2   # llr_mode flags (TX_ZERO: the all-zero codeword is sent, reading R23)
 ALPHA_DEFAULT = 0.75   # normalized min-sum parameter (reading R20; the paper leaves alpha open)
 PHI_LO = float.fromhex("0x1.a56e0cp-43")
 PHI_HI = 30.0

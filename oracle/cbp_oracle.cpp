@@ -223,8 +223,10 @@ void oracle_normals(uint64_t seed, uint64_t frame, int32_t n, float* out)
 int oracle_channel(const or_code* c, double ebn0_db, uint64_t seed, int64_t frame_begin, int64_t frames,
                    int32_t llr_mode, float* llr, int64_t ld, uint32_t* cw_out, int64_t ld_words)
 {
-    if (!c->can_encode || frames < 0 || (llr && ld < c->N) || (cw_out && ld_words < (c->N + 31) / 32)) return 1;
-    if (llr_mode != 0 && llr_mode != 1) return 1;
+    if (frames < 0 || (llr && ld < c->N) || (cw_out && ld_words < (c->N + 31) / 32)) return 1;
+    if (llr_mode < 0 || llr_mode > 3) return 1;                      // bit0 int8, bit1 all-zero codeword
+    const bool tx_zero = (llr_mode & 2) != 0;                        // reading R23
+    if (!tx_zero && !c->can_encode) return 1;
     // sigma^2 = 1 / (2 R 10^(Eb/N0 / 10)), R = K/N, L = 2 y / sigma^2 (reading R17)
     const double R = (double)c->K / (double)c->N;
     const double sigma2 = 1.0 / (2.0 * R * std::pow(10.0, ebn0_db / 10.0));
@@ -235,6 +237,9 @@ int oracle_channel(const or_code* c, double ebn0_db, uint64_t seed, int64_t fram
     std::vector<uint32_t> info(kw), cw(nw);
     for (int64_t f = 0; f < frames; ++f) {
         const uint64_t g = (uint64_t)(frame_begin + f);
+        if (tx_zero) {
+            std::fill(cw.begin(), cw.end(), 0u);                     // the all-zero codeword, no info bits drawn
+        } else {
         for (int32_t w = 0; w < kw; ++w) {
             const uint32_t ctr[4] = {(uint32_t)(w / 4), (uint32_t)g, (uint32_t)(g >> 32), 0u};
             uint32_t x[4];
@@ -243,6 +248,7 @@ int oracle_channel(const or_code* c, double ebn0_db, uint64_t seed, int64_t fram
         }
         if (c->K % 32) info[kw - 1] &= (1u << (c->K % 32)) - 1u;
         oracle_encode(c, info.data(), cw.data());
+        }
         if (cw_out) std::copy(cw.begin(), cw.end(), cw_out + f * ld_words);
         if (!llr) continue;
         for (int32_t v = 0; v < c->N; ++v) {
@@ -250,7 +256,7 @@ int oracle_channel(const or_code* c, double ebn0_db, uint64_t seed, int64_t fram
             const float n = normal_of(seed, g, v);
             const float y = sym + sigf * n;
             float L = scalef * y;
-            if (llr_mode == 1) {                                         // int8 stream (BJ config 5)
+            if (llr_mode & 1) {                                          // int8 stream (BJ config 5)
                 float q = std::rint(L * 4.0f);
                 q = std::fmin(std::fmax(q, -127.0f), 127.0f);
                 L = q * 0.25f;
@@ -668,7 +674,7 @@ int oracle_decode(const or_code* c, const float* llr, int64_t ld, int64_t frames
 int oracle_ber_sim(const or_code* c, double ebn0_db, uint64_t seed, int64_t frame_begin, int64_t frames,
                    const or_opts* o, int32_t llr_mode, int64_t* counts)
 {
-    if (!c || !c->can_encode || !opts_ok(o) || frames < 0 || !counts) return 1;
+    if (!c || !opts_ok(o) || frames < 0 || !counts) return 1;
     const int32_t N = c->N, K = c->K, nw = (N + 31) / 32;
     std::vector<float> L(N);
     std::vector<uint32_t> cw(nw), dec(nw);

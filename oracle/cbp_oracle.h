@@ -76,7 +76,8 @@ void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t
 void oracle_normals(uint64_t seed, uint64_t frame, int32_t n, float* out);
 
 /* BPSK/AWGN channel of DESIGN.md §4 for global frames [frame_begin, frame_begin+frames):
- * llr[f*ld + v] (llr_mode 0 fp32, 1 int8-quantised q = sat(rint(4L), +-127), L' = q/4),
+ * llr[f*ld + v] (llr_mode bit0: int8-quantised q = sat(rint(4L), +-127), L' = q/4;
+ * bit1: the all-zero codeword is sent, no info bits or encoder -- reading R23),
  * cw[f*ld_words + w] the transmitted codeword (either may be NULL). */
 int oracle_channel(const or_code* c, double ebn0_db, uint64_t seed, int64_t frame_begin, int64_t frames,
                    int32_t llr_mode, float* llr, int64_t ld, uint32_t* cw, int64_t ld_words);

@@ -39,6 +39,8 @@ class _Opts(ctypes.Structure):
 
 
 CBP_ALG_LOG_TANH, CBP_ALG_MIN_SUM, CBP_ALG_LBP, CBP_ALG_FBP = 0, 1, 2, 3
+# llr_mode flags of channel / ber_sim (include/cbp.h): int8 stream, all-zero codeword (reading R23)
+CBP_LLR_INT8, CBP_TX_ZERO = 1, 2
 ALPHA_DEFAULT = 0.75
 
 

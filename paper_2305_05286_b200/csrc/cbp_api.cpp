@@ -543,9 +543,10 @@ cbp_status cbp_channel(const cbp_code* c, double ebn0_db, uint64_t seed, int64_t
                        int32_t llr_mode, float* d_llr, int64_t ld, uint32_t* d_cw, int64_t ld_words, void* stream)
 {
     if (!c) return fail(CBP_E_INVALID, "cbp_channel: null code");
-    if (!c->can_encode) return fail(CBP_E_UNSUPPORTED, "cbp_channel: base has no dual-diagonal encoder structure");
     if (frames < 0 || frame_begin < 0) return fail(CBP_E_INVALID, "cbp_channel: negative frame range");
-    if (llr_mode != 0 && llr_mode != 1) return fail(CBP_E_INVALID, "cbp_channel: llr_mode must be 0 or 1");
+    if (llr_mode < 0 || llr_mode > 3) return fail(CBP_E_INVALID, "cbp_channel: llr_mode must be 0..3");
+    if (!(llr_mode & CBP_TX_ZERO) && !c->can_encode)
+        return fail(CBP_E_UNSUPPORTED, "cbp_channel: base has no dual-diagonal encoder structure (use CBP_TX_ZERO)");
     if (!std::isfinite(ebn0_db)) return fail(CBP_E_INVALID, "cbp_channel: ebn0_db not finite");
     if (frames == 0) return CBP_OK;
     if (!d_llr && !d_cw) return fail(CBP_E_INVALID, "cbp_channel: both outputs NULL");
@@ -569,11 +570,12 @@ cbp_status cbp_ber_sim(const cbp_code* c, double ebn0_db, uint64_t seed, int64_t
                        const cbp_opts* opts, int32_t llr_mode, cbp_counts* d_counts, void* stream)
 {
     if (!c) return fail(CBP_E_INVALID, "cbp_ber_sim: null code");
-    if (!c->can_encode) return fail(CBP_E_UNSUPPORTED, "cbp_ber_sim: base has no dual-diagonal encoder structure");
     cbp_status s = check_opts(c, opts);
     if (s != CBP_OK) return s;
     if (frames < 0 || frame_begin < 0) return fail(CBP_E_INVALID, "cbp_ber_sim: negative frame range");
-    if (llr_mode != 0 && llr_mode != 1) return fail(CBP_E_INVALID, "cbp_ber_sim: llr_mode must be 0 or 1");
+    if (llr_mode < 0 || llr_mode > 3) return fail(CBP_E_INVALID, "cbp_ber_sim: llr_mode must be 0..3");
+    if (!(llr_mode & CBP_TX_ZERO) && !c->can_encode)
+        return fail(CBP_E_UNSUPPORTED, "cbp_ber_sim: base has no dual-diagonal encoder structure (use CBP_TX_ZERO)");
     if (!std::isfinite(ebn0_db)) return fail(CBP_E_INVALID, "cbp_ber_sim: ebn0_db not finite");
     if (!d_counts) return fail(CBP_E_INVALID, "cbp_ber_sim: null counts");
     if (frames == 0) return CBP_OK;

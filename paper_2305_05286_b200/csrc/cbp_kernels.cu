@@ -775,6 +775,16 @@ __device__ void channel_frames(const KernelArgs& a, const Team<MULTI>& tm, const
     const DevCode& C = a.code;
     const int Z = C.Z, r = tm.r;
     const uint32_t k0 = static_cast<uint32_t>(a.seed), k1 = static_cast<uint32_t>(a.seed >> 32);
+    if (a.llr_mode & 2) {
+        // all-zero codeword (CBP_TX_ZERO, reading R23): symbols +1, no info bits, no encoder
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            if (!(fresh[p] && tm.lane_on)) continue;
+            for (int v = r; v < C.N; v += Z) g.Q(v, p) = 1.0f;
+            for (int w = r; w < C.nwords; w += Z) g.cwp(p)[w] = 0u;
+        }
+        tm.sync();
+    } else {
     // (a2) info words: word w = Philox(w/4, f_lo, f_hi, 0)[w%4]
 #pragma unroll
     for (int p = 0; p < P; ++p) {
@@ -850,6 +860,7 @@ __device__ void channel_frames(const KernelArgs& a, const Team<MULTI>& tm, const
         }
     }
     tm.sync();
+    }
     // (a4) BPSK + AWGN + LLR: y = (1-2c) + sigma n, L = (2/sigma^2) y  (equ_s4e15, R17)
 #pragma unroll
     for (int p = 0; p < P; ++p) {
@@ -868,7 +879,7 @@ __device__ void channel_frames(const KernelArgs& a, const Team<MULTI>& tm, const
                 if (v >= C.N) break;
                 const float y = __fadd_rn(g.Q(v, p), __fmul_rn(a.sigma, n[m]));
                 float Lv = __fmul_rn(a.scale, y);
-                if (a.llr_mode == 1) {
+                if (a.llr_mode & 1) {
                     float qq = rintf(__fmul_rn(Lv, 4.0f));
                     qq = fminf(fmaxf(qq, -127.0f), 127.0f);
                     Lv = __fmul_rn(qq, 0.25f);

@@ -137,7 +137,9 @@ def main(argv=None):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = inputs.CONFIGS[a.config]
+    cfg = inputs.get_config(a.config)
+    if inputs.is_peg(a.config):
+        a.llr_mode |= 2                                    # PEG codes: all-zero codeword (CBP_TX_ZERO)
     base, Z = inputs.config_base(a.config)
     code = Code(base, Z, device=local)
     ebs = [float(x) for x in a.ebn0.split(",")] if a.ebn0 else list(cfg.ebn0_db)

@@ -513,7 +513,8 @@ def test_abi_error_paths(codes):
         assert dec(opts=cbp.cbp._Opts(*bad)) == 1, bad
     assert b"opts" in L.cbp_last_error() or b"stop" in L.cbp_last_error()
     cnt = torch.zeros(8, dtype=torch.int64, device=dev)
-    assert L.cbp_ber_sim(h, 2.0, 1, 0, 10, ctypes.byref(ok), 2, cnt.data_ptr(), None) == 1   # llr_mode
+    assert L.cbp_ber_sim(h, 2.0, 1, 0, 10, ctypes.byref(ok), 4, cnt.data_ptr(), None) == 1   # llr_mode
+    assert L.cbp_ber_sim(h, 2.0, 1, 0, 10, ctypes.byref(ok), -1, cnt.data_ptr(), None) == 1
     assert L.cbp_ber_sim(h, float("nan"), 1, 0, 10, ctypes.byref(ok), 0, cnt.data_ptr(), None) == 1
     assert L.cbp_ber_sim(h, 2.0, 1, -1, 10, ctypes.byref(ok), 0, cnt.data_ptr(), None) == 1
     assert L.cbp_ber_sim(h, 2.0, 1, 0, 10, ctypes.byref(ok), 0, None, None) == 1
