@@ -343,9 +343,11 @@ def main():
         suite = [("C1", 2.0, 1_000_000, 0, 0, 0), ("C3a", 2.5, 300_000, 0, 0, 0), ("C5", 2.5, 300_000, 0, 1, 0),
                  ("C3b", 4.0, 300_000, 0, 0, 0), ("C4", 1.5, 3_000, 2, 0, 0), ("C2", 2.0, 1_000_000, 1, 0, 0),
                  ("C2", 2.0, 1_000_000, 2, 0, 0), ("C2", 2.0, 1_000_000, 0, 0, 1),
-                 ("C2", 2.0, 1_000_000, 2, 0, 2), ("C2", 2.0, 1_000_000, 2, 0, 3)]
+                 ("C2", 2.0, 1_000_000, 2, 0, 2), ("C2", 2.0, 1_000_000, 2, 0, 3),
+                 # the paper's own code families (QC-PEG; all-zero codeword, max 200 iterations)
+                 ("P2048", 2.0, 300_000, 0, 2, 0), ("P8192", 1.5, 30_000, 0, 2, 0)]
         for name, eb, nf, rule, lm, alg in suite:
-            ocfg = inputs.CONFIGS[name]
+            ocfg = inputs.get_config(name)
             ob, oz = inputs.config_base(name)
             oc = cbp.Code(ob, oz, device=local)
             c = torch.zeros(8, dtype=torch.int64, device=dev)
@@ -364,7 +366,7 @@ def main():
             if distributed:
                 dist.all_reduce(ms, op=dist.ReduceOp.MAX)
             t = c.cpu().numpy()
-            key = f"{name}@{eb}dB" + ("/int8" if lm else "") + ["", "/min-sum", "/LBP", "/FBP"][alg] + \
+            key = f"{name}@{eb}dB" + ("/int8" if lm & 1 else "") + ("/zero-cw" if lm & 2 else "") + ["", "/min-sum", "/LBP", "/FBP"][alg] + \
                 ("" if rule == 0 or name == "C4" else ["", "/W=N", "/syndrome", "/none"][rule])
             others[key] = {
                 "N": oc.N, "K": oc.K, "frames": int(t[0]), "ms": ms.item(),

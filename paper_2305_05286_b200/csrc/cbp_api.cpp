@@ -334,9 +334,20 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         int nt = static_cast<int>((smem_optin - fixed) / per_team);
         nt = std::min(nt, std::max(1, maxt / G.team_threads));
         if (G.multi) nt = std::min(nt, 15);
+        // Large frames with small teams: when shared memory holds a single team of < 8 warps
+        // and no second CTA fits beside it, the SM runs nearly idle (P8192: one 64-thread team
+        // per SM).  The global-state path runs maxt / team_threads teams per CTA with the
+        // state served from L2/L1 instead: 2.0-2.3x faster on P8192.
+        if (G.multi && P == 1 && nt >= 1 && nt * G.team_threads < 256 && 2 * (fixed + nt * per_team) > smem_optin)
+            nt = 0;
         G.state_in_smem = nt >= 1 ? 1 : 0;
         if (P == 2 && !G.state_in_smem) return G;
-        G.teams = std::max(nt, 1);
+        G.teams = G.state_in_smem ? nt : std::max(1, maxt / G.team_threads);
+        if (const char* gt = std::getenv("CBP_GLOBAL_TEAMS"); gt && P == 1 && G.multi) {
+            // A/B measurements only: force the global-state path with k teams per CTA
+            const int k = std::atoi(gt);
+            if (k >= 1 && k <= 15 && k * G.team_threads <= 1024) { G.state_in_smem = 0; G.teams = k; }
+        }
         G.threads = G.teams * G.team_threads;
         G.smem_bytes = static_cast<int32_t>(G.state_in_smem ? fixed + G.teams * per_team
                                                             : fixed + 4LL * ctl * G.teams);

@@ -28,17 +28,18 @@ ap.add_argument("--alpha", type=float, default=0.75)
 ap.add_argument("--fpl", type=int, default=0, help="frames per lane: 0 auto, 1, 2")
 a = ap.parse_args()
 ALG = dict(algorithm=a.alg, alpha=a.alpha)
-cfg = inputs.CONFIGS[a.config]
+cfg = inputs.get_config(a.config)
+LM = cbp.CBP_TX_ZERO if inputs.is_peg(a.config) else 0   # PEG codes: all-zero codeword (R23)
 base, Z = inputs.config_base(a.config)
 g = cbp.Code(base, Z, frames_per_lane=a.fpl)
 print(g.launch_info())
 if a.mode == "decode":
-    llr, _ = g.channel(a.ebn0, 1, 0, a.frames, want_cw=False)
-g.ber_sim(a.ebn0, 1, 0, 4096, cfg.max_iter)
+    llr, _ = g.channel(a.ebn0, 1, 0, a.frames, llr_mode=LM, want_cw=False)
+g.ber_sim(a.ebn0, 1, 0, 4096, cfg.max_iter, llr_mode=LM)
 torch.cuda.synchronize()
 t_end = time.perf_counter() + a.warm
 while time.perf_counter() < t_end:
-    g.ber_sim(a.ebn0, 1, 0, a.frames, cfg.max_iter, stop_rule=a.rule, **ALG)
+    g.ber_sim(a.ebn0, 1, 0, a.frames, cfg.max_iter, stop_rule=a.rule, llr_mode=LM, **ALG)
     torch.cuda.synchronize()
 best = None
 cnt = torch.zeros(8, dtype=torch.int64, device="cuda")
@@ -47,7 +48,7 @@ for _ in range(a.reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     if a.mode == "ber":
-        c = g.ber_sim(a.ebn0, 1, 0, a.frames, cfg.max_iter, stop_rule=a.rule, counts=cnt, **ALG)
+        c = g.ber_sim(a.ebn0, 1, 0, a.frames, cfg.max_iter, stop_rule=a.rule, llr_mode=LM, counts=cnt, **ALG)
     else:
         out = g.decode(llr, cfg.max_iter, a.rule, ev=True, **ALG)
     e1.record()
