@@ -343,6 +343,9 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         G.state_in_smem = nt >= 1 ? 1 : 0;
         if (P == 2 && !G.state_in_smem) return G;
         G.teams = G.state_in_smem ? nt : std::max(1, maxt / G.team_threads);
+        // a single large team (C4: 384 threads) leaves the global-state path latency-bound; two
+        // teams run in the 1024-thread instantiation (64 registers): C4 455 vs 580 ms per 2e4 frames
+        if (!G.state_in_smem && G.multi && P == 1 && G.teams == 1 && 2 * G.team_threads <= 1024) G.teams = 2;
         if (const char* gt = std::getenv("CBP_GLOBAL_TEAMS"); gt && P == 1 && G.multi) {
             // A/B measurements only: force the global-state path with k teams per CTA
             const int k = std::atoi(gt);
