@@ -217,9 +217,9 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
     //   E0 = {QS jZ, S0 + SU RS row(p) Z, R0 + RS pZ, QS s},
     //   E1 = {RS ds, first ? ~0 : 0, first | kp << 8 | s << 16, R0 + RS bZ}
     // Byte offsets are relative to the group base: QP at 0, the check records at S0, R at R0.
-    auto make_ent = [&](int P, int alg) {
+    auto make_ent = [&](int P, int alg, bool r_global) {
         const int QS = 8 * P, RS = 4 * P, SU = (alg == 1) ? 4 : 1, SW = (alg == 1) ? 4 : 1;
-        const int S0 = 4 * ((2 * P * nb * Z + 3) & ~3), R0 = S0 + 4 * P * SW * mb * Z;
+        const int S0 = 4 * ((2 * P * nb * Z + 3) & ~3), R0 = r_global ? 0 : S0 + 4 * P * SW * mb * Z;
         std::vector<int4> ent(2 * static_cast<size_t>(nent));
         for (int j = 0; j < nb; ++j) {
             const auto& L = col_ent[j];
@@ -296,8 +296,11 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
     c->num_sms = nsm > 0 ? nsm : 1;
     c->min_dc = *std::min_element(roww.begin(), roww.end());
     const int nwords = (c->N + 31) / 32;
+    // split layout (R in global memory): automatic (below), or forced on / off with CBP_SPLIT_R=1 / 0 (A/B runs)
+    const char* sr = std::getenv("CBP_SPLIT_R");
+    const int split_env = (sr && (sr[0] == '0' || sr[0] == '1') && sr[1] == 0) ? sr[0] - '0' : -1;
     // geometry with P frames per lane; G.teams == 0 if it does not apply
-    auto make_geo = [&](int alg, int P) {
+    auto make_geo = [&](int alg, int P, bool split_r) {
         cbp::Geometry G{};
         G.alg = alg;
         G.P = P;
@@ -314,8 +317,11 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         // (P words, or 4P for min-sum's 16-byte records), R (P words per edge), P codewords;
         // groups 16-byte aligned, F > 1 groups staggered by max(Zp, 4) words across banks
         // (flooding BP adds its channel LLRs, P words per variable, after the codewords)
+        // split layout (r_global): R [P E] moves to a global slot of its own, the rest stays in shared memory
+        G.r_global = (split_r && P == 1) ? 1 : 0;
+        G.r_words = G.r_global ? static_cast<int32_t>((P * c->E + 3) / 4 * 4) : 0;
         const int64_t raw = (2LL * P * c->N + 3) / 4 * 4 +
-                            P * ((alg == 1 ? 4LL : 1LL) * c->M + c->E + nwords + (alg == 3 ? c->N : 0));
+                            P * ((alg == 1 ? 4LL : 1LL) * c->M + (G.r_global ? 0 : c->E) + nwords + (alg == 3 ? c->N : 0));
         G.slot_words = static_cast<int32_t>(G.F > 1 ? (raw + 31) / 32 * 32 + std::max(G.Zp, 4) : (raw + 3) / 4 * 4);
         G.table_words = ((CBP_TEX_B2V && CBP_TEX_C2B) ? 0 : 4 * cbp::kPhiTableSegs) +
                         (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4;
@@ -341,15 +347,28 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         if (G.multi && P == 1 && nt >= 1 && nt * G.team_threads < 256 && 2 * (fixed + nt * per_team) > smem_optin)
             nt = 0;
         G.state_in_smem = nt >= 1 ? 1 : 0;
+        if (!G.state_in_smem && G.r_global) {            // no split without shared memory: all-global path
+            G.r_global = 0;
+            G.r_words = 0;
+            G.slot_words += static_cast<int32_t>((P * c->E + 3) / 4 * 4);
+        }
         if (P == 2 && !G.state_in_smem) return G;
         G.teams = G.state_in_smem ? nt : std::max(1, maxt / G.team_threads);
         // a single large team (C4: 384 threads) leaves the global-state path latency-bound; two
         // teams run in the 1024-thread instantiation (64 registers): C4 455 vs 580 ms per 2e4 frames
         if (!G.state_in_smem && G.multi && P == 1 && G.teams == 1 && 2 * G.team_threads <= 1024) G.teams = 2;
-        if (const char* gt = std::getenv("CBP_GLOBAL_TEAMS"); gt && P == 1 && G.multi) {
+        if (const char* gt = std::getenv("CBP_GLOBAL_TEAMS"); gt && P == 1) {
             // A/B measurements only: force the global-state path with k teams per CTA
             const int k = std::atoi(gt);
-            if (k >= 1 && k <= 15 && k * G.team_threads <= 1024) { G.state_in_smem = 0; G.teams = k; }
+            if (k >= 1 && (G.multi ? k <= 15 && k * G.team_threads <= 1024 : k * G.team_threads <= maxt)) {
+                G.state_in_smem = 0;
+                G.teams = k;
+                if (G.r_global) {
+                    G.r_global = 0;
+                    G.r_words = 0;
+                    G.slot_words += static_cast<int32_t>((P * c->E + 3) / 4 * 4);
+                }
+            }
         }
         G.threads = G.teams * G.team_threads;
         G.smem_bytes = static_cast<int32_t>(G.state_in_smem ? fixed + G.teams * per_team
@@ -357,7 +376,16 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         return G;
     };
     for (int alg = 0; alg < 4; ++alg) {
-        const cbp::Geometry g1 = make_geo(alg, 1), g2 = alg <= 1 ? make_geo(alg, 2) : cbp::Geometry{};
+        cbp::Geometry g1 = make_geo(alg, 1, split_env == 1);
+        const cbp::Geometry g2 = alg <= 1 ? make_geo(alg, 2, false) : cbp::Geometry{};
+        // Warp teams whose frames are too large for more than a few per SM (P2048: 45 KB, 4 warps per
+        // SM) are latency-bound; moving R to global memory (L1/L2-served) fits 2x+ the frames in
+        // shared memory: P2048 28.5 vs 34.8 ms per 1e5 frames.  Codes that already hold >= 8 warps
+        // per SM lose by it (C2 +8 %, C1 +4 %, C3a/C3b +5 %), so they keep R in shared memory.
+        if (split_env < 0 && !g1.multi && g1.state_in_smem && g1.teams * g1.team_threads < 256) {
+            const cbp::Geometry gs = make_geo(alg, 1, true);
+            if (gs.state_in_smem && gs.r_global && gs.teams >= 2 * g1.teams) g1 = gs;
+        }
         // automatic: one frame per lane.  Two interleaved frames per lane halve the warps
         // per SM at the same shared memory and measured slower on every config (C2
         // ber_sim 12.0 vs 7.65 ms); they remain a selectable geometry.
@@ -377,7 +405,7 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
             return fail(CBP_E_UNSUPPORTED, "cbp_code_create: kernel does not fit on this device");
         }
         c->ctas_per_sm[alg] = G.state_in_smem ? occ : 1;
-        c->ent[alg] = make_ent(G.P, alg);
+        c->ent[alg] = make_ent(G.P, alg, G.r_global != 0);
     }
     *out = c;
     return CBP_OK;
@@ -426,6 +454,7 @@ cbp::KernelArgs base_args(const cbp_code* c, int alg = 0)
     std::memcpy(a.pshift, c->pshift.data(), sizeof(int16_t) * c->pshift.size());
     a.Zp = G.Zp; a.F = G.F; a.slot_words = G.slot_words; a.table_words = G.table_words;
     a.ctl_words = G.ctl_words; a.fast_syn = G.fast_syn;
+    a.r_words = G.r_words;
     a.team_threads = G.team_threads;
     a.phi_m19 = 0x7ffffu;
     a.phi_one = 0x3f800000u;
@@ -471,15 +500,18 @@ cbp_status run(const cbp_code* c, cbp::KernelArgs& a, int64_t frames, void* stre
     if ((e = alloc(reinterpret_cast<void**>(&q), sizeof(unsigned long long))) != cudaSuccess)
         return fail(CBP_E_NOMEM, std::string(who) + ": " + cudaGetErrorString(e));
     float* gs = nullptr;
-    if (!G.state_in_smem) {
-        const size_t bytes = sizeof(float) * static_cast<size_t>(grid) * G.F * G.teams * G.slot_words;
+    if (!G.state_in_smem || G.r_global) {
+        // all-global layout: whole groups; split layout: the R sections only
+        const size_t words = G.state_in_smem && G.r_global ? G.r_words : G.slot_words;
+        const size_t bytes = sizeof(float) * static_cast<size_t>(grid) * G.F * G.teams * words;
         if ((e = alloc(reinterpret_cast<void**>(&gs), bytes)) != cudaSuccess) {
             cudaFreeAsync(q, st);
             return fail(CBP_E_NOMEM, std::string(who) + ": " + cudaGetErrorString(e));
         }
     }
     a.queue = q;
-    a.gstate = gs;
+    a.gstate = G.state_in_smem ? nullptr : gs;
+    a.rstate = G.state_in_smem ? gs : nullptr;
     e = cudaMemsetAsync(q, 0, sizeof(unsigned long long), st);
     int le = (e == cudaSuccess) ? cbp::launch_cbp(a, G, grid, stream) : static_cast<int>(e);
     cudaFreeAsync(q, st);

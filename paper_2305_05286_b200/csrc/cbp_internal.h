@@ -59,6 +59,8 @@ struct KernelArgs {
     int32_t fast_syn;      // warp teams with Z <= 32 and mb <= Zp: ballot-packed syndromes
     uint32_t phi_m19, phi_one;     // 0x7ffff, 0x3f800000 (phi local variable, runtime operands)
     float* gstate;         // per-CTA global state (state_in_smem == 0)
+    float* rstate;         // per-group R sections of the split layout (r_global), r_words each
+    int32_t r_words;
 };
 
 // phi lookups through the texture pipe (C2B default on, B2V default off)
@@ -82,6 +84,7 @@ struct Geometry {
     int32_t alg;                   // cbp_algorithm of this geometry
     int32_t P;                     // frames per lane (1 or 2), interleaved in a group
     int32_t ctl_words, fast_syn;   // see KernelArgs
+    int32_t r_global, r_words;     // split layout: R in the global workspace, r_words per group
 };
 
 // launch (cbp_kernels.cu); returns cudaError_t as int

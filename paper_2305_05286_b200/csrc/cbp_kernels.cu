@@ -113,6 +113,7 @@ struct Grp {
     char* qp;
     char* S;
     char* R;
+    char* rb;             // base of the hot loop's R offsets: qp (R inside the group) or R (split layout)
     uint32_t* cw;
     int nwords;
     using Ly = Lay<P, ALG>;
@@ -216,6 +217,7 @@ struct Lane {
     int r, rq, rr, ZQ, ZR;            // lane, r QS, r RS, Z QS, Z RS
     int R0;                           // byte offset of the R section in a group
     int slot_bytes;                   // group size (bounds checks of debug builds)
+    int r_bytes;                      // end of the R section relative to the R base (debug builds)
     uint32_t m19, one;                // phi local-variable masks as runtime operands (one LOP3)
     cudaTextureObject_t tex;          // phi table through the texture pipe
 };
@@ -264,7 +266,7 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
         ar[u] = L.R0 + b * L.ZR + L.rr;
         CBP_CHECK(tq >= 0 && tq < L.ZQ && tr >= 0 && tr < L.ZR);
         CBP_CHECK(aqp[u] + Ly::QS <= L.slot_bytes && A.y + tr + Ly::RS <= L.slot_bytes &&
-                  ar[u] + Ly::RS <= L.slot_bytes && aw[u] + Ly::RS <= L.slot_bytes);
+                  ar[u] + Ly::RS <= L.r_bytes && aw[u] + Ly::RS <= L.r_bytes);
         fkill[u] = static_cast<uint32_t>(B.y);
         float qp[2 * P];
         ldf<2 * P>(g.qp, aqp[u], qp);
@@ -289,13 +291,13 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
         }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) stf<P>(g.qp, aw[u], Rn[u]);   // equ_s4e22 commit of R_{cj->v} (R2), before the read (R3)
+    for (int u = 0; u < U; ++u) stf<P>(g.rb, aw[u], Rn[u]);   // equ_s4e22 commit of R_{cj->v} (R2), before the read (R3)
     float qn[U][P];
     uint32_t lb[U][P];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         float ro[P], lam[P];
-        ldf<P>(g.qp, ar[u], ro);                             // R_{ci->v}
+        ldf<P>(g.rb, ar[u], ro);                             // R_{ci->v}
         vadd<P>(q[u], Rn[u], lam);                           // equ_s4e20 (Lambda is never -0)
         vsub<P>(lam, ro, qn[u]);                             // equ_s4e19 (R15)
 #pragma unroll
@@ -443,11 +445,11 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
                                        ~(fkill[u] & s1m[p]));
         }
 #pragma unroll
-    for (int u = 0; u < U; ++u) stf<P>(g.qp, aw[u], Rn[u]);   // commit of R_{cj->v} (R2, R3)
+    for (int u = 0; u < U; ++u) stf<P>(g.rb, aw[u], Rn[u]);   // commit of R_{cj->v} (R2, R3)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         float ro[P], lam[P], qn[P], st[2 * P];
-        ldf<P>(g.qp, ar[u], ro);
+        ldf<P>(g.rb, ar[u], ro);
         vadd<P>(q[u], Rn[u], lam);                           // equ_s4e20
         vsub<P>(lam, ro, qn);                                // equ_s4e19
 #pragma unroll
@@ -525,10 +527,10 @@ __device__ __forceinline__ void lbp_pass1(const int4* __restrict__ ent, const fl
         const int4 A = ent[2 * b];
         aqp[u] = A.x + wrap(L.rq + A.w, L.ZQ);
         const int ar = L.R0 + b * L.ZR + L.rr;
-        CBP_CHECK(aqp[u] >= 0 && aqp[u] + Ly::QS <= L.slot_bytes && ar + Ly::RS <= L.slot_bytes);
+        CBP_CHECK(aqp[u] >= 0 && aqp[u] + Ly::QS <= L.slot_bytes && ar + Ly::RS <= L.r_bytes);
         float qp[2 * P], ro[P];
         ldf<2 * P>(g.qp, aqp[u], qp);
-        ldf<P>(g.qp, ar, ro);
+        ldf<P>(g.rb, ar, ro);
         float lam[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) lam[p] = qp[p];
@@ -592,7 +594,7 @@ __device__ __forceinline__ void lbp_pass2(const int4* __restrict__ ent, const fl
             st[p] = lam[p];
             st[P + p] = lam[p];
         }
-        stf<P>(g.qp, ar, Rn[u]);
+        stf<P>(g.rb, ar, Rn[u]);
         stf<2 * P>(g.qp, aqp[u], st);
     }
 }
@@ -634,10 +636,10 @@ __device__ __forceinline__ void fbp_pass1(const int4* __restrict__ ent, const fl
         const int4 A = ent[2 * b];
         const int aqp = A.x + wrap(L.rq + A.w, L.ZQ);
         ar[u] = L.R0 + b * L.ZR + L.rr;
-        CBP_CHECK(aqp >= 0 && aqp + 8 * P <= L.slot_bytes && ar[u] + 4 * P <= L.slot_bytes);
+        CBP_CHECK(aqp >= 0 && aqp + 8 * P <= L.slot_bytes && ar[u] + 4 * P <= L.r_bytes);
         float qp[2 * P], ro[P], lo[P];
         ldf<2 * P>(g.qp, aqp, qp);
-        ldf<P>(g.qp, ar[u], ro);
+        ldf<P>(g.rb, ar[u], ro);
 #pragma unroll
         for (int p = 0; p < P; ++p) lo[p] = qp[P + p];
         vsub<P>(lo, ro, q[u]);                                   // equ_s2e3 (Lambda_old - R)
@@ -655,7 +657,7 @@ __device__ __forceinline__ void fbp_pass1(const int4* __restrict__ ent, const fl
             negw[p] ^= __float_as_uint(q[u][p]);
             st[p] = __uint_as_float(__float_as_uint(ph[u][p]) | (__float_as_uint(q[u][p]) & kSign));
         }
-        stf<P>(g.qp, ar[u], st);
+        stf<P>(g.rb, ar[u], st);
     }
 }
 
@@ -672,7 +674,7 @@ __device__ __forceinline__ void fbp_pass2(const int4* __restrict__ ent, const fl
         const int4 A = ent[2 * b];
         aqp[u] = A.x + wrap(L.rq + A.w, L.ZQ);
         ar[u] = L.R0 + b * L.ZR + L.rr;
-        ldf<P>(g.qp, ar[u], w[u]);
+        ldf<P>(g.rb, ar[u], w[u]);
         float qp[2 * P];
         ldf<2 * P>(g.qp, aqp[u], qp);
 #pragma unroll
@@ -694,7 +696,7 @@ __device__ __forceinline__ void fbp_pass2(const int4* __restrict__ ent, const fl
     for (int u = 0; u < U; ++u) {
         float na[P];
         vadd<P>(acc[u], Rn[u], na);                              // equ_s2e6, ascending checks
-        stf<P>(g.qp, ar[u], Rn[u]);
+        stf<P>(g.rb, ar[u], Rn[u]);
 #pragma unroll
         for (int p = 0; p < P; ++p) reinterpret_cast<float*>(g.qp + aqp[u])[p] = na[p];
     }
@@ -898,7 +900,9 @@ __device__ void channel_frames(const KernelArgs& a, const Team<MULTI>& tm, const
 }
 
 // ---------------------------------------------------------------- the kernel
-template <bool MULTI, bool SMEM, int MAXT, int ALG, int P>
+// SMEM: 0 the group state in the global workspace, 1 in shared memory, 2 in shared memory
+// except R, which lives in the global workspace (split layout)
+template <bool MULTI, int SMEM, int MAXT, int ALG, int P>
 __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ KernelArgs a)
 {
     using Ly = Lay<P, ALG>;
@@ -936,8 +940,9 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
     }
     tm.lane_on = tm.r < Z && tm.slot < a.F;
     const int r = tm.r;
+    const int r_off = ((2 * P * C.N + 3) & ~3) + P * Ly::SW * C.M;   // word offset of R inside a group
     const Lane lane{r, r * Ly::QS, r * Ly::RS, Z * Ly::QS, Z * Ly::RS,
-                    4 * (((2 * P * C.N + 3) & ~3) + P * Ly::SW * C.M), 4 * a.slot_words,
+                    SMEM == 2 ? 0 : 4 * r_off, 4 * a.slot_words, SMEM == 2 ? 4 * a.r_words : 4 * a.slot_words,
                     a.phi_m19, a.phi_one, static_cast<cudaTextureObject_t>(C.phi_tex)};
     // shared control words: only multi-warp teams exchange ballots / queue indices through them
     const int kCtl = a.ctl_words;
@@ -945,16 +950,25 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
     long long* ctl64 = reinterpret_cast<long long*>(ctl + 128);
 
     const int nteams = blockDim.x / a.team_threads;
+    const int gidx = tm.tidx * a.F + (tm.slot < a.F ? tm.slot : 0);   // group index in the CTA
     float* sbase = SMEM ? reinterpret_cast<float*>(smem + a.table_words + nteams * kCtl)
                         : a.gstate + static_cast<size_t>(blockIdx.x) * nteams * a.F * a.slot_words;
-    float* grp0 = sbase + static_cast<size_t>(tm.tidx * a.F + (tm.slot < a.F ? tm.slot : 0)) * a.slot_words;
-    // group layout (word offsets; slot_words % 4 == 0): QP [2PN] | pad to 4 | S [P SW M] | R [P E] | cw [P nwords]
+    float* grp0 = sbase + static_cast<size_t>(gidx) * a.slot_words;
+    // group layout (word offsets; slot_words % 4 == 0): QP [2PN] | pad to 4 | S [P SW M] | R [P E] | cw [P nwords];
+    // split layout (SMEM 2): R [P E] in its own global slot of r_words, the rest in shared memory
     Grp<P, ALG> g;
     const int s_off = (2 * P * C.N + 3) & ~3;              // 16-byte aligned check records
     g.qp = reinterpret_cast<char*>(grp0);
     g.S = reinterpret_cast<char*>(grp0 + s_off);
-    g.R = reinterpret_cast<char*>(grp0 + s_off + P * Ly::SW * C.M);
-    g.cw = reinterpret_cast<uint32_t*>(grp0 + s_off + P * Ly::SW * C.M + P * C.E);
+    if constexpr (SMEM == 2) {
+        g.R = reinterpret_cast<char*>(a.rstate + (static_cast<size_t>(blockIdx.x) * nteams * a.F + gidx) * a.r_words);
+        g.rb = g.R;
+        g.cw = reinterpret_cast<uint32_t*>(grp0 + r_off);
+    } else {
+        g.R = reinterpret_cast<char*>(grp0 + r_off);
+        g.rb = g.qp;
+        g.cw = reinterpret_cast<uint32_t*>(grp0 + r_off + P * C.E);
+    }
     g.nwords = C.nwords;
     __syncthreads();
     auto put_check = [&](int p, int c, float4 v) {
@@ -1406,7 +1420,7 @@ int launch_phi_table(float4* out, void* stream)
 // Instantiations: P = 1 for every geometry (state in smem or global, warp or multi-warp
 // teams up to 1024 threads); P = 2 only with state in smem and at most 256 threads.
 // the kernel of algorithm g.alg (P = 2 exists for the CBP rules 0 and 1 only)
-template <bool MULTI, bool SMEM, int MAXT, int P>
+template <bool MULTI, int SMEM, int MAXT, int P>
 static auto kernel_of(const Geometry& g)
 {
     if constexpr (P == 1) {
@@ -1421,7 +1435,7 @@ static auto kernel_of(const Geometry& g)
     }
 }
 
-template <bool MULTI, bool SMEM, int MAXT, int P>
+template <bool MULTI, int SMEM, int MAXT, int P>
 static int launch_t(const KernelArgs& a, const Geometry& g, int grid, cudaStream_t st)
 {
     auto k = kernel_of<MULTI, SMEM, MAXT, P>(g);
@@ -1431,7 +1445,7 @@ static int launch_t(const KernelArgs& a, const Geometry& g, int grid, cudaStream
     return static_cast<int>(cudaGetLastError());
 }
 
-template <bool MULTI, bool SMEM, int MAXT, int P>
+template <bool MULTI, int SMEM, int MAXT, int P>
 static int occ_t(const Geometry& g, int* out)
 {
     auto k = kernel_of<MULTI, SMEM, MAXT, P>(g);
@@ -1440,22 +1454,27 @@ static int occ_t(const Geometry& g, int* out)
     return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, g.threads, g.smem_bytes));
 }
 
-template <template <bool, bool, int, int> class Fn, typename... Args>
+template <template <bool, int, int, int> class Fn, typename... Args>
 static int dispatch(const Geometry& g, Args... args)
 {
     if (g.P == 2) {
         if (!g.state_in_smem || g.threads > 256 || g.alg > 1) return static_cast<int>(cudaErrorInvalidConfiguration);
-        return g.multi ? Fn<true, true, 256, 2>::run(g, args...) : Fn<false, true, 256, 2>::run(g, args...);
+        if (g.r_global) return static_cast<int>(cudaErrorInvalidConfiguration);
+        return g.multi ? Fn<true, 1, 256, 2>::run(g, args...) : Fn<false, 1, 256, 2>::run(g, args...);
     }
+    const int sm = g.state_in_smem ? (g.r_global ? 2 : 1) : 0;
     if (!g.multi)
-        return g.state_in_smem ? Fn<false, true, CBP_WARP_MAXT, 1>::run(g, args...)
-                               : Fn<false, false, CBP_WARP_MAXT, 1>::run(g, args...);
+        return sm == 2 ? Fn<false, 2, CBP_WARP_MAXT, 1>::run(g, args...)
+             : sm == 1 ? Fn<false, 1, CBP_WARP_MAXT, 1>::run(g, args...)
+                       : Fn<false, 0, CBP_WARP_MAXT, 1>::run(g, args...);
     if (g.threads <= 512)
-        return g.state_in_smem ? Fn<true, true, 512, 1>::run(g, args...) : Fn<true, false, 512, 1>::run(g, args...);
-    return g.state_in_smem ? Fn<true, true, 1024, 1>::run(g, args...) : Fn<true, false, 1024, 1>::run(g, args...);
+        return sm == 2 ? Fn<true, 2, 512, 1>::run(g, args...)
+             : sm == 1 ? Fn<true, 1, 512, 1>::run(g, args...) : Fn<true, 0, 512, 1>::run(g, args...);
+    return sm == 2 ? Fn<true, 2, 1024, 1>::run(g, args...)
+         : sm == 1 ? Fn<true, 1, 1024, 1>::run(g, args...) : Fn<true, 0, 1024, 1>::run(g, args...);
 }
 
-template <bool MULTI, bool SMEM, int MAXT, int P>
+template <bool MULTI, int SMEM, int MAXT, int P>
 struct LaunchFn {
     static int run(const Geometry& g, const KernelArgs* a, int grid, cudaStream_t st)
     {
@@ -1463,7 +1482,7 @@ struct LaunchFn {
     }
 };
 
-template <bool MULTI, bool SMEM, int MAXT, int P>
+template <bool MULTI, int SMEM, int MAXT, int P>
 struct OccFn {
     static int run(const Geometry& g, int* out) { return occ_t<MULTI, SMEM, MAXT, P>(g, out); }
 };

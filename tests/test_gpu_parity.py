@@ -643,3 +643,32 @@ def test_decode_parity_size_limits(fpl, spec, seed, Z, frames, eb):
     want = o.ber_sim(eb, 61, 0, frames, 12)
     got = g.ber_sim(eb, 61, 0, frames, 12).cpu().numpy()
     assert list(got) == list(want)
+
+
+@pytest.mark.parametrize("env", [{"CBP_SPLIT_R": "1"}, {"CBP_SPLIT_R": "0"}, {"CBP_GLOBAL_TEAMS": "8"},
+                                 {"CBP_GLOBAL_TEAMS": "3"}], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+@pytest.mark.parametrize("name,eb,frames", [("C2", 2.0, 1500), ("C3a", 2.0, 200), ("C1", 2.0, 3000),
+                                            ("P2048", 1.5, 300)])
+def test_state_layouts_equal_oracle(monkeypatch, env, name, eb, frames):
+    """Every state layout the geometry can pick on the same frames: all in
+    shared memory, the split layout (R in the global workspace), and the all-global
+    workspace with warp teams and multi-warp teams (forced through the A/B switches,
+    read when a code is created): decode and ber_sim results equal the oracle's."""
+    _need_gpu()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    base, Z = inputs.config_base(name)
+    g, o = cbp.Code(base, Z), oracle.OracleCode(base, Z)
+    info = g.launch_info()
+    if "CBP_GLOBAL_TEAMS" in env:
+        assert info["state_in_smem"] == 0
+    mi = inputs.get_config(name).max_iter
+    lm = oracle.TX_ZERO if inputs.is_peg(name) else 0
+    llr, _ = o.channel(eb, 9, 0, frames, llr_mode=lm)
+    assert_same(gpu_decode(g, llr, mi), o.decode(llr, mi, want_omega=True), o.N)
+    assert_same(gpu_decode(g, llr, mi, algorithm=1), o.decode(llr, mi, arith=oracle.MINSUM, want_omega=True),
+                o.N, omega=False)
+    got = g.ber_sim(eb, 12, 100, frames, mi, llr_mode=lm).cpu().numpy()
+    assert list(got) == list(o.ber_sim(eb, 12, 100, frames, mi, llr_mode=lm))
+    got = g.ber_sim(eb, 12, 100, frames // 2, mi, 2, llr_mode=lm, algorithm=3).cpu().numpy()
+    assert list(got) == list(o.ber_sim(eb, 12, 100, frames // 2, mi, 2, llr_mode=lm, arith=oracle.FBP))
