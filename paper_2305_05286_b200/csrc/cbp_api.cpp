@@ -300,7 +300,8 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
     const char* sr = std::getenv("CBP_SPLIT_R");
     const int split_env = (sr && (sr[0] == '0' || sr[0] == '1') && sr[1] == 0) ? sr[0] - '0' : -1;
     // geometry with P frames per lane; G.teams == 0 if it does not apply
-    auto make_geo = [&](int alg, int P, bool split_r) {
+    static const int multi_maxt_env = [] { const char* e = std::getenv("CBP_MULTI_MAXT"); return e ? std::atoi(e) : 0; }();
+    auto make_geo = [&](int alg, int P, bool split_r, int multi_maxt = 512) {
         cbp::Geometry G{};
         G.alg = alg;
         G.P = P;
@@ -328,7 +329,10 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         G.team_threads = G.threads;
         // teams per CTA: as many independent teams as shared memory, the thread limit of the
         // instantiation (512 for P = 1, 256 for P = 2) and 15 named barriers allow
-        const int maxt = (P == 2) ? 256 : (G.multi ? 512 : CBP_WARP_MAXT);
+        // thread limit of the instantiation: 512 for multi-warp teams, 768 (80 registers) for the split
+        // layout's multi-warp teams; CBP_MULTI_MAXT overrides it for A/B runs
+        if (multi_maxt_env == 512 || multi_maxt_env == 768 || multi_maxt_env == 1024) multi_maxt = multi_maxt_env;
+        const int maxt = (P == 2) ? 256 : (G.multi ? multi_maxt : CBP_WARP_MAXT);
         if (G.team_threads > maxt && P == 2) return G;
         // shared control words: multi-warp teams exchange ballots and queue indices; warp teams keep
         // nb ballot words for the packed syndrome (kernel syndrome_nz)
@@ -385,6 +389,14 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         if (split_env < 0 && !g1.multi && g1.state_in_smem && g1.teams * g1.team_threads < 256) {
             const cbp::Geometry gs = make_geo(alg, 1, true);
             if (gs.state_in_smem && gs.r_global && gs.teams >= 2 * g1.teams) g1 = gs;
+        }
+        // Multi-warp teams (Z > 32): the split layout with up to 768 threads doubles C3a's teams per SM
+        // (4 -> 8): C3a 11.1 vs 12.4 ms per 5e4 frames at 2.5 dB, 7.9 vs 8.5 at 1.5 dB, C3b 11.7 vs 12.7.
+        // Taken when it at least doubles the threads of the shared-memory geometry (P8192's global
+        // workspace with 8 teams keeps more frames in flight than 2 split teams and stays).
+        if (split_env < 0 && g1.multi && !g1.r_global) {
+            const cbp::Geometry gs = make_geo(alg, 1, true, 768);
+            if (gs.state_in_smem && gs.r_global && gs.teams * gs.team_threads >= 2 * g1.teams * g1.team_threads) g1 = gs;
         }
         // automatic: one frame per lane.  Two interleaved frames per lane halve the warps
         // per SM at the same shared memory and measured slower on every config (C2

@@ -1470,6 +1470,7 @@ static int dispatch(const Geometry& g, Args... args)
     if (g.threads <= 512)
         return sm == 2 ? Fn<true, 2, 512, 1>::run(g, args...)
              : sm == 1 ? Fn<true, 1, 512, 1>::run(g, args...) : Fn<true, 0, 512, 1>::run(g, args...);
+    if (g.threads <= 768 && sm == 2) return Fn<true, 2, 768, 1>::run(g, args...);   // split layout, 85 registers
     return sm == 2 ? Fn<true, 2, 1024, 1>::run(g, args...)
          : sm == 1 ? Fn<true, 1, 1024, 1>::run(g, args...) : Fn<true, 0, 1024, 1>::run(g, args...);
 }
