@@ -191,9 +191,11 @@ cbp_status cbp_ber_sim(const cbp_code* code, double ebn0_db, uint64_t seed, int6
 
 /* Launch geometry the library picks for this code's log-tanh decoder (for reports):
  * threads per CTA, CTAs per SM, frames per CTA, dynamic smem bytes, state in smem (1)
- * or global (0), SMs, frames per lane (1 or 2). */
+ * or global (0), SMs, frames per lane (1 or 2), and r_in_global = 1 for the split layout
+ * (state in smem except the R messages, which live in a global workspace). */
 typedef struct {
     int32_t threads, ctas_per_sm, frames_per_cta, smem_bytes, state_in_smem, num_sms, frames_per_lane;
+    int32_t r_in_global;
 } cbp_launch_info;
 cbp_status cbp_get_launch_info(const cbp_code* code, cbp_launch_info* out);
 

@@ -50,7 +50,7 @@ def _opts(max_iter, stop_rule, algorithm, alpha):
 
 class LaunchInfo(ctypes.Structure):
     _fields_ = [(n, _i32) for n in ("threads", "ctas_per_sm", "frames_per_cta", "smem_bytes", "state_in_smem",
-                                    "num_sms", "frames_per_lane")]
+                                    "num_sms", "frames_per_lane", "r_in_global")]
 
 
 class _CodeConfig(ctypes.Structure):

@@ -444,6 +444,7 @@ cbp_status cbp_get_launch_info(const cbp_code* c, cbp_launch_info* o)
     o->state_in_smem = G.state_in_smem;
     o->num_sms = c->num_sms;
     o->frames_per_lane = G.P;
+    o->r_in_global = G.r_global;
     return CBP_OK;
 }
 

@@ -661,7 +661,11 @@ def test_state_layouts_equal_oracle(monkeypatch, env, name, eb, frames):
     g, o = cbp.Code(base, Z), oracle.OracleCode(base, Z)
     info = g.launch_info()
     if "CBP_GLOBAL_TEAMS" in env:
-        assert info["state_in_smem"] == 0
+        assert info["state_in_smem"] == 0 and info["r_in_global"] == 0
+    if env.get("CBP_SPLIT_R") == "1":
+        assert info["state_in_smem"] == 1 and info["r_in_global"] == 1
+    if env.get("CBP_SPLIT_R") == "0":
+        assert info["r_in_global"] == 0
     mi = inputs.get_config(name).max_iter
     lm = oracle.TX_ZERO if inputs.is_peg(name) else 0
     llr, _ = o.channel(eb, 9, 0, frames, llr_mode=lm)
