@@ -32,6 +32,11 @@ constexpr uint32_t kSign = 0x80000000u;
 #ifndef CBP_CHUNK
 #define CBP_CHUNK 3
 #endif
+// R_{ci->v} loaded with the chunk's other operands instead of after the commits (DESIGN.md §5:
+// C3a -7 %, P2048 -16 %, C2 neutral); 0 restores the load after the commits
+#ifndef CBP_EARLY_R
+#define CBP_EARLY_R 1
+#endif
 // A/B switches CBP_TEX_C2B / CBP_TEX_B2V: evaluate the C2B / B2V phi with the table row
 // fetched through the texture pipe instead of LDS (default: C2B through TEX, DESIGN.md §5;
 // B2V through TEX as well, or one B2V lookup per chunk, measured 4-10% slower).
@@ -253,6 +258,9 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
     using Ly = Lay<P, 0>;
     int aqp[U], aw[U], ar[U];
     float q[U][P], p0[U][P], scj[U][P], Rn[U][P];
+#if CBP_EARLY_R
+    float roe[U][P];
+#endif
     uint32_t fkill[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -276,6 +284,9 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
             p0[u][p] = qp[P + p];
         }
         ldf<P>(g.qp, A.y + tr, scj[u]);
+#if CBP_EARLY_R
+        ldf<P>(g.rb, ar[u], roe[u]);                        // R_{ci->v}, before the commits (see below)
+#endif
     }
     // B2V (equ_s4e18): R^new_{cj->v} = sgn(Omega_cj) sgn(Q) phi(|phi(|Omega_cj|) - phi(|Q|)|), phi(|Omega|) = S (R11)
 #pragma unroll
@@ -297,7 +308,14 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         float ro[P], lam[P];
+#if CBP_EARLY_R
+        // loaded early: only a degree-1 column's entry commits to its own slot (prev(b) = b, aw = ar),
+        // and then the committed value is the one read (R3); no other edge of the chunk shares a slot
+#pragma unroll
+        for (int p = 0; p < P; ++p) ro[p] = (aw[u] == ar[u]) ? Rn[u][p] : roe[u][p];
+#else
         ldf<P>(g.rb, ar[u], ro);                             // R_{ci->v}
+#endif
         vadd<P>(q[u], Rn[u], lam);                           // equ_s4e20 (Lambda is never -0)
         vsub<P>(lam, ro, qn[u]);                             // equ_s4e19 (R15)
 #pragma unroll
@@ -412,6 +430,9 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
     float q[U][P], p0[U][P], Rn[U][P];
     float cm1[U][P], cm2[U][P];
     uint32_t cow[U][P], fkill[U];
+#if CBP_EARLY_R
+    float roe[U][P];
+#endif
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int b = e0 + k0 + u;
@@ -433,6 +454,9 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
             p0[u][p] = qp[P + p];
         }
         ld_rec<P>(g.qp, A.y + Ly::SU * tr, cm1[u], cm2[u], cow[u]);   // record of the previous check c_j
+#if CBP_EARLY_R
+        ldf<P>(g.rb, ar[u], roe[u]);                        // R_{ci->v} early (edge_chunk)
+#endif
     }
     // B2V (equ_s4e18xx)
 #pragma unroll
@@ -449,7 +473,12 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         float ro[P], lam[P], qn[P], st[2 * P];
+#if CBP_EARLY_R
+#pragma unroll
+        for (int p = 0; p < P; ++p) ro[p] = (aw[u] == ar[u]) ? Rn[u][p] : roe[u][p];   // degree-1 column: R3
+#else
         ldf<P>(g.rb, ar[u], ro);
+#endif
         vadd<P>(q[u], Rn[u], lam);                           // equ_s4e20
         vsub<P>(lam, ro, qn);                                // equ_s4e19
 #pragma unroll
