@@ -3,6 +3,7 @@
 # bench; one ncu --set full capture of the C2 2 dB ber_sim launch (tools/profile_summary.py)
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print(\"smoke ok\")" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
 timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
 head -c 1500 gpurun_out/bench.json; echo; tail -2 gpurun_out/bench.err
 B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-suite --frames 200000"
