@@ -194,3 +194,12 @@ def test_oracle_ber_sim_peg_tx_zero():
         o.ber_sim(3.0, 1, 0, 2, 200)
     c = o.ber_sim(3.0, 1, 0, 20, 200, llr_mode=oracle.TX_ZERO)
     assert c[0] == 20 and c[1] == 0 and c[3] == 0 and c[6] == 0
+
+
+@pytest.mark.parametrize("name", ["P2048", "P8192"])
+def test_peg_golden_hash(name):
+    """The QC-PEG members are frozen like the BASELINE codes (tests/golden/base_hashes.txt,
+    tools/write_goldens.py): a change to the constructor must regenerate them and say why."""
+    from tests.test_inputs import _golden
+    base, Z = inputs.config_base(name)
+    assert inputs.base_sha256(base, Z) == _golden()[name]
