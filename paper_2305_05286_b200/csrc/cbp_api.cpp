@@ -232,7 +232,7 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
                 // the previous check (min-sum minimum owner, reading R20)
                 const int kp = p - row_ptr[ent_row[p]];
                 ent[2 * b] = make_int4(QS * j * Z, S0 + SU * RS * ent_row[p] * Z, R0 + RS * p * Z, QS * ent_s[b]);
-                ent[2 * b + 1] = make_int4(RS * ds, first ? -1 : 0, first | (kp << 8) | (ent_s[b] << 16), R0 + RS * b * Z);
+                ent[2 * b + 1] = make_int4(RS * ds, first ? 0 : -1, first | (kp << 8) | (ent_s[b] << 16), R0 + RS * b * Z);
             }
         }
         return ent;

@@ -141,8 +141,8 @@ struct Grp {
 // byte offsets from the group base (QP at 0, check records at S0, R at R0):
 //   E0 = {QS jZ, S0 + SU RS row(prev(b)) Z, R0 + RS prev(b) Z, QS s}: variable block (QP), check
 //        block of the previous check of the same variables, R block of prev(b), rotation of the block
-//   E1 = {RS ds, first ? ~0 : 0, first | kp << 8 | s << 16, R0 + RS b Z}   ds = (s - s_prev) mod Z;
-//        first: no latest check in sweep 1 (R1), as a kill mask and a bit; kp = position of prev(b)
+//   E1 = {RS ds, first ? 0 : ~0, first | kp << 8 | s << 16, R0 + RS b Z}   ds = (s - s_prev) mod Z;
+//        first: no latest check in sweep 1 (R1), as a keep mask and a bit; kp = position of prev(b)
 //        in its row (min-sum owner, R20); own R block
 // The hot loop reads E0 and E1.xy (16 + 8 bytes, 3 shared-memory wavefronts per warp instead of
 // 4) and computes the own R block as R0 + b Z RS.
@@ -244,8 +244,8 @@ struct RowAcc {
 
 // U consecutive edges of lane r's check for the P frames.  Loads first, then U x P
 // independent B2V phi chains, commits / V2C, U x P independent C2B phi chains and
-// the ordered S accumulation (reading R12).  A frame in sweep 1 (s1m[p] all ones)
-// gets R^new = 0 on the first visits of a column (reading R1; kill mask B.w) -- the
+// the ordered S accumulation (reading R12).  A frame in sweep 1 (s1m[p] zero)
+// gets R^new = 0 on the first visits of a column (reading R1; keep mask E1.y = 0 there) -- the
 // commit then writes that 0 into an R slot that still holds its initial 0 (no edge
 // of the column has been processed yet in sweep 1), identical to not writing.  The
 // previous hard bits are recorded for the rollback of a mid-row stop (R5).
@@ -297,8 +297,8 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
         for (int p = 0; p < P; ++p) {
             const float mag = phi_sel<CBP_TEX_B2V>(fabsf(d[p]), ptab, L);
             const uint32_t sg = (__float_as_uint(scj[u][p]) ^ __float_as_uint(q[u][p])) & kSign;
-            // first visit of a frame in sweep 1 (R1): R^new = +0 (kill mask, one LOP3)
-            Rn[u][p] = __uint_as_float((__float_as_uint(mag) | sg) & ~(fkill[u] & s1m[p]));
+            // first visit of a frame in sweep 1 (R1): R^new = +0 (keep mask, one LOP3)
+            Rn[u][p] = __uint_as_float((__float_as_uint(mag) | sg) & (fkill[u] | s1m[p]));
         }
     }
 #pragma unroll
@@ -466,7 +466,7 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
             const uint32_t ow = cow[u][p];
             const float mag = (static_cast<int>(ow & 0xffu) == kp[u]) ? cm2[u][p] : cm1[u][p];
             Rn[u][p] = __uint_as_float((__float_as_uint(mag) | ((ow ^ __float_as_uint(q[u][p])) & kSign)) &
-                                       ~(fkill[u] & s1m[p]));
+                                       (fkill[u] | s1m[p]));
         }
 #pragma unroll
     for (int u = 0; u < U; ++u) stf<P>(g.rb, aw[u], Rn[u]);   // commit of R_{cj->v} (R2, R3)
@@ -1246,9 +1246,9 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_kernel(const __grid_constant__ Ke
                     ro.Snew[p] = ro.Sold[p] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                 }
                 if (live && tm.lane_on) {
-                    uint32_t s1[P];   // all ones for a frame in sweep 1 (first-visit kill mask, R1)
+                    uint32_t s1[P];   // zero for a frame in sweep 1, else all ones (first-visit keep mask, R1)
 #pragma unroll
-                    for (int p = 0; p < P; ++p) s1[p] = (active[p] && sweep[p] == 1) ? kFull : 0u;
+                    for (int p = 0; p < P; ++p) s1[p] = (active[p] && sweep[p] == 1) ? 0u : kFull;
                     const int sidx = (i * Z + r) * Ly::RS;
                     // one code path for every row (smaller code, fewer instruction-cache misses):
                     // first-visit handling and rollback bits always evaluated
