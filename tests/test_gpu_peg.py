@@ -112,3 +112,24 @@ def test_codeword_symmetry_full_size(codes, alg):
     assert torch.equal(a["iters"], b["iters"]) and torch.equal(a["flags"], b["flags"])
     assert torch.equal(a["bits"] ^ cw, b["bits"])
     assert (a["iters"] > 1).any()
+
+
+def test_sweep_cli_peg_equals_oracle(tmp_path, capsys):
+    """The resumable sweep CLI on a PEG code (all-zero codeword chosen automatically):
+    its totals equal the oracle's ber_sim, and a rerun resumes from the checkpoint."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import json
+    from paper_2305_05286_b200 import sweep
+    out = tmp_path / "p2048.jsonl"
+    args = ["--config", "P2048", "--frames", "3000", "--chunk", "1000", "--ebn0", "2.0", "--out", str(out)]
+    sweep.main(args)
+    first = [json.loads(ln) for ln in capsys.readouterr().out.splitlines() if ln.startswith("{")]
+    base, Z = inputs.config_base("P2048")
+    want = oracle.OracleCode(base, Z).ber_sim(2.0, 1, 0, 3000, 200, llr_mode=oracle.TX_ZERO)
+    got = first[0]
+    assert [got[k] for k in cbp.COUNT_NAMES] == [int(x) for x in want]
+    assert json.loads(out.read_text().splitlines()[0])["header"]["llr_mode"] == 2
+    sweep.main(args)                                   # resumes: every chunk already recorded
+    again = [json.loads(ln) for ln in capsys.readouterr().out.splitlines() if ln.startswith("{")]
+    assert again == first and len(out.read_text().splitlines()) == 4
