@@ -261,7 +261,7 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
 #if CBP_EARLY_R
     float roe[U][P];
 #endif
-    uint32_t fkill[U];
+    uint32_t fkeep[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int b = e0 + k0 + u;
@@ -275,7 +275,7 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
         CBP_CHECK(tq >= 0 && tq < L.ZQ && tr >= 0 && tr < L.ZR);
         CBP_CHECK(aqp[u] + Ly::QS <= L.slot_bytes && A.y + tr + Ly::RS <= L.slot_bytes &&
                   ar[u] + Ly::RS <= L.r_bytes && aw[u] + Ly::RS <= L.r_bytes);
-        fkill[u] = static_cast<uint32_t>(B.y);
+        fkeep[u] = static_cast<uint32_t>(B.y);
         float qp[2 * P];
         ldf<2 * P>(g.qp, aqp[u], qp);
 #pragma unroll
@@ -298,7 +298,7 @@ __device__ __forceinline__ void edge_chunk(const int4* __restrict__ ent, const f
             const float mag = phi_sel<CBP_TEX_B2V>(fabsf(d[p]), ptab, L);
             const uint32_t sg = (__float_as_uint(scj[u][p]) ^ __float_as_uint(q[u][p])) & kSign;
             // first visit of a frame in sweep 1 (R1): R^new = +0 (keep mask, one LOP3)
-            Rn[u][p] = __uint_as_float((__float_as_uint(mag) | sg) & (fkill[u] | s1m[p]));
+            Rn[u][p] = __uint_as_float((__float_as_uint(mag) | sg) & (fkeep[u] | s1m[p]));
         }
     }
 #pragma unroll
@@ -429,7 +429,7 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
     int aqp[U], aw[U], ar[U], kp[U];
     float q[U][P], p0[U][P], Rn[U][P];
     float cm1[U][P], cm2[U][P];
-    uint32_t cow[U][P], fkill[U];
+    uint32_t cow[U][P], fkeep[U];
 #if CBP_EARLY_R
     float roe[U][P];
 #endif
@@ -444,7 +444,7 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
         aqp[u] = A.x + tq;
         aw[u] = A.z + tr;
         ar[u] = L.R0 + b * L.ZR + L.rr;
-        fkill[u] = static_cast<uint32_t>(B.y);
+        fkeep[u] = static_cast<uint32_t>(B.y);
         kp[u] = (B.z >> 8) & 0xff;
         float qp[2 * P];
         ldf<2 * P>(g.qp, aqp[u], qp);
@@ -466,7 +466,7 @@ __device__ __forceinline__ void edge_chunk_ms(const int4* __restrict__ ent, int 
             const uint32_t ow = cow[u][p];
             const float mag = (static_cast<int>(ow & 0xffu) == kp[u]) ? cm2[u][p] : cm1[u][p];
             Rn[u][p] = __uint_as_float((__float_as_uint(mag) | ((ow ^ __float_as_uint(q[u][p])) & kSign)) &
-                                       (fkill[u] | s1m[p]));
+                                       (fkeep[u] | s1m[p]));
         }
 #pragma unroll
     for (int u = 0; u < U; ++u) stf<P>(g.rb, aw[u], Rn[u]);   // commit of R_{cj->v} (R2, R3)
