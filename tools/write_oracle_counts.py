@@ -7,7 +7,8 @@ Calls only oracle/ (test infrastructure), never the CUDA path.  The unmodified
 single-threaded oracle runs in one process per core on disjoint frame ranges; the
 counters are integer sums, so the result does not depend on the split.
 
-python tools/write_oracle_counts.py C2 1000000 [cores]
+python tools/write_oracle_counts.py C2 1000000 [cores] [points]
+python tools/write_oracle_counts.py C3a 1e7 16 2.5          (one Eb/N0 point of BASELINE configs[2])
 """
 import json
 import multiprocessing as mp
@@ -35,18 +36,19 @@ if __name__ == "__main__":
     name, frames = sys.argv[1], int(float(sys.argv[2]))
     cores = int(sys.argv[3]) if len(sys.argv) > 3 else os.cpu_count()
     cfg = inputs.CONFIGS[name]
+    points = tuple(float(x) for x in sys.argv[4].split(",")) if len(sys.argv) > 4 else cfg.ebn0_db
     seed, piece = 1, 5000
     jobs = [(name, eb, seed, b, min(piece, frames - b), cfg.max_iter)
-            for eb in cfg.ebn0_db for b in range(0, frames, piece)]
+            for eb in points for b in range(0, frames, piece)]
     t0 = time.time()
-    tot = {eb: np.zeros(8, np.int64) for eb in cfg.ebn0_db}
+    tot = {eb: np.zeros(8, np.int64) for eb in points}
     with mp.get_context("fork").Pool(cores) as pool:
         for eb, c in pool.imap_unordered(work, jobs, chunksize=1):
             tot[eb] += c
     out = {"config": name, "frames_per_point": frames, "seed": seed, "max_iter": cfg.max_iter,
            "stop_rule": "belief W=M (0)", "llr_mode": 0, "algorithm": "CBP log-tanh (0)",
            "written_by": "tools/write_oracle_counts.py (oracle only)", "cpu_seconds_wall": round(time.time() - t0, 1),
-           "counts": {str(eb): [int(x) for x in tot[eb]] for eb in cfg.ebn0_db}}
+           "counts": {str(eb): [int(x) for x in tot[eb]] for eb in points}}
     path = ROOT / "tests" / "golden" / f"oracle_counts_{name}.json"
     path.write_text(json.dumps(out, indent=1) + "\n")
     print(path, out["cpu_seconds_wall"], "s")
