@@ -544,10 +544,10 @@ def test_abi_error_paths(codes):
     gg.decode(torch.zeros((2, 16), dtype=torch.float32, device=dev), 5)
 
 
-@pytest.mark.parametrize("name", ["C2", "C3a"])
+@pytest.mark.parametrize("name", ["C2", "C3a", "C3b"])
 def test_ber_sim_all_frames_equal_oracle_counts(codes, name):
     """BASELINE configs[1] exactly as bench.py runs it (C2, 1.0..3.0 dB, 10^6 frames per
-    point, seed 1, max_iter 30), and configs[2] at 2.5 dB (C3a, all 10^7 frames): the fused
+    point, seed 1, max_iter 30), and configs[2] (C3a at 2.5 dB, C3b at 4.0 dB, all 10^7 frames): the fused
     GPU counters over EVERY frame equal the CPU oracle's (tests/golden/oracle_counts_<name>.json,
     written by tools/write_oracle_counts.py from oracle/ alone) -- bit errors, frame errors,
     iteration and edge-visit sums."""
