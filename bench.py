@@ -1,19 +1,24 @@
 #!/usr/bin/env python
 """Benchmark of the CBP hot path (BASELINE.json metric) -- one JSON line on rank 0.
 
-A step = one fused cbp_ber_sim launch (Philox info bits -> encoder -> BPSK/AWGN
--> CBP decode -> error counting) per Eb/N0 point of BASELINE configs[1]
-(C2: N=648 rate-1/2 QC-LDPC, Eb/N0 1.0..3.0 dB, 1e6 frames per point per GPU,
-max_iter 30) followed by the NCCL all-reduce of the 8 counters per point.
+Headline workload = BASELINE configs[4] (C5, the metric's "per GPU and 8xB200" scaling
+workload): the N=1944 rate-1/2 QC-LDPC code (C3a) at Eb/N0 = 2.5 dB, max_iter 30, fp32 LLR
+stream; the int8 stream (q = sat(rint(4L), +-127)) is measured the same way and reported
+beside it.  A step = one fused cbp_ber_sim launch over this rank's slice of the C5 frame range
+(Philox info bits -> encoder -> BPSK/AWGN -> CBP decode -> error counting), followed by the
+NCCL all-reduce of the 8 counters.  Step s of rank g simulates global frames
+[(s W + g) F, (s W + g + 1) F) of the 10^9-frame C5 range (weak scaling, F per GPU fixed).
 
-  python bench.py [--gpus N --steps K --warmup W]          (N>1: under torchrun)
-  python bench.py --impl reference ...                     (CPU oracle on the host cores)
+  python bench.py [--gpus N --steps K --warmup W]      (N>1: re-launches itself under torchrun)
+  python bench.py --impl reference ...                 (CPU oracle on the host cores)
+  python bench.py --config C2 ...                      (another BASELINE config as the step)
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -25,19 +30,11 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "CBP info Gbit/s and frames/s per GPU and 8×B200 at Eb/N0, % of roofline"
 UNIT = "info Gbit/s"
-I_EDGE = 38            # algorithmic fp32/int ops per edge visit of the arithmetic contract v2
-B_EDGE = 60            # algorithmic on-chip bytes per edge visit: QP r/w 8+8, S_cj 4, R_ci 4, R_cj 4, 2 phi rows 2x16
-
-
-def kernel_traffic():
-    """DRAM bytes per launch and pipe utilisation of the dominant kernel from the
-    latest committed ncu capture (profiles/*_kernel_traffic.json, tools/profile_summary.py)."""
-    caps = sorted((ROOT / "profiles").glob("r*_kernel_traffic.json"))
-    if not caps:
-        return None, None
-    d = json.loads(caps[-1].read_text())
-    d["file"] = caps[-1].name
-    return d["dram_bytes_read"] + d["dram_bytes_write"], d
+I_EDGE = 38            # algorithmic fp32/int ops per edge visit of the arithmetic contract
+BASELINE_INDEX = {"C1": 0, "C2": 1, "C3a": 2, "C3b": 2, "C4": 3, "C5": 4}
+DEFAULT_STEP_FRAMES = {"C5": 4_000_000, "C3a": 4_000_000, "C3b": 4_000_000, "C1": 20_000_000, "C2": 1_000_000,
+                       "C4": 20_000}
+CPU_FRAMES = {"C5": 1000, "C3a": 1000, "C3b": 600, "C1": 20000, "C2": 3000, "C4": 4}
 
 
 def parse():
@@ -46,19 +43,42 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cbp", choices=["cbp", "reference"])
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--frames", type=int, default=None, help="frames per Eb/N0 point per GPU (default: BASELINE)")
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--frames", type=int, default=None, help="frames per Eb/N0 point per GPU and step")
     ap.add_argument("--ebn0", type=str, default=None, help="comma list (default: the config's points)")
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--llr-mode", type=int, default=0)
+    ap.add_argument("--no-int8", action="store_true", help="skip the int8-stream measurement")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-decode", action="store_true", help="skip the cbp_decode (HBM LLR input) roofline")
     ap.add_argument("--no-suite", action="store_true", help="skip the other-config measurements")
-    ap.add_argument("--e2e-frames", type=int, default=200_000)
-    ap.add_argument("--cpu-frames", type=int, default=400,
+    ap.add_argument("--e2e-frames", type=int, default=400_000)
+    ap.add_argument("--cpu-frames", type=int, default=None,
                     help="oracle frames per Eb/N0 point and core (cpu_baseline, reference arm)")
     ap.add_argument("--cpu-cores", type=int, default=0, help="oracle processes (default: all host cores)")
     return ap.parse_args()
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args):
+    """--gpus N: one process per GPU.  Without torchrun's environment the script re-executes
+    itself under torch.distributed.run (127.0.0.1 rendezvous); under torchrun the world size
+    must equal N."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is None:
+        if args.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve()),
+                   *sys.argv[1:]]
+            os.execv(sys.executable, cmd)
+        return
+    if int(world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch with --nproc-per-node {args.gpus}")
 
 
 class ClockSampler:
@@ -107,6 +127,39 @@ def measured_peaks():
         return {}
 
 
+def kernel_traffic(cfg_name: str):
+    """DRAM bytes per frame of the dominant kernel from the latest committed `ncu --set full`
+    capture of the same workload (profiles/r*_<config>_kernel_traffic.json, written by
+    tools/profile_summary.py), or None."""
+    caps = sorted((ROOT / "profiles").glob(f"r*_{cfg_name.lower()}_kernel_traffic.json"))
+    if not caps:
+        return None
+    d = json.loads(caps[-1].read_text())
+    if not d.get("frames"):
+        return None
+    d["file"] = caps[-1].name
+    d["bytes_per_frame"] = (d["dram_bytes_read"] + d["dram_bytes_write"]) / d["frames"]
+    return d
+
+
+def workload_label(cfg, ebn0s):
+    mb, nb, Z = cfg.spec[0], cfg.spec[1], cfg.spec[2]
+    idx = BASELINE_INDEX.get(cfg.name)
+    tag = f"BASELINE configs[{idx}]" if idx is not None else "test code"
+    what = {"C5": "C3a code, 10^9-frame scaling workload"}.get(cfg.name, "")
+    return (f"{cfg.name} ({tag}{', ' + what if what else ''}): QC-LDPC N={nb * Z} K={(nb - mb) * Z} "
+            f"rate {1 - mb / nb:.3f}, Z={Z}, fused cbp_ber_sim at Eb/N0 {', '.join(f'{e:g}' for e in ebn0s)} dB")
+
+
+def config_block(cfg, ebn0s, frames, args, n_gpus, llr="fp32"):
+    return {"workload": workload_label(cfg, ebn0s),
+            "ebn0_db": list(ebn0s), "frames_per_point_per_gpu_per_step": frames, "max_iter": cfg.max_iter,
+            "stop_rule": "belief W=M + syndrome verify", "llr": llr,
+            "seed": args.seed, "parallelism": f"dp{n_gpus} (frame-range shards, NCCL allreduce of counters)",
+            "frame_range": "step s of rank g: global frames [(s*W+g)*F, (s*W+g+1)*F)",
+            "l2": "flushed (256 MiB write) before every step; ber_sim reads no input from HBM"}
+
+
 # ------------------------------------------------------------------ reference arm (CPU oracle)
 def _oracle_slice(job):
     """worker: the unmodified single-threaded oracle on one frame range (one process per core)"""
@@ -133,11 +186,12 @@ def oracle_timed(name, ebn0s, seed, begin, frames, max_iter, llr_mode, cores):
                 jobs.append((name, eb, seed, b, n, max_iter, llr_mode))
     ctx = mpr.get_context("fork")
     with ctx.Pool(cores) as pool:
-        pool.map(_oracle_slice, jobs[:cores])              # warm the workers (library load)
+        pool.map(_oracle_slice, [(j[0], j[1], j[2], j[3], 1, j[5], j[6]) for j in jobs[:cores]])   # warm the workers
         t0 = time.perf_counter()
         res = pool.map(_oracle_slice, jobs, chunksize=1)
         dt = time.perf_counter() - t0
     return np.sum(res, axis=0), dt
+
 
 def run_reference(args, cfg, ebn0s):
     rank = int(os.environ.get("RANK", "0"))
@@ -149,20 +203,20 @@ def run_reference(args, cfg, ebn0s):
     base, Z = inputs.config_base(cfg.name)
     o = oracle.OracleCode(base, Z)
     cores = args.cpu_cores or os.cpu_count() or 1
-    frames = args.cpu_frames * cores
+    frames = (args.cpu_frames or CPU_FRAMES.get(cfg.name, 100)) * cores
     for _ in range(args.warmup):
-        o.ber_sim(ebn0s[0], args.seed, 0, 8, cfg.max_iter)
+        o.ber_sim(ebn0s[0], args.seed, 0, 2, cfg.max_iter)
     times = []
     tot = np.zeros(8, np.int64)
     for s in range(args.steps):
-        c, dt = oracle_timed(cfg.name, ebn0s, args.seed, s * frames, frames, cfg.max_iter, args.llr_mode, cores)
+        c, dt = oracle_timed(cfg.name, ebn0s, args.seed, s * frames, frames, cfg.max_iter, 0, cores)
         tot += c
         times.append(dt)
     T = sum(times)
     fps = tot[0] / T
     gbps = fps * o.K / 1e9
-    sample = (f"{frames} frames x {len(ebn0s)} Eb/N0 points per step ({cfg.name}): the single-threaded oracle in "
-              f"{cores} processes on disjoint frame ranges")
+    sample = (f"{frames} frames x {len(ebn0s)} Eb/N0 point(s) per step ({cfg.name}, fp32 stream): the "
+              f"single-threaded oracle in {cores} processes on disjoint frame ranges")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": gbps, "unit": UNIT, "frames_per_s": fps,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
@@ -173,18 +227,10 @@ def run_reference(args, cfg, ebn0s):
     }))
 
 
-def config_block(cfg, ebn0s, frames, args, n_gpus):
-    return {"workload": f"{cfg.name}: QC-LDPC N={cfg.spec[1] * cfg.spec[2]} rate {1 - cfg.spec[0] / cfg.spec[1]:.3f} "
-                        f"(BASELINE configs[1]) fused cbp_ber_sim, {len(ebn0s)} Eb/N0 points",
-            "ebn0_db": list(ebn0s), "frames_per_point_per_gpu": frames, "max_iter": cfg.max_iter,
-            "stop_rule": "belief W=M + syndrome verify", "llr": "int8" if args.llr_mode else "fp32",
-            "seed": args.seed, "parallelism": f"dp{n_gpus} (frame-range shards, NCCL allreduce of counters)",
-            "l2": "flushed (256 MiB write) before every step; ber_sim reads no input from HBM"}
-
-
 # ------------------------------------------------------------------ product arm
 def main():
     args = parse()
+    self_launch(args)
     import inputs
     cfg = inputs.CONFIGS[args.config]
     ebn0s = [float(x) for x in args.ebn0.split(",")] if args.ebn0 else list(cfg.ebn0_db)
@@ -204,147 +250,188 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    # under torchrun the NCCL process group is set up even for one rank, so the counter
-    # all-reduce and the max-over-ranks timing run through NCCL at every N
-    distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
-    if distributed:
-        dist.init_process_group("nccl", device_id=dev)
-    frames = args.frames or cfg.frames
+    # the NCCL process group exists at every N (a one-rank group when not under torchrun), so the
+    # counter all-reduce of the multi-GPU path runs through NCCL in every bench run
+    if "MASTER_ADDR" not in os.environ:
+        os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(_free_port()), "RANK": "0",
+                           "WORLD_SIZE": "1"})
+    dist.init_process_group("nccl", device_id=dev)
+    n_allreduce = [0]
+
+    def reduce(c):
+        n_allreduce[0] += 1
+        return allreduce_counts(c)
+
+    frames = args.frames or DEFAULT_STEP_FRAMES.get(cfg.name, cfg.frames)
     base, Z = inputs.config_base(cfg.name)
     code = cbp.Code(base, Z, device=local)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)   # 256 MiB > L2
     stream = torch.cuda.current_stream(dev)
+    peaks = measured_peaks()
 
     def barrier():
-        if distributed:
-            dist.barrier()
+        dist.barrier()
 
-    def step(counts_per_point, launch_ms=None):
-        for p, eb in enumerate(ebn0s):
-            c = counts_per_point[p]
-            c.zero_()
-            if launch_ms is not None:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            # this rank's frame range of the global workload (weak scaling: frames per GPU fixed)
-            code.ber_sim(eb, args.seed, rank * frames, frames, cfg.max_iter, llr_mode=args.llr_mode, counts=c,
-                         stream=stream)
-            if launch_ms is not None:
-                e1.record(stream)
-                launch_ms.append((p, e0, e1))
-            allreduce_counts(c)
+    def measure(llr_mode):
+        """W warm-up + K timed steps of the fused ber_sim on this rank's slices; returns
+        (seconds max over ranks, summed counters [points, 8], per-launch ms, local edge visits per launch)."""
+        counts = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in ebn0s]
+        local_ev = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in ebn0s]
 
-    counts = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in ebn0s]
-    for _ in range(args.warmup):
-        step(counts)
-    torch.cuda.synchronize()
+        def step(s, launch_ms=None):
+            for p, eb in enumerate(ebn0s):
+                c = counts[p]
+                c.zero_()
+                if launch_ms is not None:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                code.ber_sim(eb, args.seed, (s * world + rank) * frames, frames, cfg.max_iter, llr_mode=llr_mode,
+                             counts=c, stream=stream)
+                if launch_ms is not None:
+                    e1.record(stream)
+                    launch_ms.append((p, e0, e1))
+                    local_ev[p].copy_(c)
+                reduce(c)
 
-    launches = []
-    step_ms = []
-    with ClockSampler(local) as clk:
-        barrier()
+        for w in range(args.warmup):
+            step(10_000 + w)                                   # warm-up frames outside the timed range
         torch.cuda.synchronize()
-        for _ in range(args.steps):
-            flush.fill_(1.0)                                   # L2 flush outside the step events
-            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s0.record(stream)
-            step(counts, launches)
-            s1.record(stream)
-            step_ms.append((s0, s1))
-        torch.cuda.synchronize()
-        barrier()
-    t_ms = sum(a.elapsed_time(b) for a, b in step_ms)
-    t_max = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-    if distributed:
+        launches, step_ev = [], []
+        with ClockSampler(local) as clk:
+            barrier()
+            torch.cuda.synchronize()
+            for s in range(args.steps):
+                flush.fill_(1.0)                               # L2 flush outside the step events
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record(stream)
+                step(s, launches)
+                s1.record(stream)
+                step_ev.append((s0, s1))
+            torch.cuda.synchronize()
+            barrier()
+        t_ms = sum(a.elapsed_time(b) for a, b in step_ev)
+        t_max = torch.tensor([t_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    T = t_max.item() / 1e3
-    tot = torch.stack(counts).cpu().numpy()                   # counts of the last step, all ranks summed
-    frames_all = int(tot[:, 0].sum()) * args.steps
+        per_launch = np.array([a.elapsed_time(b) for _, a, b in launches]).reshape(args.steps, len(ebn0s))
+        tot = torch.stack(counts).cpu().numpy()                # last step, all ranks summed
+        ev_loc = torch.stack(local_ev).cpu().numpy()[:, 5]     # last step, this rank's edge visits per launch
+        return t_max.item() / 1e3, tot, per_launch, ev_loc, clk.summary()
+
+    T, tot, per_launch, ev_loc, clocks = measure(0)
+    frames_all = frames * len(ebn0s) * args.steps * world
     fps = frames_all / T
     gbps = fps * code.K / 1e9
 
-    # roofline of the dominant kernel (the fused cbp_kernel launch, one per Eb/N0 point)
-    per_launch_ms = [a.elapsed_time(b) for _, a, b in launches]
-    ev_local = []
-    for p in range(len(ebn0s)):
-        ev_local.append(int(tot[p, 5]) // max(world, 1))       # edge visits per launch (this rank's share)
-    dur = np.array(per_launch_ms).reshape(args.steps, len(ebn0s)).mean(axis=0) / 1e3
-    ops = np.array(ev_local, dtype=np.float64) * I_EDGE
-    traffic, traffic_src = kernel_traffic()
-    achieved = float(ops.sum() / dur.sum())                    # ops/s averaged over the launches of a step
+    # roofline of the dominant kernel (the fused cbp_kernel launch): I_edge x exact edge visits of a
+    # launch / its mean CUDA-event duration, against the derived issue peak (DESIGN.md §7)
     li = code.launch_info()
-    clocks = clk.summary()
-    f_sm = measured_peaks().get("sm_max_mhz", 1965.0)
+    f_sm = peaks.get("sm_max_mhz", 1965.0)
     peak = li["num_sms"] * 128 * f_sm * 1e6
+    dur = per_launch.mean(axis=0) / 1e3
+    achieved = float((ev_loc.astype(np.float64) * I_EDGE).sum() / dur.sum())
+    tr = kernel_traffic(cfg.name)
     roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Top/s",
-                "frac": achieved / peak, "traffic": traffic,
-                "note": f"I_edge={I_EDGE} contract ops/edge-visit x exact edge visits / mean launch time; peak = "
-                        f"{li['num_sms']} SM x 128 lanes x {f_sm:.0f} MHz (sm_max, MEASURED_PEAKS.json, derived "
-                        f"issue peak); traffic = DRAM bytes/launch from "
-                        f"{traffic_src.get('file', 'n/a') if traffic_src else 'n/a'} (algorithmic HBM bytes of "
-                        f"ber_sim: 0 in, 64 out)"}
-    # the resources that actually bind: the on-chip data pipes and the issue slots,
-    # measured by ncu on the same kernel (C2, 2 dB, 1e5 frames) and committed under profiles/
-    on_chip = float(np.array(ev_local, dtype=np.float64).sum() * B_EDGE / dur.sum())
-    onchip_peak = li["num_sms"] * 128 * f_sm * 1e6
-    roofline_onchip = {"bound": "smem+tex data pipes", "achieved": on_chip / 1e12, "peak": onchip_peak / 1e12,
-                       "unit": "TB/s", "frac": on_chip / onchip_peak,
-                       "note": f"B_edge={B_EDGE} algorithmic on-chip bytes/edge-visit (no bank conflicts) x edge "
-                               f"visits / mean launch time; peak = 128 B/clk/SM x {li['num_sms']} SM x {f_sm:.0f} MHz "
-                               f"(one shared-memory wavefront per clock)"}
-    if traffic_src:
-        roofline_onchip["ncu_pipe_utilisation_pct"] = {k: traffic_src.get(k) for k in (
-            "smem_pipe_pct", "tex_pipe_pct", "issue_active_pct", "alu_pipe_pct", "fma_pipe_pct")}
-        roofline_onchip["ncu_lane_slots_per_edge_visit"] = traffic_src.get("lane_slots_per_edge_visit")
-        roofline_onchip["ncu_source"] = traffic_src.get("file")
+                "frac": achieved / peak,
+                "traffic": tr["bytes_per_frame"] * frames if tr else None,
+                "edge_visits_per_launch": int(ev_loc.mean()), "launch_ms": float(dur.mean() * 1e3),
+                "edge_visits_per_s": float(ev_loc.sum() / dur.sum()),
+                "note": f"I_edge={I_EDGE} contract ops/edge visit x exact edge visits / mean launch time (CUDA events "
+                        f"on the launch stream); peak = {li['num_sms']} SM x 128 lanes x {f_sm:.0f} MHz (sm_max, "
+                        f"MEASURED_PEAKS.json; derived issue peak); traffic = DRAM bytes per launch scaled from the "
+                        f"per-frame bytes of {tr['file'] if tr else 'n/a'} (ncu --set full of this workload); "
+                        f"algorithmic HBM bytes of ber_sim: 0 in, 64 out"}
+    if tr:
+        roofline["ncu"] = {k: tr.get(k) for k in ("issue_active_pct", "lane_slots_per_edge_visit", "smem_pipe_pct",
+                                                  "tex_pipe_pct", "alu_pipe_pct", "fma_pipe_pct", "file")}
 
-    # end-to-end over the same Eb/N0 points: host LLRs -> cbp_decode (pipelined H2D / decode / D2H)
-    # -> host outputs.  Per point the pinned host buffer is filled (untimed), then decode_host is
-    # timed on the host clock (copies in both directions inside); the step time is the sum.
+    int8 = None
+    if not args.no_int8:
+        T8, tot8, pl8, ev8, clk8 = measure(1)
+        f8 = frames * len(ebn0s) * args.steps * world / T8
+        d8 = pl8.mean(axis=0) / 1e3
+        int8 = {"value": f8 * code.K / 1e9, "unit": UNIT, "frames_per_s": f8, "ms_per_step": 1e3 * T8 / args.steps,
+                "roofline_frac": float((ev8.astype(np.float64) * I_EDGE).sum() / d8.sum() / peak),
+                "ber": float(tot8[:, 1].sum() / max(1, tot8[:, 0].sum() * code.K)),
+                "fer": float(tot8[:, 2].sum() / max(1, tot8[:, 0].sum())),
+                "avg_iters": float(tot8[:, 4].sum() / max(1, tot8[:, 0].sum())), "clocks": clk8,
+                "what": "the same steps with the int8 LLR stream (q = sat(rint(4L), +-127), L = q/4)"}
+
+    # cbp_decode roofline: LLRs resident in HBM (read once per frame) against the ALU term
+    decode_rl = None
+    if not args.no_decode:
+        Fd = min(frames, 2_000_000)
+        ld = (code.N + 3) // 4 * 4
+        llr = torch.empty((Fd, ld), dtype=torch.float32, device=dev)
+        for b in range(0, Fd, 1 << 18):
+            n = min(1 << 18, Fd - b)
+            l_, _ = code.channel(ebn0s[0], args.seed + 2, rank * Fd + b, n, want_cw=False)
+            llr[b:b + n].copy_(l_)
+        out = code.alloc_outputs(Fd, ev=True)
+        code.decode(llr[:1024], cfg.max_iter, out={k: v[:1024] for k, v in out.items()}, stream=stream)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(3):
+            flush.fill_(1.0)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            code.decode(llr, cfg.max_iter, out=out, stream=stream)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a0.elapsed_time(a1) / 1e3)
+        td = float(np.median(ts))
+        evd = float(out["ev"].sum().item())
+        llr_bytes = Fd * ld * 4
+        out_bytes = Fd * (code.words * 4 + 5)
+        t_hbm = (llr_bytes + out_bytes) / (peaks.get("hbm_gbs", 6556.2) * 1e9)
+        t_alu = evd * I_EDGE / peak
+        decode_rl = {"bound": "alu" if t_alu >= t_hbm else "hbm", "frames": Fd, "ms": td * 1e3,
+                     "frames_per_s": Fd / td, "info_gbps": Fd * code.K / td / 1e9,
+                     "achieved": evd * I_EDGE / td / 1e12, "peak": peak / 1e12, "unit": "Top/s",
+                     "frac": max(t_alu, t_hbm) / td, "hbm_term_ms": t_hbm * 1e3, "alu_term_ms": t_alu * 1e3,
+                     "llr_bytes": llr_bytes, "achieved_hbm_gbs": (llr_bytes + out_bytes) / td / 1e9,
+                     "hbm_peak_gbs": peaks.get("hbm_gbs", 6556.2),
+                     "what": f"cbp_decode of {Fd} device-resident fp32 C5 frames (ld={ld}); roofline time = max(LLR + "
+                             f"output bytes / HBM peak, I_edge x edge visits / issue peak); frac = roofline time / "
+                             f"median measured time (3 launches, L2 flushed)"}
+        del llr, out
+
+    # end-to-end: host LLRs -> cbp_decode -> host outputs (pinned host buffers, copies timed)
     e2e = None
     if not args.no_e2e:
         Fe = args.e2e_frames
         ld = (code.N + 3) // 4 * 4
         host = torch.empty((Fe, ld), dtype=torch.float32, pin_memory=True)
         hout = pipeline.alloc_host_outputs(code, Fe)
-        te = 0.0
+        for b in range(0, Fe, 1 << 17):
+            n = min(1 << 17, Fe - b)
+            llr_, _ = code.channel(ebn0s[0], args.seed + 1, rank * Fe + b, n, want_cw=False)
+            host[b:b + n].copy_(llr_)
+        torch.cuda.synchronize()
+        pipeline.decode_host(code, host, cfg.max_iter, out=hout)         # warm-up
         reps = max(1, min(args.steps, 3))
-        for eb in ebn0s:
-            for b in range(0, Fe, 1 << 17):
-                n = min(1 << 17, Fe - b)
-                llr, _ = code.channel(eb, args.seed + 1, rank * Fe + b, n, want_cw=False)
-                host[b:b + n].copy_(llr)
-            torch.cuda.synchronize()
-            pipeline.decode_host(code, host, cfg.max_iter, out=hout)     # warm-up of this point
-            barrier()
-            t0 = time.perf_counter()
-            for _ in range(reps):
-                pipeline.decode_host(code, host, cfg.max_iter, out=hout)
-            te += time.perf_counter() - t0
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            pipeline.decode_host(code, host, cfg.max_iter, out=hout)
+        te = time.perf_counter() - t0
         tmax = torch.tensor([te], dtype=torch.float64, device=dev)
-        if distributed:
-            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         te = tmax.item()
-        e2e = {"value": reps * len(ebn0s) * Fe * world * code.K / te / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": len(ebn0s) * Fe * ld * 4 * world,
-               "d2h_bytes_per_step": len(ebn0s) * Fe * (code.words * 4 + 5) * world,
-               "what": f"cbp_decode via pipeline.decode_host on {Fe} host-resident frames/GPU at each of the "
-                       f"{len(ebn0s)} Eb/N0 points (pinned host LLRs, H2D + decode + D2H of bits/iters/flags "
-                       f"timed, host wall clock, max over ranks)"}
+        e2e = {"value": reps * Fe * world * code.K / te / 1e9, "unit": UNIT,
+               "frames_per_s": reps * Fe * world / te,
+               "h2d_bytes_per_step": Fe * ld * 4 * world, "d2h_bytes_per_step": Fe * (code.words * 4 + 5) * world,
+               "what": f"{pipeline.API_NAME} on {Fe} host-resident fp32 frames/GPU of the same workload (pinned host "
+                       f"LLRs; H2D + decode + D2H of bits/iters/flags inside the timed region; host wall clock, "
+                       f"max over ranks; {reps} reps)"}
 
-    # the other BASELINE configs, one timed fused launch each (after a warm-up launch):
-    # C1 @ 2 dB; C3a / C3b (rates 1/2, 5/6); C4 (global-state path, syndrome stop);
-    # C5 = C3a @ 2.5 dB with the fp32 and the int8 LLR stream
+    # the other BASELINE configs and variants, one timed fused launch each (after a warm-up launch)
     others = {}
     if not args.no_suite:
-        # (config, Eb/N0, frames, stop rule, llr mode, algorithm): the other BASELINE configs, the C2 stop-rule
-        # variants (W=N, syndrome per sweep), normalized min-sum CBP (NEXT-1) and the paper's comparison
-        # schedules LBP / FBP (NEXT-3) on the same frames
-        suite = [("C1", 2.0, 1_000_000, 0, 0, 0), ("C3a", 2.5, 300_000, 0, 0, 0), ("C5", 2.5, 300_000, 0, 1, 0),
-                 ("C3b", 4.0, 300_000, 0, 0, 0), ("C4", 1.5, 3_000, 2, 0, 0), ("C2", 2.0, 1_000_000, 1, 0, 0),
-                 ("C2", 2.0, 1_000_000, 2, 0, 0), ("C2", 2.0, 1_000_000, 0, 0, 1),
-                 ("C2", 2.0, 1_000_000, 2, 0, 2), ("C2", 2.0, 1_000_000, 2, 0, 3),
-                 # the paper's own code families (QC-PEG; all-zero codeword, max 200 iterations)
+        suite = [("C2", 1.0, 500_000, 0, 0, 0), ("C2", 2.0, 500_000, 0, 0, 0), ("C2", 3.0, 500_000, 0, 0, 0),
+                 ("C1", 2.0, 2_000_000, 0, 0, 0), ("C3a", 1.5, 300_000, 0, 0, 0),
+                 ("C3b", 4.0, 300_000, 0, 0, 0), ("C4", 1.5, 3_000, 2, 0, 0),
+                 ("C2", 2.0, 500_000, 1, 0, 0), ("C2", 2.0, 500_000, 2, 0, 0), ("C2", 2.0, 500_000, 0, 0, 1),
+                 ("C2", 2.0, 500_000, 2, 0, 2), ("C2", 2.0, 500_000, 2, 0, 3),
                  ("P2048", 2.0, 300_000, 0, 2, 0), ("P8192", 1.5, 30_000, 0, 2, 0)]
         for name, eb, nf, rule, lm, alg in suite:
             ocfg = inputs.get_config(name)
@@ -360,22 +447,25 @@ def main():
             oc.ber_sim(eb, args.seed, rank * nf, nf, ocfg.max_iter, rule, lm, counts=c, stream=stream,
                        algorithm=alg)
             a1.record(stream)
-            allreduce_counts(c)
+            reduce(c)
             torch.cuda.synchronize()
             ms = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
-            if distributed:
-                dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
             t = c.cpu().numpy()
-            key = f"{name}@{eb}dB" + ("/int8" if lm & 1 else "") + ("/zero-cw" if lm & 2 else "") + ["", "/min-sum", "/LBP", "/FBP"][alg] + \
+            key = f"{name}@{eb}dB" + ("/int8" if lm & 1 else "") + ("/zero-cw" if lm & 2 else "") + \
+                ["", "/min-sum", "/LBP", "/FBP"][alg] + \
                 ("" if rule == 0 or name == "C4" else ["", "/W=N", "/syndrome", "/none"][rule])
             others[key] = {
                 "N": oc.N, "K": oc.K, "frames": int(t[0]), "ms": ms.item(),
                 "frames_per_s": t[0] / ms.item() * 1e3, "info_gbps": t[0] * oc.K / ms.item() / 1e6,
-                "edge_visits_per_s": t[5] / ms.item() * 1e3, "ber": t[1] / max(1, t[0] * oc.K),
+                "edge_visits_per_s": t[5] / ms.item() * 1e3,
+                "alu_frac": t[5] / world * I_EDGE / (ms.item() / 1e3) / peak,
+                "ber": t[1] / max(1, t[0] * oc.K),
                 "fer": t[2] / max(1, t[0]), "avg_iters": t[4] / max(1, t[0]),
                 "stop_rule": ["belief W=M", "belief W=N", "syndrome", "none"][rule],
                 "algorithm": ["CBP log-tanh", "CBP normalized min-sum (alpha 0.75)", "layered BP (comparison)",
                               "flooding BP (comparison)"][alg],
+                "note": "fixed 25 sweeps: FER ~1, the weak C4 code never converges" if name == "C4" else "",
                 "launch": oc.launch_info()}
 
     cpu = None
@@ -383,20 +473,20 @@ def main():
         try:
             import oracle
             o = oracle.OracleCode(base, Z)
+            nfc = args.cpu_frames or CPU_FRAMES.get(cfg.name, 100)
             t0 = time.perf_counter()
             c1 = np.zeros(8, np.int64)
-            for p, eb in enumerate(ebn0s):
-                c1 += o.ber_sim(eb, args.seed, 0, args.cpu_frames, cfg.max_iter, llr_mode=args.llr_mode)
+            for eb in ebn0s:
+                c1 += o.ber_sim(eb, args.seed, 0, max(1, nfc // 4), cfg.max_iter)
             t1 = time.perf_counter() - t0
             cores = args.cpu_cores or os.cpu_count() or 1
-            cN, tN = oracle_timed(cfg.name, ebn0s, args.seed, 0, args.cpu_frames * cores, cfg.max_iter,
-                                  args.llr_mode, cores)
+            cN, tN = oracle_timed(cfg.name, ebn0s, args.seed, 0, nfc * cores, cfg.max_iter, 0, cores)
             cpu = {"value": cN[0] * o.K / tN / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
-                   "sample": f"{args.cpu_frames * cores} frames x {len(ebn0s)} Eb/N0 points of the same workload: "
-                             f"the single-threaded C++ oracle in {cores} processes on disjoint frame ranges, "
-                             f"{tN:.1f} s", "frames_per_s": cN[0] / tN,
+                   "sample": f"{nfc * cores} frames x {len(ebn0s)} Eb/N0 point(s) of the same workload (fp32 "
+                             f"stream): the single-threaded C++ oracle in {cores} processes on disjoint frame "
+                             f"ranges, {tN:.1f} s", "frames_per_s": cN[0] / tN,
                    "single_core": {"value": c1[0] * o.K / t1 / 1e9, "frames_per_s": c1[0] / t1,
-                                   "sample": f"{args.cpu_frames} frames x {len(ebn0s)} points, {t1:.1f} s"}}
+                                   "sample": f"{max(1, nfc // 4)} frames x {len(ebn0s)} point(s), {t1:.1f} s"}}
         except Exception as ex:   # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {ex}"}
 
@@ -412,14 +502,16 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_block(cfg, ebn0s, frames, args, world),
-            "roofline": roofline, "roofline_onchip": roofline_onchip, "cpu_baseline": cpu, "e2e": e2e,
-            "clocks": clocks,
-            "gpu_launches": args.steps * len(ebn0s), "launch": li, "results": results,
-            "other_configs": others,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "int8_stream": int8, "roofline_decode": decode_rl,
+            "gpu_launches": args.steps * len(ebn0s),
+            "collectives": {"backend": dist.get_backend(), "world_size": world,
+                            "counter_allreduce_calls": n_allreduce[0],
+                            "per_timed_step": len(ebn0s)},
+            "launch": li, "results_last_step": results, "other_configs": others,
         }
         print(json.dumps(line))
-    if distributed:
-        dist.destroy_process_group()
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -54,6 +54,8 @@ def _lib():
             "oracle_minsum_cbp_trace": ([_p, _p, _i32, _f32, _p], ctypes.c_int),
             "oracle_minsum_lbp_trace": ([_p, _p, _i32, _f32, _p], ctypes.c_int),
             "oracle_ml_decode": ([_p, _p, _p], ctypes.c_int),
+            "oracle_decode_window": ([_p, _p, _i64, _i64, _p, _i64, _p, _i64, _p, _p, _p, _p], ctypes.c_int),
+            "oracle_cbp_visit_trace": ([_p, _p, _i32, _i32, _f32, _p, _p], ctypes.c_int),
             "oracle_phi32": ([_f32], _f32),
             "oracle_ln32": ([_f32], _f32),
             "oracle_sincos_quarter32": ([ctypes.c_uint32, _p, _p], None),
@@ -125,6 +127,32 @@ class OracleCode:
         if want_omega:
             out["omega"] = om
         return out
+
+    def decode_window(self, llr: np.ndarray, max_iter: int, window: int, stop_rule: int = STOP_BELIEF_M,
+                      arith: int = FP32_CONTRACT, alpha: float = ALPHA_DEFAULT) -> dict:
+        """decode with the belief window W (reading R4) replaced by `window` (test-only hook)."""
+        llr = np.ascontiguousarray(llr, dtype=np.float32).reshape(-1, self.N)
+        F = llr.shape[0]
+        out = {"bits": np.zeros((F, self.words), np.uint32), "iters": np.zeros(F, np.int32),
+               "flags": np.zeros(F, np.uint8), "edge_visits": np.zeros(F, np.int64),
+               "fires": np.zeros(F, np.int32)}
+        o = Opts(max_iter, stop_rule, arith, alpha)
+        rc = _lib().oracle_decode_window(self._h, _ptr(llr), self.N, F, ctypes.byref(o), window, _ptr(out["bits"]),
+                                         self.words, _ptr(out["iters"]), _ptr(out["flags"]),
+                                         _ptr(out["edge_visits"]), _ptr(out["fires"]))
+        if rc:
+            raise ValueError(f"oracle_decode_window rc={rc}")
+        return out
+
+    def visit_trace(self, llr: np.ndarray, sweeps: int, arith: int = FP64, alpha: float = ALPHA_DEFAULT):
+        """(lam, qn) float64 [sweeps, E]: Lambda^new and Q^new of every edge visit, no stop rule."""
+        lam = np.zeros((sweeps, self.E), np.float64)
+        qn = np.zeros((sweeps, self.E), np.float64)
+        rc = _lib().oracle_cbp_visit_trace(self._h, _ptr(np.ascontiguousarray(llr, np.float32)), sweeps, arith,
+                                           alpha, _ptr(lam), _ptr(qn))
+        if rc:
+            raise ValueError("oracle_cbp_visit_trace failed")
+        return lam, qn
 
     def encode(self, info_bits: np.ndarray) -> np.ndarray:
         """info_bits: uint8[K] -> codeword uint8[N]."""

@@ -298,13 +298,23 @@ struct FrameResult {
     int32_t fires = 0;
 };
 
+// Test-only instrumentation of cbp_frame (no effect on the arithmetic): `window` > 0 replaces
+// the stop window W of reading R4 (a small W forces mid-row fires and failed verifications
+// for the stop-rule pin); `lam` / `qn` receive Lambda^new / Q^new of every edge visit, at
+// [(sweep-1) E + e] when `per_sweep`, else at [e] (overwritten every sweep).
+struct Instr {
+    int64_t window = 0;
+    double* lam = nullptr;
+    double* qn = nullptr;
+    bool per_sweep = false;
+};
+
 // One frame of CBP, §IV-C.  `literal` selects the literal psi+
 // recursion (equ_s4e5/equ_s4e6) instead of the phi-domain accumulator (R11).
-// `trace` (fp64 test pin) receives Lambda^new per edge visit.
 template <class T>
 static FrameResult cbp_frame(const or_code* c, const float* L, const or_opts* o, bool literal,
                              std::vector<uint8_t>& xhat, std::vector<T>* S_out, std::vector<uint8_t>* neg_out,
-                             double* trace)
+                             const Instr& ins = Instr())
 {
     const int32_t N = c->N, M = c->M;
     const int32_t NONE = -1;
@@ -320,7 +330,8 @@ static FrameResult cbp_frame(const or_code* c, const float* L, const or_opts* o,
         Q[v] = (T)L[v];
         xhat[v] = Q[v] < (T)0;                   // decision rule equ_s2e7
     }
-    const int64_t W = (o->stop_rule == OR_STOP_BELIEF_N) ? (int64_t)N : (int64_t)M;   // R4
+    int64_t W = (o->stop_rule == OR_STOP_BELIEF_N) ? (int64_t)N : (int64_t)M;   // R4
+    if (ins.window > 0) W = ins.window;
     const bool belief = o->stop_rule == OR_STOP_BELIEF_M || o->stop_rule == OR_STOP_BELIEF_N;
     int64_t consec = 0;
     FrameResult res;
@@ -356,7 +367,11 @@ static FrameResult cbp_frame(const or_code* c, const float* L, const or_opts* o,
                 // (1c) V2C, equ_s4e20 / equ_s4e19 (rounding order R15)
                 const T lam = Q[v] + Rn;
                 const T qn = lam - R[e];
-                if (trace) trace[e] = (double)lam;
+                if (ins.lam) {
+                    const int64_t at = (ins.per_sweep ? (int64_t)(sweep - 1) * c->E : 0) + e;
+                    ins.lam[at] = (double)lam;
+                    if (ins.qn) ins.qn[at] = (double)qn;
+                }
                 const uint8_t bit = lam < (T)0;  // hard decision, equ_s2e7 (l.450)
                 if (bit != xhat[v]) flip = true; // equ_s4e24 (R7)
                 xhat[v] = bit;
@@ -419,7 +434,7 @@ static FrameResult cbp_frame(const or_code* c, const float* L, const or_opts* o,
 // sgn(R^new) = sgn(Omega_cj) sgn(Q), sgn(Omega_c) = prod sgn(Q^new).  Omega^(-1) = (inf, inf).
 // Everything else (Step 1, V2C, commit, stop rule) is the CBP schedule of cbp_frame.
 static FrameResult minsum_frame(const or_code* c, const float* L, const or_opts* o, std::vector<uint8_t>& xhat,
-                                std::vector<float>* om_out, float* trace)
+                                std::vector<float>* om_out, const Instr& ins = Instr())
 {
     const int32_t N = c->N, M = c->M;
     const int32_t NONE = -1;
@@ -434,7 +449,8 @@ static FrameResult minsum_frame(const or_code* c, const float* L, const or_opts*
         Q[v] = L[v];
         xhat[v] = Q[v] < 0.0f;
     }
-    const int64_t W = (o->stop_rule == OR_STOP_BELIEF_N) ? (int64_t)N : (int64_t)M;
+    int64_t W = (o->stop_rule == OR_STOP_BELIEF_N) ? (int64_t)N : (int64_t)M;
+    if (ins.window > 0) W = ins.window;
     const bool belief = o->stop_rule == OR_STOP_BELIEF_M || o->stop_rule == OR_STOP_BELIEF_N;
     int64_t consec = 0;
     FrameResult res;
@@ -458,7 +474,11 @@ static FrameResult minsum_frame(const or_code* c, const float* L, const or_opts*
                 }
                 const float lam = Q[v] + Rn;                      // V2C, equ_s4e20 / equ_s4e19
                 const float qn = lam - R[e];
-                if (trace) trace[e] = lam;
+                if (ins.lam) {
+                    const int64_t at = (ins.per_sweep ? (int64_t)(sweep - 1) * c->E : 0) + e;
+                    ins.lam[at] = (double)lam;
+                    if (ins.qn) ins.qn[at] = (double)qn;
+                }
                 const uint8_t bit = lam < 0.0f;
                 if (bit != xhat[v]) flip = true;
                 xhat[v] = bit;
@@ -619,9 +639,9 @@ static bool opts_ok(const or_opts* o)
     return true;
 }
 
-int oracle_decode(const or_code* c, const float* llr, int64_t ld, int64_t frames, const or_opts* o,
-                  uint32_t* bits, int64_t ld_words, int32_t* iters, uint8_t* flags,
-                  int64_t* edge_visits, int32_t* fires, float* omega)
+static int decode_impl(const or_code* c, const float* llr, int64_t ld, int64_t frames, const or_opts* o,
+                       uint32_t* bits, int64_t ld_words, int32_t* iters, uint8_t* flags,
+                       int64_t* edge_visits, int32_t* fires, float* omega, const Instr& ins)
 {
     if (!c || !opts_ok(o) || frames < 0 || ld < c->N || (bits && ld_words < (c->N + 31) / 32)) return 1;
     std::vector<uint8_t> xhat;
@@ -633,12 +653,12 @@ int oracle_decode(const or_code* c, const float* llr, int64_t ld, int64_t frames
             if (omega) std::fill(omega + f * c->M, omega + (f + 1) * c->M, 0.0f);
         } else if (o->arith == OR_MINSUM) {
             std::vector<float> om;
-            r = minsum_frame(c, L, o, xhat, omega ? &om : nullptr, nullptr);
+            r = minsum_frame(c, L, o, xhat, omega ? &om : nullptr, ins);
             if (omega) std::copy(om.begin(), om.end(), omega + f * c->M);
         } else if (o->arith == OR_FP32_CONTRACT) {
             std::vector<float> S;
             std::vector<uint8_t> neg;
-            r = cbp_frame<float>(c, L, o, false, xhat, omega ? &S : nullptr, &neg, nullptr);
+            r = cbp_frame<float>(c, L, o, false, xhat, omega ? &S : nullptr, &neg, ins);
             // Omega_c = sgn * phi(S_c)  (equ_s4e3 in the phi domain)
             if (omega)
                 for (int32_t ck = 0; ck < c->M; ++ck) {
@@ -649,7 +669,7 @@ int oracle_decode(const or_code* c, const float* llr, int64_t ld, int64_t frames
             std::vector<double> S;
             std::vector<uint8_t> neg;
             const bool lit = o->arith == OR_FP64_LITERAL;
-            r = cbp_frame<double>(c, L, o, lit, xhat, omega ? &S : nullptr, &neg, nullptr);
+            r = cbp_frame<double>(c, L, o, lit, xhat, omega ? &S : nullptr, &neg, ins);
             if (omega)
                 for (int32_t ck = 0; ck < c->M; ++ck) {
                     double m;
@@ -669,6 +689,23 @@ int oracle_decode(const or_code* c, const float* llr, int64_t ld, int64_t frames
         if (fires) fires[f] = r.fires;
     }
     return 0;
+}
+
+int oracle_decode(const or_code* c, const float* llr, int64_t ld, int64_t frames, const or_opts* o,
+                  uint32_t* bits, int64_t ld_words, int32_t* iters, uint8_t* flags,
+                  int64_t* edge_visits, int32_t* fires, float* omega)
+{
+    return decode_impl(c, llr, ld, frames, o, bits, ld_words, iters, flags, edge_visits, fires, omega, Instr());
+}
+
+int oracle_decode_window(const or_code* c, const float* llr, int64_t ld, int64_t frames, const or_opts* o,
+                         int64_t window, uint32_t* bits, int64_t ld_words, int32_t* iters, uint8_t* flags,
+                         int64_t* edge_visits, int32_t* fires)
+{
+    if (window < 1 || !o || o->arith == OR_LBP || o->arith == OR_FBP) return 1;
+    Instr ins;
+    ins.window = window;
+    return decode_impl(c, llr, ld, frames, o, bits, ld_words, iters, flags, edge_visits, fires, nullptr, ins);
 }
 
 int oracle_ber_sim(const or_code* c, double ebn0_db, uint64_t seed, int64_t frame_begin, int64_t frames,
@@ -706,16 +743,29 @@ int oracle_ber_sim(const or_code* c, double ebn0_db, uint64_t seed, int64_t fram
 int oracle_cbp_trace_f64(const or_code* c, const float* llr, int32_t sweeps, double* lam)
 {
     if (!c || sweeps < 1) return 1;
-    // cbp_frame overwrites trace[e] on every visit, so running s sweeps leaves
-    // sweep s's values; re-run each prefix (O(sweeps^2), sweeps are small).
     or_opts o = {sweeps, OR_STOP_NONE, OR_FP64, 0};
+    Instr ins;
+    ins.lam = lam;
+    ins.per_sweep = true;
     std::vector<uint8_t> xhat;
-    for (int32_t s = 1; s <= sweeps; ++s) {
-        o.max_iter = s;
-        std::vector<double> tmp(c->E);
-        cbp_frame<double>(c, llr, &o, false, xhat, nullptr, nullptr, tmp.data());
-        std::copy(tmp.begin(), tmp.end(), lam + (int64_t)(s - 1) * c->E);
-    }
+    cbp_frame<double>(c, llr, &o, false, xhat, nullptr, nullptr, ins);
+    return 0;
+}
+
+int oracle_cbp_visit_trace(const or_code* c, const float* llr, int32_t sweeps, int32_t arith, float alpha,
+                           double* lam, double* qn)
+{
+    if (!c || sweeps < 1 || !lam || !qn || (arith != OR_FP32_CONTRACT && arith != OR_FP64 && arith != OR_MINSUM))
+        return 1;
+    or_opts o = {sweeps, OR_STOP_NONE, arith, alpha};
+    Instr ins;
+    ins.lam = lam;
+    ins.qn = qn;
+    ins.per_sweep = true;
+    std::vector<uint8_t> xhat;
+    if (arith == OR_FP64) cbp_frame<double>(c, llr, &o, false, xhat, nullptr, nullptr, ins);
+    else if (arith == OR_MINSUM) minsum_frame(c, llr, &o, xhat, nullptr, ins);
+    else cbp_frame<float>(c, llr, &o, false, xhat, nullptr, nullptr, ins);
     return 0;
 }
 
@@ -787,13 +837,13 @@ int oracle_minsum_cbp_trace(const or_code* c, const float* llr, int32_t sweeps, 
 {
     if (!c || sweeps < 1) return 1;
     or_opts o = {sweeps, OR_STOP_NONE, OR_MINSUM, alpha};
+    std::vector<double> tmp((size_t)sweeps * c->E);
+    Instr ins;
+    ins.lam = tmp.data();
+    ins.per_sweep = true;
     std::vector<uint8_t> xhat;
-    for (int32_t s = 1; s <= sweeps; ++s) {       // prefix re-runs, as oracle_cbp_trace_f64
-        o.max_iter = s;
-        std::vector<float> tmp(c->E);
-        minsum_frame(c, llr, &o, xhat, nullptr, tmp.data());
-        std::copy(tmp.begin(), tmp.end(), lam + (int64_t)(s - 1) * c->E);
-    }
+    minsum_frame(c, llr, &o, xhat, nullptr, ins);
+    for (size_t k = 0; k < tmp.size(); ++k) lam[k] = (float)tmp[k];
     return 0;
 }
 

@@ -98,6 +98,18 @@ int oracle_lbp_trace_f64(const or_code* c, const float* llr, int32_t sweeps, dou
 int oracle_minsum_cbp_trace(const or_code* c, const float* llr, int32_t sweeps, float alpha, float* lam);
 int oracle_minsum_lbp_trace(const or_code* c, const float* llr, int32_t sweeps, float alpha, float* lam);
 
+/* Test-only hooks of the stop-rule pin (tests/test_oracle_stop.py).
+ * oracle_decode_window: oracle_decode of the CBP arithmetics (log-tanh fp32/fp64/literal, min-sum)
+ * with the belief window W of reading R4 replaced by `window` (> 0); no omega output.
+ * oracle_cbp_visit_trace: `sweeps` full sweeps without stopping (arith OR_FP32_CONTRACT, OR_FP64
+ * or OR_MINSUM); lam[s*E + e] = Lambda^new (equ_s4e20) and qn[s*E + e] = Q^new (equ_s4e19) of the
+ * visit of edge e = (c, v) in sweep s -- the raw trajectory, none of the stop logic. */
+int oracle_decode_window(const or_code* c, const float* llr, int64_t ld, int64_t frames, const or_opts* o,
+                         int64_t window, uint32_t* bits, int64_t ld_words, int32_t* iters, uint8_t* flags,
+                         int64_t* edge_visits, int32_t* fires);
+int oracle_cbp_visit_trace(const or_code* c, const float* llr, int32_t sweeps, int32_t arith, float alpha,
+                           double* lam, double* qn);
+
 /* brute-force maximum-likelihood codeword (K <= 20): argmax sum_v L_v (1 - 2 c_v) */
 int oracle_ml_decode(const or_code* c, const float* llr, uint32_t* cw);
 

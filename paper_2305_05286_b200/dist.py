@@ -23,8 +23,11 @@ def shard_range(frames: int, rank: int, world: int) -> tuple[int, int]:
 
 
 def allreduce_counts(counts: torch.Tensor, group=None) -> torch.Tensor:
-    """Sum the int64[8] counters over all ranks in place (one collective)."""
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    """Sum the int64[8] counters over all ranks in place (one collective).
+
+    The collective is issued whenever a process group exists -- at world size 1 too, so
+    every single-GPU bench run executes the NCCL all-reduce of the multi-GPU path."""
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
     return counts
 

@@ -10,6 +10,7 @@ import torch
 from .cbp import CBP_STOP_BELIEF_M, Code
 
 
+API_NAME = "pipeline.decode_host (chunked H2D -> cbp_decode -> D2H on 4 streams)"
 _CACHE: dict = {}
 
 

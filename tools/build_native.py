@@ -23,8 +23,9 @@ INPUTS_SRC = [ROOT / "inputs" / "qc_construct.c"]
 ORACLE_SRC = [ROOT / "oracle" / "cbp_oracle.cpp", ROOT / "oracle" / "contract32.c"]
 CBP_SRC = sorted((ROOT / "paper_2305_05286_b200" / "csrc").glob("*.cu")) + sorted(
     (ROOT / "paper_2305_05286_b200" / "csrc").glob("*.cpp"))
-CBP_HDR = sorted((ROOT / "paper_2305_05286_b200" / "csrc").glob("*.cuh")) + [ROOT / "include" / "cbp.h",
-                                                                            ROOT / "inputs" / "cbp_inputs.h"]
+# every file under csrc/ (kernels, host code, *.cuh and *.h headers) is a dependency of libcbp.so
+CBP_HDR = sorted(p for p in (ROOT / "paper_2305_05286_b200" / "csrc").iterdir() if p.is_file()) + [
+    ROOT / "include" / "cbp.h", ROOT / "inputs" / "cbp_inputs.h"]
 
 INPUTS_SO = ROOT / "inputs" / "libcbp_inputs.so"
 ORACLE_SO = ROOT / "oracle" / "liboracle.so"

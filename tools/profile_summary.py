@@ -1,6 +1,6 @@
 """Summarise one `ncu --set full` capture of cbp_kernel into profiles/.
 
-python tools/profile_summary.py gpurun_out/prof_a0_p1.ncu-rep <edge_visits> <prefix> "<what was captured>"
+python tools/profile_summary.py gpurun_out/prof_a0_p1.ncu-rep <edge_visits> <prefix> "<what was captured>" [frames]
 
 writes profiles/<prefix>_ncu_full_summary.txt (SOL / scheduler / pipe metrics,
 SASS opcode mix, stall reasons) and profiles/<prefix>_kernel_traffic.json (the
@@ -17,6 +17,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 rep, ev, prefix, what = sys.argv[1], float(sys.argv[2]), sys.argv[3], sys.argv[4]
+frames = int(float(sys.argv[5])) if len(sys.argv) > 5 else None
 
 
 def ncu(*args):
@@ -52,6 +53,7 @@ M = {
     "fma_pipe_pct": f("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
     "registers_per_thread": f("launch__registers_per_thread"),
     "edge_visits": ev,
+    "frames": frames,
 }
 M["lane_slots_per_edge_visit"] = M["inst_executed"] * 32 / ev if M["inst_executed"] else None
 stalls = {}
