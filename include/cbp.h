@@ -144,6 +144,27 @@ cbp_status cbp_decode_i8(const cbp_code* code, const int8_t* d_q, int64_t ld, fl
                          const cbp_opts* opts, uint32_t* d_bits, int64_t ld_words, int32_t* d_iters,
                          uint8_t* d_flags, float* d_omega, int64_t* d_ev, void* stream);
 
+/* Host-buffer decoding (SPEC.md decode_cbp: LLRs in, hard bits, iteration counts
+ * and flags out): the same results as cbp_decode / cbp_decode_i8 for caller-owned HOST buffers.
+ * The library splits the batch into chunks of `chunk_frames` frames (0 = 16384) and pipelines
+ * host->device copy, decode and device->host copy of each chunk round-robin over `nstreams`
+ * (0 = 4, at most 16) CUDA streams of its own, with device buffers from its memory pool, so the
+ * PCIe transfers overlap the kernels.  The call BLOCKS until every output is in host memory.
+ * Pinned (page-locked) host memory is strongly recommended: with pageable memory the copies
+ * are staged by the driver and do not overlap.
+ *   h_llr / h_q : host float[frames][ld] (ld >= N) / int8[frames][ld] (ld >= N, ld % 16 == 0)
+ *   h_bits      : host uint32[frames][ld_words] (ld_words >= ceil(N/32))
+ *   h_iters     : host int32[frames];   h_flags : host uint8[frames]
+ * Errors: CBP_E_INVALID as for cbp_decode (null buffers, sizes, options); CBP_E_NOMEM if a
+ * device buffer cannot be allocated; CBP_E_CUDA for copy / launch / synchronisation failures
+ * (the contents of the outputs are then unspecified). */
+cbp_status cbp_decode_host(const cbp_code* code, const float* h_llr, int64_t ld, int64_t frames, const cbp_opts* opts,
+                           uint32_t* h_bits, int64_t ld_words, int32_t* h_iters, uint8_t* h_flags,
+                           int64_t chunk_frames, int32_t nstreams);
+cbp_status cbp_decode_host_i8(const cbp_code* code, const int8_t* h_q, int64_t ld, float scale, int64_t frames,
+                              const cbp_opts* opts, uint32_t* h_bits, int64_t ld_words, int32_t* h_iters,
+                              uint8_t* h_flags, int64_t chunk_frames, int32_t nstreams);
+
 /* ---------------------------------------------------------------- channel */
 
 /* llr_mode flags of cbp_channel / cbp_ber_sim (OR-ed; 0..3 valid). */
@@ -201,13 +222,13 @@ cbp_status cbp_get_launch_info(const cbp_code* code, cbp_launch_info* out);
 
 /* Element-wise evaluation of the fp32 arithmetic contract on the device
  * for the bit-equality pins: fn 0 phi32(x), 1 ln32(x),
- * 2 / 3 sin / cos(2 pi m 2^-24) with m = the low 24 bits of x's bit pattern,
- * 4 the clamped reference formula phi_v1(x) the v2 table interpolates.
+ * 2 / 3 sin / cos(2 pi m 2^-24) with m = the low 24 bits of x's bit pattern.
  * d_x, d_y: device float[n] on `device`. */
 cbp_status cbp_eval_contract(int32_t fn, const float* d_x, float* d_y, int64_t n, int32_t device, void* stream);
 
-/* Copy the phi contract v2 table of `device` (929 segments x {c0, c1, c2, c3},
- * DESIGN.md §3, built on the device at first use) into d_out (device float[3716]). */
+/* Copy the phi contract v3 table of `device` (1153 segments x {c0, c1, c2, c3} in the
+ * kernel's storage form; built on the host and uploaded at first use) into
+ * d_out (device float[4612]). */
 cbp_status cbp_phi_table(int32_t device, float* d_out, void* stream);
 
 #ifdef __cplusplus

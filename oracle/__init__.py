@@ -60,9 +60,8 @@ def _lib():
             "oracle_ln32": ([_f32], _f32),
             "oracle_sincos_quarter32": ([ctypes.c_uint32, _p, _p], None),
             "oracle_phi32_n": ([_p, _p, _i64], None),
-            "oracle_phi32_v1": ([_f32], _f32),
             "oracle_phi32_table": ([_p], None),
-            "oracle_phi32_clamp_check": ([_p, _p, _p], None),
+            "oracle_phi32_exhaustive": ([_p, _p, _p, _p], None),
             "oracle_ln32_n": ([_p, _p, _i64], None),
         }
         for name, (args, res) in sig.items():
@@ -252,19 +251,19 @@ def ln32_array(x: np.ndarray) -> np.ndarray:
     return y
 
 
-def phi32_v1(x: float) -> float:
-    return float(_lib().oracle_phi32_v1(x))
+PHI_SEGS = 1153
 
 
-def phi32_clamp_check():
-    """(#below PHI_LO, #above PHI_HI, max) of the unclamped v2 cubic over every float in [PHI_LO, 30]."""
-    b, a, m = _i64(), _i64(), _f32()
-    _lib().oracle_phi32_clamp_check(ctypes.byref(b), ctypes.byref(a), ctypes.byref(m))
-    return b.value, a.value, m.value
+def phi32_exhaustive():
+    """(#below PHI_LO, #above PHI_HI, max ulp, argmax) of the unclamped v3 cubic over every
+    binary32 x in [PHI_LO, 30], error against the double phi."""
+    b, a, m, at = _i64(), _i64(), _f64(), _f32()
+    _lib().oracle_phi32_exhaustive(ctypes.byref(b), ctypes.byref(a), ctypes.byref(m), ctypes.byref(at))
+    return b.value, a.value, m.value, at.value
 
 
 def phi32_table() -> np.ndarray:
-    t = np.zeros((929, 4), np.float32)
+    t = np.zeros((PHI_SEGS, 4), np.float32)
     _lib().oracle_phi32_table(_ptr(t))
     return t
 

@@ -115,9 +115,9 @@ int oracle_ml_decode(const or_code* c, const float* llr, uint32_t* cw);
 
 /* contract functions re-exported for the pin tests */
 float oracle_phi32(float x);
-float oracle_phi32_v1(float x);
-void  oracle_phi32_table(float* out);    /* 929 x 4 floats */
-void  oracle_phi32_clamp_check(int64_t* below, int64_t* above, float* maxp);
+void  oracle_phi32_table(float* out);    /* 1153 x 4 floats */
+/* every binary32 x in [PHI_LO, PHI_HI]: unclamped cubic below / above the bounds, max ulp error */
+void  oracle_phi32_exhaustive(int64_t* below, int64_t* above, double* max_ulp, float* at);
 float oracle_ln32(float x);
 void  oracle_sincos_quarter32(uint32_t m24, float* s, float* c);
 /* element-wise over arrays (pin tests) */

@@ -21,10 +21,9 @@ extern "C" {
 #define OR_PHI_LO 0x1.a56e0cp-43f
 
 float oracle_ln32(float x);              /* natural log, x normal and > 0          */
-float oracle_phi32(float x);             /* phi contract v2 (table-driven cubic)   */
-float oracle_phi32_v1(float x);          /* phi reference formula v1 (clamped)     */
-void  oracle_phi32_table(float* out);    /* the 929 x 4 v2 coefficients            */
-void  oracle_phi32_clamp_check(int64_t* below, int64_t* above, float* maxp);
+float oracle_phi32(float x);             /* phi contract v3 (table-driven cubic)   */
+void  oracle_phi32_table(float* out);    /* the 1153 x 4 v3 coefficients           */
+void  oracle_phi32_exhaustive(int64_t* below, int64_t* above, double* max_ulp, float* at);
 void  oracle_sincos_quarter32(uint32_t m24, float* s, float* c); /* sin/cos(2*pi*m24*2^-24) */
 
 #ifdef __cplusplus

@@ -42,6 +42,7 @@ CBP_ALG_LOG_TANH, CBP_ALG_MIN_SUM, CBP_ALG_LBP, CBP_ALG_FBP = 0, 1, 2, 3
 # llr_mode flags of channel / ber_sim (include/cbp.h): int8 stream, all-zero codeword (reading R23)
 CBP_LLR_INT8, CBP_TX_ZERO = 1, 2
 ALPHA_DEFAULT = 0.75
+PHI_SEGS = 1153        # segments of the phi contract v3 table (include/cbp.h, cbp_phi_table)
 
 
 def _opts(max_iter, stop_rule, algorithm, alpha):
@@ -67,6 +68,8 @@ SIGNATURES = {
     "cbp_code_dims": ([_p, _p, _p, _p, _p], _i32),
     "cbp_decode": ([_p, _p, _i64, _i64, _p, _p, _i64, _p, _p, _p, _p, _p], _i32),
     "cbp_decode_i8": ([_p, _p, _i64, _f32, _i64, _p, _p, _i64, _p, _p, _p, _p, _p], _i32),
+    "cbp_decode_host": ([_p, _p, _i64, _i64, _p, _p, _i64, _p, _p, _i64, _i32], _i32),
+    "cbp_decode_host_i8": ([_p, _p, _i64, _f32, _i64, _p, _p, _i64, _p, _p, _i64, _i32], _i32),
     "cbp_channel": ([_p, _f64, _u64, _i64, _i64, _i32, _p, _i64, _p, _i64, _p], _i32),
     "cbp_ber_sim": ([_p, _f64, _u64, _i64, _i64, _p, _i32, _p, _p], _i32),
     "cbp_get_launch_info": ([_p, _p], _i32),
@@ -169,12 +172,26 @@ class Code:
             out["ev"] = torch.empty(frames, dtype=torch.int64, device=d)
         return out
 
+    def _check_out(self, out: dict, frames: int, who: str):
+        """The C ABI cannot see buffer sizes: every output must hold `frames` rows (omega [frames, M])."""
+        rows = {"bits": 2, "iters": 1, "flags": 1, "omega": 2, "ev": 1}
+        for k, t in out.items():
+            if k not in rows or t is None:
+                continue
+            if t.dim() != rows[k] or t.shape[0] < frames:
+                raise CbpError(f"{who}: out[{k!r}] must be {rows[k]}-D with >= {frames} rows, got {tuple(t.shape)}")
+        if out["bits"].shape[1] < self.words:
+            raise CbpError(f"{who}: out['bits'] needs >= {self.words} words per frame")
+        if out.get("omega") is not None and out["omega"].shape[1] != self.M:
+            raise CbpError(f"{who}: out['omega'] must be [frames, M={self.M}]")
+
     def decode(self, llr: torch.Tensor, max_iter: int, stop_rule: int = CBP_STOP_BELIEF_M, out: dict | None = None,
                omega: bool = False, ev: bool = False, stream=None, algorithm: int = CBP_ALG_LOG_TANH,
                alpha: float = ALPHA_DEFAULT) -> dict:
         """cbp_decode: llr float32 [frames, ld] on the code's device (ld >= N, ld % 4 == 0)."""
         frames, ld = llr.shape
         out = out if out is not None else self.alloc_outputs(frames, omega, ev)
+        self._check_out(out, frames, "decode")
         o = _opts(max_iter, stop_rule, algorithm, alpha)
         d = self.device
         rc = lib().cbp_decode(self._h, _dptr(llr, torch.float32, d, "llr"), ld, frames, ctypes.byref(o),
@@ -191,6 +208,7 @@ class Code:
         """cbp_decode_i8: q int8 [frames, ld] (ld % 16 == 0), L = scale * q."""
         frames, ld = q.shape
         out = out if out is not None else self.alloc_outputs(frames, omega, ev)
+        self._check_out(out, frames, "decode_i8")
         o = _opts(max_iter, stop_rule, algorithm, alpha)
         d = self.device
         rc = lib().cbp_decode_i8(self._h, _dptr(q, torch.int8, d, "q"), ld, scale, frames, ctypes.byref(o),
@@ -200,6 +218,45 @@ class Code:
                                  _dptr(out.get("omega"), torch.float32, d, "omega"),
                                  _dptr(out.get("ev"), torch.int64, d, "ev"), _stream(stream))
         _check(rc, "cbp_decode_i8")
+        return out
+
+    # -------------------------------------------------------------- host buffers
+    def alloc_host_outputs(self, frames: int) -> dict:
+        """pinned host outputs of decode_host"""
+        return {"bits": torch.empty((frames, self.words), dtype=torch.int32, pin_memory=True),
+                "iters": torch.empty(frames, dtype=torch.int32, pin_memory=True),
+                "flags": torch.empty(frames, dtype=torch.uint8, pin_memory=True)}
+
+    def decode_host(self, llr: torch.Tensor, max_iter: int, stop_rule: int = CBP_STOP_BELIEF_M,
+                    out: dict | None = None, scale: float | None = None, chunk_frames: int = 0, nstreams: int = 0,
+                    algorithm: int = CBP_ALG_LOG_TANH, alpha: float = ALPHA_DEFAULT) -> dict:
+        """cbp_decode_host / cbp_decode_host_i8: host (pinned) float32 [frames, ld] LLRs, or int8
+        [frames, ld] with `scale`, -> host outputs; blocks until the outputs are in host memory."""
+        if llr.is_cuda or llr.dim() != 2 or not llr.is_contiguous():
+            raise CbpError("decode_host: llr must be a contiguous 2-D host tensor")
+        frames, ld = llr.shape
+        out = out if out is not None else self.alloc_host_outputs(frames)
+        for k, dt in (("bits", torch.int32), ("iters", torch.int32), ("flags", torch.uint8)):
+            t = out[k]
+            if t.is_cuda or t.dtype != dt or not t.is_contiguous() or t.shape[0] < frames:
+                raise CbpError(f"decode_host: out[{k!r}] must be a contiguous host {dt} tensor with >= {frames} rows")
+        if out["bits"].dim() != 2 or out["bits"].shape[1] < self.words:
+            raise CbpError(f"decode_host: out['bits'] needs >= {self.words} words per frame")
+        o = _opts(max_iter, stop_rule, algorithm, alpha)
+        if llr.dtype == torch.int8:
+            if scale is None:
+                raise CbpError("decode_host: int8 LLRs need `scale`")
+            rc = lib().cbp_decode_host_i8(self._h, llr.data_ptr(), ld, float(scale), frames, ctypes.byref(o),
+                                          out["bits"].data_ptr(), out["bits"].shape[1], out["iters"].data_ptr(),
+                                          out["flags"].data_ptr(), chunk_frames, nstreams)
+            _check(rc, "cbp_decode_host_i8")
+        elif llr.dtype == torch.float32:
+            rc = lib().cbp_decode_host(self._h, llr.data_ptr(), ld, frames, ctypes.byref(o), out["bits"].data_ptr(),
+                                       out["bits"].shape[1], out["iters"].data_ptr(), out["flags"].data_ptr(),
+                                       chunk_frames, nstreams)
+            _check(rc, "cbp_decode_host")
+        else:
+            raise CbpError("decode_host: llr must be float32 or int8")
         return out
 
     # -------------------------------------------------------------- channel / ber
@@ -222,6 +279,8 @@ class Code:
         """cbp_ber_sim: accumulates into `counts` (int64 [8] on device; zeroed if not given)."""
         if counts is None:
             counts = torch.zeros(8, dtype=torch.int64, device=self.device)
+        if counts.numel() != 8:
+            raise CbpError("ber_sim: counts must hold the 8 int64 counters of cbp_counts")
         o = _opts(max_iter, stop_rule, algorithm, alpha)
         rc = lib().cbp_ber_sim(self._h, float(ebn0_db), seed, frame_begin, frames, ctypes.byref(o), llr_mode,
                                _dptr(counts, torch.int64, self.device, "counts"), _stream(stream))
@@ -238,8 +297,8 @@ def eval_contract(fn: int, x: torch.Tensor, stream=None) -> torch.Tensor:
 
 
 def phi_table(device: int = 0, stream=None) -> torch.Tensor:
-    """cbp_phi_table: the device's phi contract v2 table, float32 [929, 4] (on the device)."""
-    out = torch.empty((929, 4), dtype=torch.float32, device=torch.device("cuda", device))
+    """cbp_phi_table: the device's phi contract v3 table, float32 [PHI_SEGS, 4] (on the device)."""
+    out = torch.empty((PHI_SEGS, 4), dtype=torch.float32, device=torch.device("cuda", device))
     _check(lib().cbp_phi_table(device, out.data_ptr(), _stream(stream)), "cbp_phi_table")
     return out
 

@@ -46,7 +46,37 @@ struct DeviceGuard {
     }
 };
 
-// phi contract v2 table, built once per device by phi_table_kernel
+// phi contract v3 table, device storage form: segment seg holds the cubic
+// through phi at u = 0, 1/4, 3/4, 1 of its interval, phi(x) = -log(tanh(x/2))
+// evaluated in IEEE double as log1p(2 / expm1(x)) (no cancellation of tanh -> 1); Newton divided
+// differences in double in the contract's order, coefficients rounded to binary32; the x < 2
+// rows scaled for the kernel's local variable u/16 (c1 x 16, c2 x 256, c3 x 4096, exact).
+//   seg < 704:  x(u) = 2^e (1 + (j + u)/16), e = -43 + seg/16, j = seg % 16
+//   seg >= 704: x(u) = 2 + (seg - 704 + u)/16
+void build_phi_rows(float4* rows)
+{
+    static const int kQ4[4] = {0, 1, 3, 4};
+    for (int seg = 0; seg < cbp::kPhiTableSegs; ++seg) {
+        double f[4];
+        for (int k = 0; k < 4; ++k) {
+            const float x = (seg < 704) ? std::ldexp(static_cast<float>(64 + 4 * (seg % 16) + kQ4[k]), -43 + seg / 16 - 6)
+                                        : static_cast<float>(128 + 4 * (seg - 704) + kQ4[k]) * 0.015625f;
+            f[k] = std::log1p(2.0 / std::expm1(static_cast<double>(x)));
+        }
+        const double d01 = (f[1] - f[0]) * 4.0, d12 = (f[2] - f[1]) * 2.0, d23 = (f[3] - f[2]) * 4.0;
+        const double d012 = ((d12 - d01) * 4.0) / 3.0, d123 = ((d23 - d12) * 4.0) / 3.0;
+        const double d0123 = d123 - d012;
+        float4 c = make_float4(static_cast<float>(f[0]), static_cast<float>((d01 - d012 * 0.25) + d0123 * 0.1875),
+                               static_cast<float>(d012 - d0123), static_cast<float>(d0123));
+        if (seg < 704) {
+            c.y *= 16.0f;
+            c.z *= 256.0f;
+            c.w *= 4096.0f;
+        }
+        rows[seg] = c;
+    }
+}
+
 std::mutex g_tab_mu;
 float4* g_tab[128] = {};
 cudaTextureObject_t g_tex[128] = {};   // texture objects over g_tab (TEX-pipe lookups)
@@ -61,12 +91,10 @@ const float4* phi_table(int device, std::string* err, cudaTextureObject_t* tex =
     }
     DeviceGuard g(device);
     float4* p = nullptr;
-    cudaStream_t st = nullptr;
+    std::vector<float4> rows(cbp::kPhiTableSegs);
+    build_phi_rows(rows.data());
     cudaError_t e = cudaMalloc(&p, sizeof(float4) * cbp::kPhiTableSegs);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = static_cast<cudaError_t>(cbp::launch_phi_table(p, st));
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (st) cudaStreamDestroy(st);
+    if (e == cudaSuccess) e = cudaMemcpy(p, rows.data(), sizeof(float4) * cbp::kPhiTableSegs, cudaMemcpyHostToDevice);
     cudaTextureObject_t t = 0;
     if (e == cudaSuccess) {
         cudaResourceDesc rd{};
@@ -130,6 +158,14 @@ struct cbp_code {
     cudaTextureObject_t phi_tex = 0;   // per-device texture object over phi_tab, not owned
     cbp::Geometry geo[4]{};           // per cbp_algorithm
     int ctas_per_sm[4] = {1, 1, 1, 1}, num_sms = 1;
+    cbp::Geometry geo_chan{};          // cbp_channel: cbp_kernel (the warp kernel has no channel-only mode)
+    int ctas_chan = 1;
+    int4* ent_dev[4] = {};             // device copies of ent[] (bulk-copied by cbp_warp_kernel)
+    ~cbp_code()
+    {
+        for (int4* p : ent_dev)
+            if (p) cudaFree(p);
+    }
 };
 
 extern "C" {
@@ -231,6 +267,12 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
                 // kp: position of prev(b) among its row's entries = the variable's edge index inside
                 // the previous check (min-sum minimum owner, reading R20)
                 const int kp = p - row_ptr[ent_row[p]];
+                if (alg == 0 || alg == 2) {
+                    // producer-side layout (CBP log-tanh, layered BP): variable block and rotation only
+                    ent[2 * b] = make_int4(QS * j * Z, QS * ent_s[b], 0, 0);
+                    ent[2 * b + 1] = make_int4(0, 0, ent_s[b] << 16, 0);
+                    continue;
+                }
                 ent[2 * b] = make_int4(QS * j * Z, S0 + SU * RS * ent_row[p] * Z, R0 + RS * p * Z, QS * ent_s[b]);
                 ent[2 * b + 1] = make_int4(RS * ds, first ? 0 : -1, first | (kp << 8) | (ent_s[b] << 16), R0 + RS * b * Z);
             }
@@ -301,10 +343,46 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
     const int split_env = (sr && (sr[0] == '0' || sr[0] == '1') && sr[1] == 0) ? sr[0] - '0' : -1;
     // geometry with P frames per lane; G.teams == 0 if it does not apply
     static const int multi_maxt_env = [] { const char* e = std::getenv("CBP_MULTI_MAXT"); return e ? std::atoi(e) : 0; }();
-    auto make_geo = [&](int alg, int P, bool split_r, int multi_maxt = 512) {
+    const char* wv = std::getenv("CBP_WARP_KERNEL");     // 0: cbp_kernel only (A/B runs)
+    // (CBP_GLOBAL_TEAMS forces cbp_kernel's global-state path and so disables the warp kernel too)
+    const bool use_warp = !(wv && wv[0] == '0' && wv[1] == 0) && !std::getenv("CBP_GLOBAL_TEAMS");
+    const int split_r_env = split_env;
+    auto make_geo = [&](int alg, int P, bool split_r, int multi_maxt = 512, bool allow_warp = true) {
         cbp::Geometry G{};
         G.alg = alg;
         G.P = P;
+        if (use_warp && allow_warp && (alg == 0 || alg == 2) && P == 1 && Z >= 17 && Z <= 128) {
+            // cbp_warp_kernel: one frame per warp, K = ceil(Z/32) check slots per lane
+            G.wk = 1;
+            G.kslots = (Z + 31) / 32;
+            G.lanes = (Z + G.kslots - 1) / G.kslots;
+            G.multi = 0; G.F = 1; G.Zp = 32; G.team_threads = 32; G.state_in_smem = 1;
+            const int maxt = G.kslots == 1 ? 512 : 384;
+            const int64_t rw = static_cast<int64_t>(nent) * G.kslots * 32;
+            G.table_words = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4 + 4;
+            auto per_warp = [&](bool rg) {   // counters (8 x u64) | QP [2N] | S [M] | cw | R
+                return (16 + 2LL * c->N + c->M + (nwords + 3) / 4 * 4 + (rg ? 0 : rw) + 3) / 4 * 4;
+            };
+            auto warps_of = [&](bool rg) {
+                const int64_t w = (smem_optin - 4LL * G.table_words) / (4 * per_warp(rg));
+                return static_cast<int>(std::min<int64_t>(w, maxt / 32));
+            };
+            const int ws = warps_of(false), wg = warps_of(true);
+            // R in global memory (coalesced, L1/L2-served) when shared memory holds fewer than 8 frames
+            bool rg = ws < 8 && wg > ws;
+            if (split_r_env == 0) rg = false;
+            if (split_r_env == 1) rg = true;
+            G.r_global = rg ? 1 : 0;
+            G.r_words = rg ? static_cast<int32_t>(rw) : 0;
+            G.slot_words = static_cast<int32_t>(per_warp(rg));
+            G.teams = rg ? wg : ws;
+            if (G.teams < 1) { G.wk = 0; G.teams = 0; }
+            else {
+                G.threads = 32 * G.teams;
+                G.smem_bytes = static_cast<int32_t>(4LL * G.table_words + 4LL * G.teams * G.slot_words);
+                return G;
+            }
+        }
         if (Z <= 16) {
             int zp = 1;
             while (zp < Z) zp <<= 1;
@@ -418,6 +496,26 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         }
         c->ctas_per_sm[alg] = G.state_in_smem ? occ : 1;
         c->ent[alg] = make_ent(G.P, alg, G.r_global != 0);
+        const size_t eb = sizeof(int4) * c->ent[alg].size();
+        if (cudaMalloc(&c->ent_dev[alg], eb) != cudaSuccess ||
+            cudaMemcpy(c->ent_dev[alg], c->ent[alg].data(), eb, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaGetLastError();
+            cbp_code_destroy(c);
+            return fail(CBP_E_NOMEM, "cbp_code_create: schedule table upload failed");
+        }
+    }
+    // cbp_channel (no decoding) runs on cbp_kernel with the log-tanh entries
+    c->geo_chan = c->geo[0];
+    c->ctas_chan = c->ctas_per_sm[0];
+    if (c->geo[0].wk) {
+        c->geo_chan = make_geo(0, 1, false, 512, false);
+        int occ = 0;
+        if (cbp::occupancy_ctas_per_sm(c->geo_chan, &occ) != 0 || occ < 1) {
+            cudaGetLastError();
+            cbp_code_destroy(c);
+            return fail(CBP_E_UNSUPPORTED, "cbp_code_create: channel kernel does not fit on this device");
+        }
+        c->ctas_chan = c->geo_chan.state_in_smem ? occ : 1;
     }
     *out = c;
     return CBP_OK;
@@ -452,17 +550,19 @@ cbp_status cbp_get_launch_info(const cbp_code* c, cbp_launch_info* o)
 
 namespace {
 
-cbp::KernelArgs base_args(const cbp_code* c, int alg = 0)
+cbp::KernelArgs base_args(const cbp_code* c, int alg = 0, bool chan = false)
 {
     cbp::KernelArgs a{};
     cbp::DevCode& d = a.code;
-    const cbp::Geometry& G = c->geo[alg];
+    const cbp::Geometry& G = chan ? c->geo_chan : c->geo[alg];
     d.N = c->N; d.K = c->K; d.M = c->M; d.Z = c->Z; d.mb = c->mb; d.nb = c->nb; d.kb = c->kb; d.core = c->core;
     d.nent = c->nent; d.E = static_cast<int32_t>(c->E); d.nwords = (c->N + 31) / 32; d.kwords = (c->K + 31) / 32;
     d.max_dc = c->max_dc; d.can_encode = c->can_encode; d.mid = c->mid;
     d.phi_tab = c->phi_tab;
     d.phi_tex = static_cast<unsigned long long>(c->phi_tex);
     std::memcpy(a.ent, c->ent[alg].data(), sizeof(int4) * c->ent[alg].size());
+    a.ent_dev = c->ent_dev[alg];
+    a.lanes = G.lanes;
     std::memcpy(a.row_ptr, c->row_ptr.data(), sizeof(int32_t) * c->row_ptr.size());
     std::memcpy(a.pshift, c->pshift.data(), sizeof(int16_t) * c->pshift.size());
     a.Zp = G.Zp; a.F = G.F; a.slot_words = G.slot_words; a.table_words = G.table_words;
@@ -499,11 +599,13 @@ cbp_status run(const cbp_code* c, cbp::KernelArgs& a, int64_t frames, void* stre
     DeviceGuard g(c->device);
     if (!g.ok) return fail(CBP_E_CUDA, std::string(who) + ": cudaSetDevice failed");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const cbp::Geometry& G = c->geo[a.algorithm];
+    const bool chan = a.mode == cbp::MODE_CHANNEL;
+    const cbp::Geometry& G = chan ? c->geo_chan : c->geo[a.algorithm];
     const int64_t per_cta = static_cast<int64_t>(G.F) * G.teams * G.P;
     const int64_t ctas_needed = (frames + per_cta - 1) / per_cta;
     const int grid = static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>(static_cast<int64_t>(c->num_sms) * c->ctas_per_sm[a.algorithm], ctas_needed)));
+        1, std::min<int64_t>(static_cast<int64_t>(c->num_sms) * (chan ? c->ctas_chan : c->ctas_per_sm[a.algorithm]),
+                             ctas_needed)));
     cudaError_t e;
     unsigned long long* q = nullptr;
     cudaMemPool_t pool = work_pool(c->device);
@@ -578,9 +680,97 @@ cbp_status decode_common(const cbp_code* c, const void* in, int32_t mode, int64_
     return run(c, a, frames, stream, who);
 }
 
+// Host-buffer decode (include/cbp.h cbp_decode_host): chunks of `chunk` frames round-robin over
+// `ns` streams, each chunk H2D -> decode kernel -> D2H on its stream (stream order makes the reuse
+// of a stream's device buffers safe); blocks until all streams are done.
+cbp_status decode_host_common(const cbp_code* c, const void* h_in, int32_t mode, int64_t ld, float scale,
+                              int64_t frames, const cbp_opts* opts, uint32_t* h_bits, int64_t ld_words,
+                              int32_t* h_iters, uint8_t* h_flags, int64_t chunk, int32_t ns, const char* who)
+{
+    if (!c) return fail(CBP_E_INVALID, std::string(who) + ": null code");
+    cbp_status s = check_opts(c, opts);
+    if (s != CBP_OK) return s;
+    if (frames < 0) return fail(CBP_E_INVALID, std::string(who) + ": frames < 0");
+    if (chunk < 0 || ns < 0 || ns > 16) return fail(CBP_E_INVALID, std::string(who) + ": need chunk_frames >= 0, 0 <= nstreams <= 16");
+    if (frames == 0) return CBP_OK;
+    if (!h_in || !h_bits || !h_iters || !h_flags) return fail(CBP_E_INVALID, std::string(who) + ": null buffer");
+    const int64_t esz = (mode == cbp::MODE_DECODE_I8) ? 1 : 4;
+    if (ld < c->N || (ld * esz) % 16 != 0) return fail(CBP_E_INVALID, std::string(who) + ": need ld >= N and ld*elem % 16 == 0");
+    if (ld_words < (c->N + 31) / 32) return fail(CBP_E_INVALID, std::string(who) + ": ld_words < ceil(N/32)");
+    if (mode == cbp::MODE_DECODE_I8 && !(std::isfinite(scale) && scale > 0.0f))
+        return fail(CBP_E_INVALID, std::string(who) + ": scale must be finite and > 0");
+    if (chunk == 0) chunk = 1 << 14;
+    if (ns == 0) ns = 4;
+    chunk = std::min(chunk, frames);
+    const int64_t nchunks = (frames + chunk - 1) / chunk;
+    ns = static_cast<int32_t>(std::min<int64_t>(ns, nchunks));
+    DeviceGuard g(c->device);
+    if (!g.ok) return fail(CBP_E_CUDA, std::string(who) + ": cudaSetDevice failed");
+    cudaMemPool_t pool = work_pool(c->device);
+    struct Slot {
+        cudaStream_t st = nullptr;
+        void* in = nullptr;
+        uint32_t* bits = nullptr;
+        int32_t* iters = nullptr;
+        uint8_t* flags = nullptr;
+    };
+    std::vector<Slot> slots(ns);
+    cudaError_t e = cudaSuccess;
+    auto alloc = [&](void** p, size_t bytes, cudaStream_t st) {
+        return pool ? cudaMallocFromPoolAsync(p, bytes, pool, st) : cudaMallocAsync(p, bytes, st);
+    };
+    for (auto& sl : slots) {
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = alloc(&sl.in, static_cast<size_t>(chunk * ld * esz), sl.st);
+        if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&sl.bits), static_cast<size_t>(chunk * ld_words * 4), sl.st);
+        if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&sl.iters), static_cast<size_t>(chunk * 4), sl.st);
+        if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&sl.flags), static_cast<size_t>((chunk + 15) / 16 * 16), sl.st);
+    }
+    cbp_status rs = (e == cudaSuccess) ? CBP_OK : fail(CBP_E_NOMEM, std::string(who) + ": " + cudaGetErrorString(e));
+    const char* src = static_cast<const char*>(h_in);
+    for (int64_t k = 0; k < nchunks && rs == CBP_OK; ++k) {
+        Slot& sl = slots[k % ns];
+        const int64_t b = k * chunk, n = std::min(chunk, frames - b);
+        e = cudaMemcpyAsync(sl.in, src + b * ld * esz, static_cast<size_t>(n * ld * esz), cudaMemcpyHostToDevice, sl.st);
+        if (e != cudaSuccess) { rs = cuda_fail(e, who); break; }
+        rs = decode_common(c, sl.in, mode, ld, scale, n, opts, sl.bits, ld_words, sl.iters, sl.flags, nullptr, nullptr,
+                           sl.st, who);
+        if (rs != CBP_OK) break;
+        e = cudaMemcpyAsync(h_bits + b * ld_words, sl.bits, static_cast<size_t>(n * ld_words * 4), cudaMemcpyDeviceToHost, sl.st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h_iters + b, sl.iters, static_cast<size_t>(n * 4), cudaMemcpyDeviceToHost, sl.st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h_flags + b, sl.flags, static_cast<size_t>(n), cudaMemcpyDeviceToHost, sl.st);
+        if (e != cudaSuccess) rs = cuda_fail(e, who);
+    }
+    for (auto& sl : slots) {
+        if (!sl.st) continue;
+        for (void* p : {sl.in, static_cast<void*>(sl.bits), static_cast<void*>(sl.iters), static_cast<void*>(sl.flags)})
+            if (p) cudaFreeAsync(p, sl.st);
+        const cudaError_t se = cudaStreamSynchronize(sl.st);
+        if (se != cudaSuccess && rs == CBP_OK) rs = cuda_fail(se, who);
+        cudaStreamDestroy(sl.st);
+    }
+    return rs;
+}
+
 }  // namespace
 
 extern "C" {
+
+cbp_status cbp_decode_host(const cbp_code* c, const float* h_llr, int64_t ld, int64_t frames, const cbp_opts* opts,
+                           uint32_t* h_bits, int64_t ld_words, int32_t* h_iters, uint8_t* h_flags,
+                           int64_t chunk_frames, int32_t nstreams)
+{
+    return decode_host_common(c, h_llr, cbp::MODE_DECODE_F32, ld, 1.0f, frames, opts, h_bits, ld_words, h_iters,
+                              h_flags, chunk_frames, nstreams, "cbp_decode_host");
+}
+
+cbp_status cbp_decode_host_i8(const cbp_code* c, const int8_t* h_q, int64_t ld, float scale, int64_t frames,
+                              const cbp_opts* opts, uint32_t* h_bits, int64_t ld_words, int32_t* h_iters,
+                              uint8_t* h_flags, int64_t chunk_frames, int32_t nstreams)
+{
+    return decode_host_common(c, h_q, cbp::MODE_DECODE_I8, ld, scale, frames, opts, h_bits, ld_words, h_iters,
+                              h_flags, chunk_frames, nstreams, "cbp_decode_host_i8");
+}
 
 cbp_status cbp_decode(const cbp_code* c, const float* d_llr, int64_t ld, int64_t frames, const cbp_opts* opts,
                       uint32_t* d_bits, int64_t ld_words, int32_t* d_iters, uint8_t* d_flags, float* d_omega,
@@ -611,7 +801,7 @@ cbp_status cbp_channel(const cbp_code* c, double ebn0_db, uint64_t seed, int64_t
     if (!d_llr && !d_cw) return fail(CBP_E_INVALID, "cbp_channel: both outputs NULL");
     if (d_llr && ld < c->N) return fail(CBP_E_INVALID, "cbp_channel: ld < N");
     if (d_cw && ld_words < (c->N + 31) / 32) return fail(CBP_E_INVALID, "cbp_channel: ld_words < ceil(N/32)");
-    cbp::KernelArgs a = base_args(c);
+    cbp::KernelArgs a = base_args(c, 0, true);
     a.mode = cbp::MODE_CHANNEL;
     a.frames = frames;
     a.frame_begin = frame_begin;
@@ -655,7 +845,7 @@ cbp_status cbp_ber_sim(const cbp_code* c, double ebn0_db, uint64_t seed, int64_t
 
 cbp_status cbp_eval_contract(int32_t fn, const float* d_x, float* d_y, int64_t n, int32_t device, void* stream)
 {
-    if (fn < 0 || fn > 4) return fail(CBP_E_INVALID, "cbp_eval_contract: fn must be 0..4");
+    if (fn < 0 || fn > 3) return fail(CBP_E_INVALID, "cbp_eval_contract: fn must be 0..3");
     if (n < 0 || (n > 0 && (!d_x || !d_y))) return fail(CBP_E_INVALID, "cbp_eval_contract: bad buffers");
     DeviceGuard g(device);
     if (!g.ok) return fail(CBP_E_CUDA, "cbp_eval_contract: cudaSetDevice failed");

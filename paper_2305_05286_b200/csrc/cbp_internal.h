@@ -12,7 +12,7 @@ struct DevCode {
     int32_t max_dc;
     int32_t can_encode;
     int32_t mid;           // floor(core/2)
-    const float4* phi_tab; // [929] phi contract v2 coefficients
+    const float4* phi_tab; // [kPhiTableSegs] phi contract v3 coefficients
     unsigned long long phi_tex;   // cudaTextureObject_t over phi_tab (float4 elements)
 };
 
@@ -58,6 +58,8 @@ struct KernelArgs {
     int32_t ctl_words;     // shared control words per team (multi-warp teams; warp teams: syndrome scratch)
     int32_t fast_syn;      // warp teams with Z <= 32 and mb <= Zp: ballot-packed syndromes
     uint32_t phi_m19, phi_one;     // 0x7ffff, 0x3f800000 (phi local variable, runtime operands)
+    const int4* ent_dev;   // device copy of `ent` (bulk-copied into shared memory by cbp_warp_kernel)
+    int32_t lanes;         // cbp_warp_kernel: lanes with check slots, L = ceil(Z / K)
     float* gstate;         // per-CTA global state (state_in_smem == 0)
     float* rstate;         // per-group R sections of the split layout (r_global), r_words each
     int32_t r_words;
@@ -76,7 +78,9 @@ struct KernelArgs {
 #define CBP_WARP_MAXT 512
 #endif
 
-constexpr int kCtlTeamWords = 136;  // shared control words per multi-warp team: 2 x P(2) x 32 ballots + broadcast
+// shared control words per multi-warp team: row reduction [2 buffers][P <= 2][first 32 | last 32 per warp]
+// + the queue-index broadcast (2 x int64)
+constexpr int kCtlTeamWords = 264;
 
 struct Geometry {
     int32_t threads, F, Zp, slot_words, table_words, smem_bytes, state_in_smem, multi;
@@ -85,13 +89,14 @@ struct Geometry {
     int32_t P;                     // frames per lane (1 or 2), interleaved in a group
     int32_t ctl_words, fast_syn;   // see KernelArgs
     int32_t r_global, r_words;     // split layout: R in the global workspace, r_words per group
+    int32_t wk;                    // 1: cbp_warp_kernel (one frame per warp, K check slots per lane)
+    int32_t kslots, lanes;         // cbp_warp_kernel: K and L = ceil(Z / K)
 };
 
 // launch (cbp_kernels.cu); returns cudaError_t as int
 int launch_cbp(const KernelArgs& a, const Geometry& g, int grid, void* stream);
 int occupancy_ctas_per_sm(const Geometry& g, int* out);
 int launch_contract_eval(int fn, const float* x, float* y, int64_t n, const float4* tab, void* stream);
-int launch_phi_table(float4* out, void* stream);
-constexpr int kPhiTableSegs = 929;
+constexpr int kPhiTableSegs = 1153;   // phi contract v3 (contract.cuh kPhiSegs)
 
 }  // namespace cbp

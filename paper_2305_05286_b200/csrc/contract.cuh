@@ -51,103 +51,20 @@ __device__ __forceinline__ float ln32(float x)
     return __fmaf_rn(kf, kLn2Hi, t);
 }
 
-// regime A (x < 1): phi = x^2 G(x^2) - ln(x/2)
-__device__ __forceinline__ float phi_small(float x)
-{
-    const float l = ln32(__fmul_rn(0.5f, x));
-    const float y = __fmul_rn(x, x);
-    float g = -0x1.78439ep-16f;
-    g = __fmaf_rn(g, y, 0x1.63e3a2p-12f);
-    g = __fmaf_rn(g, y, -0x1.3e8c42p-8f);
-    g = __fmaf_rn(g, y, 0x1.555552p-4f);
-    g = __fmul_rn(g, y);
-    return __fsub_rn(g, l);
-}
-
-// regime B (x >= 1): t = e^-x = 2^-n e^-r, phi = 2 t H(t^2)
-__device__ __forceinline__ float phi_large(float x)
-{
-    const float a = __fmul_rn(x, kInvLn2);
-    const float n = rintf(a);
-    float rr = __fmaf_rn(-n, kLn2Hi, x);
-    rr = __fmaf_rn(-n, kLn2Lo, rr);
-    float e = 0x1.6b4e62p-10f;
-    e = __fmaf_rn(e, rr, -0x1.126f76p-7f);
-    e = __fmaf_rn(e, rr, 0x1.555796p-5f);
-    e = __fmaf_rn(e, rr, -0x1.555406p-3f);
-    e = __fmaf_rn(e, rr, 0x1.fffffcp-2f);
-    e = __fmaf_rn(e, rr, -1.0f);
-    e = __fmaf_rn(e, rr, 1.0f);
-    const int32_t ni = static_cast<int32_t>(n);
-    const float s = __uint_as_float(static_cast<uint32_t>(127 - ni) << 23);
-    const float t = __fmul_rn(e, s);
-    const float w = __fmul_rn(t, t);
-    float h = 0x1.2e8fe8p-3f;
-    h = __fmaf_rn(h, w, 0x1.1b78f8p-3f);
-    h = __fmaf_rn(h, w, 0x1.9a05a6p-3f);
-    h = __fmaf_rn(h, w, 0x1.555490p-2f);
-    h = __fmaf_rn(h, w, 1.0f);
-    const float u = __fmul_rn(t, h);
-    return __fadd_rn(u, u);
-}
-
-// phi v1 reference formula (unclamped): only used to build the v2 table
-__device__ __forceinline__ float phi_v1_unclamped(float x)
-{
-    return (x < 1.0f) ? phi_small(x) : phi_large(x);
-}
-
-// ---- phi contract v2: 929-segment cubic in u in [0, 1)
-constexpr int kPhiSegs = 929;
-
-// Coefficients of one segment: cubic through v1 at u = 0, 1/4, 3/4, 1 by
-// Newton divided differences in IEEE double, in the DESIGN.md order.
-__device__ __forceinline__ float4 phi_segment_coeffs(int seg)
-{
-    const int q4[4] = {0, 1, 3, 4};
-    double f[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        float x;
-        if (seg < 704) {
-            const int e = -43 + seg / 16, j = seg % 16;
-            x = __fmul_rn(static_cast<float>(64 + 4 * j + q4[k]), __uint_as_float(static_cast<uint32_t>(127 + e - 6) << 23));
-        } else {
-            x = __fmul_rn(static_cast<float>(64 + 4 * (seg - 704) + q4[k]), 0.03125f);
-        }
-        f[k] = static_cast<double>(phi_v1_unclamped(x));
-    }
-    const double d01 = __dmul_rn(__dsub_rn(f[1], f[0]), 4.0);
-    const double d12 = __dmul_rn(__dsub_rn(f[2], f[1]), 2.0);
-    const double d23 = __dmul_rn(__dsub_rn(f[3], f[2]), 4.0);
-    const double d012 = __ddiv_rn(__dmul_rn(__dsub_rn(d12, d01), 4.0), 3.0);
-    const double d123 = __ddiv_rn(__dmul_rn(__dsub_rn(d23, d12), 4.0), 3.0);
-    const double d0123 = __dsub_rn(d123, d012);
-    const double t2 = __dsub_rn(d01, __dmul_rn(d012, 0.25));
-    const double t3 = __dmul_rn(d0123, 0.1875);
-    float4 c = make_float4(__double2float_rn(f[0]), __double2float_rn(__dadd_rn(t2, t3)),
-                           __double2float_rn(__dsub_rn(d012, d0123)), __double2float_rn(d0123));
-    if (seg < 704) {
-        // device storage form: the local variable of x < 2 is taken as u' = u/16 (no shift),
-        // so c1, c2, c3 are stored times 16, 256, 4096 -- exact, and every product of the
-        // Horner evaluation is scaled by the same power of two: identical results.
-        c.y = __fmul_rn(c.y, 16.0f);
-        c.z = __fmul_rn(c.z, 256.0f);
-        c.w = __fmul_rn(c.w, 4096.0f);
-    }
-    return c;
-}
+// ---- phi contract v3: 1153-segment cubic in u in [0, 1)
+constexpr int kPhiSegs = 1153;
 
 // phi(x) = -log(tanh(x/2)) (equ_s2e5) with the R9 input clamp:
-// segment index and local u from the float's bits (x < 2) or from 8(x - 2)
-// (x >= 2), one 16-byte table load, three FMA.  The contract's output clamp is
-// omitted: on every float of [PHI_LO, 30] the cubic already lies in [PHI_LO, 30]
-// (exhaustive check, tests/test_oracle_contract.py), so results are identical.
+// segment index and local u from the float's bits (x < 2) or from 16(x - 2)
+// (x >= 2), one 16-byte table row (built on the host, cbp_api.cpp), three FMA.  The
+// contract's output clamp is omitted: on every float of [PHI_LO, 30] the cubic already lies
+// in [PHI_LO, 30] (exhaustive check, tests/test_oracle_contract.py), so results are identical.
 // m19 = 0x7ffff and one = 0x3f800000 are passed in registers so that
-// (b & m19) | one is a single LOP3 (immediates would take two).
-// x >= 2 without the XU pipe: m = fma_rz(x, 8, 2^23 - 16) = 2^23 + floor(8x - 16)
+// (b & m19) | one is a single LOP3 (immediates would take two); the x < 2 rows are stored
+// for the local variable u' = u/16 (c1, c2, c3 scaled by 16, 256, 4096: exact).
+// x >= 2 without the XU pipe: m = fma_rz(x, 16, 2^23 - 32) = 2^23 + floor(16x - 32)
 // exactly (the fma is exact before its one rounding toward zero, ulp 1 in
-// [2^23, 2^24)), so seg = bits(m) - bits(2^23) + 704 and u = fma(x, 8, -(16 + i))
+// [2^23, 2^24)), so seg = bits(m) - bits(2^23) + 704 and u = fma(x, 16, -(32 + i))
 // = t - i exactly: the contract's i = (int)t and u = t - (float)i, bit for bit.
 // segment index and local variable of x (clamped to [PHI_LO, PHI_HI])
 __device__ __forceinline__ void phi32_index(float x, uint32_t m19, uint32_t one, int& seg, float& u)
@@ -157,9 +74,9 @@ __device__ __forceinline__ void phi32_index(float x, uint32_t m19, uint32_t one,
     const int seg_lo = static_cast<int>(b >> 19) - 1344;
     uint32_t ub;
     asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(ub) : "r"(b), "r"(m19), "r"(one));   // (b & m19) | one
-    const float u_lo = __fsub_rn(__uint_as_float(ub), 1.0f);   // u/16, see phi_segment_coeffs
-    const float m = __fmaf_rz(x, 8.0f, 8388592.0f);
-    const float u_hi = __fmaf_rn(x, 8.0f, __fsub_rn(8388592.0f, m));
+    const float u_lo = __fsub_rn(__uint_as_float(ub), 1.0f);   // u/16
+    const float m = __fmaf_rz(x, 16.0f, 8388576.0f);
+    const float u_hi = __fmaf_rn(x, 16.0f, __fsub_rn(8388576.0f, m));
     const int seg_hi = static_cast<int>(__float_as_uint(m)) - (0x4b000000 - 704);
     const bool hi = x >= 2.0f;
     seg = hi ? seg_hi : seg_lo;

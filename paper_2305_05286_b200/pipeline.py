@@ -1,61 +1,20 @@
-"""Host-buffer decoding: chunked H2D -> cbp_decode -> D2H round-robin over four
-CUDA streams so PCIe transfers overlap the decode kernels (the end-to-end call a
-user with LLRs in host memory makes).  Chunks of 2^14 frames on 4 streams (tools/e2e_sweep.py,
-C2): 6.13e6 frames/s at 1 dB against 6.67e6 device-resident (92 %), 1.92e7 at 3 dB where the
-55.6 GB/s pinned H2D bounds it at 2.14e7; 2^15 / 2^16 chunks or 6 streams are no better."""
+"""Host-buffer decoding: the C ABI's cbp_decode_host (include/cbp.h) -- chunked H2D ->
+cbp_decode -> D2H pipelined over library-owned CUDA streams, so PCIe transfers overlap the
+decode kernels.  This module only keeps the round-1 Python entry points as thin wrappers."""
 from __future__ import annotations
 
 import torch
 
 from .cbp import CBP_STOP_BELIEF_M, Code
 
-
-API_NAME = "pipeline.decode_host (chunked H2D -> cbp_decode -> D2H on 4 streams)"
-_CACHE: dict = {}
+API_NAME = "cbp_decode_host (C ABI: chunked H2D -> decode -> D2H on 4 library streams)"
 
 
 def alloc_host_outputs(code: Code, frames: int) -> dict:
-    return {"bits": torch.empty((frames, code.words), dtype=torch.int32, pin_memory=True),
-            "iters": torch.empty(frames, dtype=torch.int32, pin_memory=True),
-            "flags": torch.empty(frames, dtype=torch.uint8, pin_memory=True)}
+    return code.alloc_host_outputs(frames)
 
 
 def decode_host(code: Code, llr_host: torch.Tensor, max_iter: int, stop_rule: int = CBP_STOP_BELIEF_M,
-                out: dict | None = None, chunk: int = 1 << 14, streams=None, nstreams: int = 4) -> dict:
-    """Decode float32 LLRs [frames, ld] held in (pinned) host memory; returns pinned host outputs.
-
-    The copies and launches are enqueued on `nstreams` streams (each with its own
-    device buffers); the call returns after synchronising them, so the outputs are ready."""
-    frames, ld = llr_host.shape
-    out = out if out is not None else alloc_host_outputs(code, frames)
-    if frames == 0:
-        return out
-    dev = code.device
-    n = min(chunk, frames)
-    key = (id(code), dev.index, nstreams, n, ld)
-    if streams is None:
-        # streams and device buffers persist across calls (no per-call stream creation / frees)
-        if key not in _CACHE:
-            ss = [torch.cuda.Stream(device=dev) for _ in range(nstreams)]
-            _CACHE.clear()
-            _CACHE[key] = (ss, [(torch.empty((n, ld), dtype=torch.float32, device=dev), code.alloc_outputs(n))
-                                for _ in ss])
-        streams, bufs = _CACHE[key]
-    else:
-        bufs = [(torch.empty((n, ld), dtype=torch.float32, device=dev), code.alloc_outputs(n)) for _ in streams]
-    cur = torch.cuda.current_stream(dev)
-    for s in streams:
-        s.wait_stream(cur)
-    for k, b in enumerate(range(0, frames, n)):
-        e = min(b + n, frames)
-        s = streams[k % len(streams)]
-        dl, dout = bufs[k % len(streams)]
-        with torch.cuda.stream(s):
-            dl[: e - b].copy_(llr_host[b:e], non_blocking=True)
-            o = {key: v[: e - b] for key, v in dout.items()}
-            code.decode(dl[: e - b], max_iter, stop_rule, out=o, stream=s)
-            for key in ("bits", "iters", "flags"):
-                out[key][b:e].copy_(o[key], non_blocking=True)
-    for s in streams:
-        s.synchronize()
-    return out
+                out: dict | None = None, chunk: int = 1 << 14, nstreams: int = 4) -> dict:
+    """Decode float32 LLRs [frames, ld] held in (pinned) host memory; returns host outputs."""
+    return code.decode_host(llr_host, max_iter, stop_rule, out=out, chunk_frames=chunk, nstreams=nstreams)

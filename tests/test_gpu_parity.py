@@ -77,8 +77,8 @@ def test_contract_bit_equal_on_device():
     rng = np.random.default_rng(0)
     lo, hi = np.log(1e-14), np.log(40.0)
     x = np.concatenate([np.exp(rng.uniform(lo, hi, 1 << 22)), [0.0, 1.0, 30.0, 1e-40, 1e30, np.inf]]).astype(np.float32)
-    # dense exhaustive slice around the regime switch x = 1 and the clamp 30
-    for centre in (1.0, 30.0, oracle.PHI_LO):
+    # dense exhaustive slices around the regime switch x = 2 and the clamps 30, PHI_LO
+    for centre in (1.0, 2.0, 30.0, oracle.PHI_LO):
         b = np.float32(centre).view(np.uint32).astype(np.int64)
         x = np.concatenate([x, (np.arange(b - 100000, b + 100000)).astype(np.uint32).view(np.float32)])
     y_gpu = cbp.cbp.eval_contract(0, torch.from_numpy(x).cuda()).cpu().numpy()
@@ -95,21 +95,15 @@ def test_contract_bit_equal_on_device():
         assert np.float32(s) == s_gpu[k] and np.float32(c) == c_gpu[k]
 
 
-def test_phi_table_built_on_device_equals_oracle_table():
-    """The v2 table is generated on the GPU (fp32 v1 values + fp64 Newton
-    differences) and independently by the oracle on the host: identical bits."""
+def test_phi_table_of_the_product_equals_oracle_table():
+    """The v3 table is built by the product (cbp_api.cpp, host double log1p/expm1 + Newton
+    differences, uploaded per device) and independently by the oracle: identical bits."""
     _need_gpu()
     g = cbp.cbp.phi_table(0).cpu().numpy()
     o = oracle.phi32_table()
     # device storage form: x < 2 segments keep c1, c2, c3 times 16, 256, 4096 (exact scaling)
     o[:704] *= np.float32([1.0, 16.0, 256.0, 4096.0])
-    assert (g.view(np.uint32) == o.view(np.uint32)).all()
-    rng = np.random.default_rng(1)
-    x = np.exp(rng.uniform(np.log(1e-14), np.log(40.0), 1 << 20)).astype(np.float32)
-    v1 = cbp.cbp.eval_contract(4, torch.from_numpy(x).cuda()).cpu().numpy()
-    sample = x[:20000]
-    assert (v1[:20000].view(np.uint32) == np.array([oracle.phi32_v1(float(t)) for t in sample],
-                                                    np.float32).view(np.uint32)).all()
+    assert g.shape == o.shape and (g.view(np.uint32) == o.view(np.uint32)).all()
 
 
 # ---------------------------------------------------------------- decode parity
@@ -357,6 +351,43 @@ def test_decode_host_pipeline(codes):
     oo = o.decode(np.ascontiguousarray(l_o), 30)
     assert (out["bits"].numpy()[idx].view(np.uint32)[:, :oo["bits"].shape[1]] == oo["bits"]).all()
     assert (out["iters"].numpy()[idx] == oo["iters"]).all()
+
+
+def test_decode_host_abi_int8_and_errors(codes):
+    """cbp_decode_host_i8 (host int8 LLRs) equals the device decode; chunk / stream settings do
+    not change results; the host entry points reject bad arguments without touching outputs,
+    and the binding rejects undersized output buffers (the ABI cannot see their sizes)."""
+    import ctypes
+    g, o = codes("C2")
+    F = 5000
+    llr, _ = g.channel(2.0, 21, 0, F, llr_mode=1, want_cw=False)
+    q = torch.round(llr * 4).clamp(-127, 127).to(torch.int8)
+    ldq = (g.N + 15) // 16 * 16
+    qh = torch.zeros((F, ldq), dtype=torch.int8, pin_memory=True)
+    qh[:, :g.N].copy_(q[:, :g.N])
+    ref = g.decode_i8(qh.cuda(), 0.25, 30)
+    for chunk, ns in ((0, 0), (777, 3), (F, 1)):
+        out = g.decode_host(qh, 30, scale=0.25, chunk_frames=chunk, nstreams=ns)
+        for k in ("bits", "iters", "flags"):
+            assert torch.equal(out[k], ref[k].cpu()), (k, chunk, ns)
+    L = cbp.lib()
+    ok = cbp.cbp._Opts(30, 0, 0, 0.75)
+    hb = torch.zeros((F, g.words), dtype=torch.int32)
+    hi = torch.full((F,), -7, dtype=torch.int32)
+    hf = torch.zeros(F, dtype=torch.uint8)
+    lh = torch.zeros((F, 648), dtype=torch.float32)
+
+    def call(ld=648, frames=F, lw=g.words, chunk=0, ns=0, ptr=True):
+        return L.cbp_decode_host(g.handle, lh.data_ptr() if ptr else None, ld, frames, ctypes.byref(ok),
+                                 hb.data_ptr(), lw, hi.data_ptr(), hf.data_ptr(), chunk, ns)
+    assert call(ld=640) == 1 and call(ld=650) == 1 and call(frames=-1) == 1 and call(lw=g.words - 1) == 1
+    assert call(chunk=-1) == 1 and call(ns=17) == 1 and call(ptr=False) == 1
+    assert (hi == -7).all()                                  # nothing ran
+    assert call(frames=0) == 0
+    with pytest.raises(cbp.CbpError):
+        g.decode(llr, 30, out=g.alloc_outputs(F - 1))        # too few rows for the batch
+    with pytest.raises(cbp.CbpError):
+        g.ber_sim(2.0, 1, 0, 10, 30, counts=torch.zeros(4, dtype=torch.int64, device=g.device))
 
 
 # ---------------------------------------------------------------- NEXT-3: comparison schedules
@@ -651,7 +682,9 @@ def test_decode_parity_size_limits(fpl, spec, seed, Z, frames, eb):
 
 
 @pytest.mark.parametrize("env", [{"CBP_SPLIT_R": "1"}, {"CBP_SPLIT_R": "0"}, {"CBP_GLOBAL_TEAMS": "8"},
-                                 {"CBP_GLOBAL_TEAMS": "3"}], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+                                 {"CBP_GLOBAL_TEAMS": "3"}, {"CBP_WARP_KERNEL": "0"},
+                                 {"CBP_WARP_KERNEL": "0", "CBP_SPLIT_R": "1"}],
+                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 @pytest.mark.parametrize("name,eb,frames", [("C2", 2.0, 1500), ("C3a", 2.0, 200), ("C1", 2.0, 3000),
                                             ("P2048", 1.5, 300)])
 def test_state_layouts_equal_oracle(monkeypatch, env, name, eb, frames):

@@ -77,14 +77,15 @@ def build_cbp(force=False, out=None, defines=()):
     if force or _stale(out, deps):
         tmp = ROOT / "build" / ("cbp" if out == CBP_SO else "cbp_" + out.stem)
         tmp.mkdir(parents=True, exist_ok=True)
-        objs = []
         common = ["-I", ROOT / "include", "-I", ROOT / "inputs", "-I", ROOT / "paper_2305_05286_b200" / "csrc"]
-        for src in CBP_SRC:
-            obj = tmp / (src.stem + ".o")
-            _run([NVCC, "-std=c++17", *ARCH, "-O3", "-lineinfo", *NVCC_CONTRACT, "-Xptxas", "-v",
-                  "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-Xcompiler", "-ffp-contract=off",
-                  *[f"-D{d}" for d in defines], *common, "-c", src, "-o", obj])
-            objs.append(obj)
+        cmds = [[NVCC, "-std=c++17", *ARCH, "-O3", "-lineinfo", *NVCC_CONTRACT, "-Xptxas", "-v",
+                 "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-Xcompiler", "-ffp-contract=off",
+                 *[f"-D{d}" for d in defines], *common, "-c", src, "-o", tmp / (src.stem + ".o")] for src in CBP_SRC]
+        objs = [c[-1] for c in cmds]
+        # one nvcc per translation unit, in parallel (the kernels are split by algorithm)
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+            list(ex.map(_run, cmds))
         inp_obj = tmp / "qc_construct.o"
         _run(["gcc", "-std=c11", "-O2", "-fPIC", "-c", INPUTS_SRC[0], "-o", inp_obj])
         objs.append(inp_obj)
