@@ -160,6 +160,8 @@ struct cbp_code {
     int ctas_per_sm[4] = {1, 1, 1, 1}, num_sms = 1;
     cbp::Geometry geo_chan{};          // cbp_channel: cbp_kernel (the warp kernel has no channel-only mode)
     int ctas_chan = 1;
+    cbp::Geometry geo_omega{};         // log-tanh decode with Omega output on cbp_warp_kernel: room for S
+    int ctas_omega = 1;
     int4* ent_dev[4] = {};             // device copies of ent[] (bulk-copied by cbp_warp_kernel)
     ~cbp_code()
     {
@@ -347,7 +349,11 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
     // (CBP_GLOBAL_TEAMS forces cbp_kernel's global-state path and so disables the warp kernel too)
     const bool use_warp = !(wv && wv[0] == '0' && wv[1] == 0) && !std::getenv("CBP_GLOBAL_TEAMS");
     const int split_r_env = split_env;
-    auto make_geo = [&](int alg, int P, bool split_r, int multi_maxt = 512, bool allow_warp = true) {
+    // cbp_warp_kernel phi-row path (A/B runs): CBP_WARP_TEX=0 C2B rows through TEX (default), 1 both, 2 none
+    const char* t2 = std::getenv("CBP_WARP_TEX");
+    const int tex2_env = (t2 && t2[0] >= '0' && t2[0] <= '2' && t2[1] == 0) ? t2[0] - '0' : -1;
+    auto make_geo = [&](int alg, int P, bool split_r, int multi_maxt = 512, bool allow_warp = true,
+                        bool with_S = false) {
         cbp::Geometry G{};
         G.alg = alg;
         G.P = P;
@@ -357,11 +363,12 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
             G.kslots = (Z + 31) / 32;
             G.lanes = (Z + G.kslots - 1) / G.kslots;
             G.multi = 0; G.F = 1; G.Zp = 32; G.team_threads = 32; G.state_in_smem = 1;
-            const int maxt = G.kslots == 1 ? 512 : 384;
+            const int maxt = G.kslots == 1 ? CBP_WARPK1_MAXT : CBP_WARPK_MAXT;
             const int64_t rw = static_cast<int64_t>(nent) * G.kslots * 32;
-            G.table_words = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4 + 4;
-            auto per_warp = [&](bool rg) {   // counters (8 x u64) | QP [2N] | S [M] | cw | R
-                return (16 + 2LL * c->N + c->M + (nwords + 3) / 4 * 4 + (rg ? 0 : rw) + 3) / 4 * 4;
+            G.tex2 = tex2_env >= 0 ? tex2_env : 0;
+            G.table_words = (G.tex2 == 1 ? 0 : 4 * cbp::kPhiTableSegs) + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4 + 4;
+            auto per_warp = [&](bool rg) {   // counters (8 x u64) | QP [2N] | cw | R | S [M] (Omega output only)
+                return (16 + 2LL * c->N + (nwords + 3) / 4 * 4 + (rg ? 0 : rw) + (with_S ? c->M : 0) + 3) / 4 * 4;
             };
             auto warps_of = [&](bool rg) {
                 const int64_t w = (smem_optin - 4LL * G.table_words) / (4 * per_warp(rg));
@@ -507,6 +514,18 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
     // cbp_channel (no decoding) runs on cbp_kernel with the log-tanh entries
     c->geo_chan = c->geo[0];
     c->ctas_chan = c->ctas_per_sm[0];
+    c->geo_omega = c->geo[0];
+    c->ctas_omega = c->ctas_per_sm[0];
+    if (c->geo[0].wk) {
+        c->geo_omega = make_geo(0, 1, false, 512, true, true);
+        int occ = 0;
+        if (!c->geo_omega.wk || cbp::occupancy_ctas_per_sm(c->geo_omega, &occ) != 0 || occ < 1) {
+            cudaGetLastError();
+            cbp_code_destroy(c);
+            return fail(CBP_E_UNSUPPORTED, "cbp_code_create: Omega-output kernel does not fit on this device");
+        }
+        c->ctas_omega = occ;
+    }
     if (c->geo[0].wk) {
         c->geo_chan = make_geo(0, 1, false, 512, false);
         int occ = 0;
@@ -550,11 +569,28 @@ cbp_status cbp_get_launch_info(const cbp_code* c, cbp_launch_info* o)
 
 namespace {
 
-cbp::KernelArgs base_args(const cbp_code* c, int alg = 0, bool chan = false)
+// the geometry a launch runs with: cbp_channel on cbp_kernel; a log-tanh decode with Omega output
+// on the warp kernel's geometry that has room for the check records
+const cbp::Geometry& geo_for(const cbp_code* c, int alg, bool chan, bool omega, int* ctas)
+{
+    if (chan) {
+        *ctas = c->ctas_chan;
+        return c->geo_chan;
+    }
+    if (omega && alg == 0 && c->geo[0].wk) {
+        *ctas = c->ctas_omega;
+        return c->geo_omega;
+    }
+    *ctas = c->ctas_per_sm[alg];
+    return c->geo[alg];
+}
+
+cbp::KernelArgs base_args(const cbp_code* c, int alg = 0, bool chan = false, bool omega = false)
 {
     cbp::KernelArgs a{};
     cbp::DevCode& d = a.code;
-    const cbp::Geometry& G = chan ? c->geo_chan : c->geo[alg];
+    int ctas = 0;
+    const cbp::Geometry& G = geo_for(c, alg, chan, omega, &ctas);
     d.N = c->N; d.K = c->K; d.M = c->M; d.Z = c->Z; d.mb = c->mb; d.nb = c->nb; d.kb = c->kb; d.core = c->core;
     d.nent = c->nent; d.E = static_cast<int32_t>(c->E); d.nwords = (c->N + 31) / 32; d.kwords = (c->K + 31) / 32;
     d.max_dc = c->max_dc; d.can_encode = c->can_encode; d.mid = c->mid;
@@ -599,13 +635,12 @@ cbp_status run(const cbp_code* c, cbp::KernelArgs& a, int64_t frames, void* stre
     DeviceGuard g(c->device);
     if (!g.ok) return fail(CBP_E_CUDA, std::string(who) + ": cudaSetDevice failed");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const bool chan = a.mode == cbp::MODE_CHANNEL;
-    const cbp::Geometry& G = chan ? c->geo_chan : c->geo[a.algorithm];
+    int ctas = 1;
+    const cbp::Geometry& G = geo_for(c, a.algorithm, a.mode == cbp::MODE_CHANNEL, a.omega != nullptr, &ctas);
     const int64_t per_cta = static_cast<int64_t>(G.F) * G.teams * G.P;
     const int64_t ctas_needed = (frames + per_cta - 1) / per_cta;
     const int grid = static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>(static_cast<int64_t>(c->num_sms) * (chan ? c->ctas_chan : c->ctas_per_sm[a.algorithm]),
-                             ctas_needed)));
+        1, std::min<int64_t>(static_cast<int64_t>(c->num_sms) * ctas, ctas_needed)));
     cudaError_t e;
     unsigned long long* q = nullptr;
     cudaMemPool_t pool = work_pool(c->device);
@@ -660,7 +695,7 @@ cbp_status decode_common(const cbp_code* c, const void* in, int32_t mode, int64_
     if (ld_words < (c->N + 31) / 32) return fail(CBP_E_INVALID, std::string(who) + ": ld_words < ceil(N/32)");
     if (mode == cbp::MODE_DECODE_I8 && !(std::isfinite(scale) && scale > 0.0f))
         return fail(CBP_E_INVALID, std::string(who) + ": scale must be finite and > 0");
-    cbp::KernelArgs a = base_args(c, opts->algorithm);
+    cbp::KernelArgs a = base_args(c, opts->algorithm, false, d_omega != nullptr);
     a.mode = mode;
     a.max_iter = opts->max_iter;
     a.stop_rule = opts->stop_rule;

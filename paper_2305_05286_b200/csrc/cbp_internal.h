@@ -73,6 +73,14 @@ struct KernelArgs {
 #define CBP_TEX_B2V 0
 #endif
 
+// thread limits (launch bounds) of cbp_warp_kernel: K = 1 (Z <= 32) and K >= 2 check slots per lane
+#ifndef CBP_WARPK1_MAXT
+#define CBP_WARPK1_MAXT 512
+#endif
+#ifndef CBP_WARPK_MAXT
+#define CBP_WARPK_MAXT 384
+#endif
+
 // thread limit (launch bound) of the one-frame-per-lane warp-team instantiation
 #ifndef CBP_WARP_MAXT
 #define CBP_WARP_MAXT 512
@@ -91,6 +99,7 @@ struct Geometry {
     int32_t r_global, r_words;     // split layout: R in the global workspace, r_words per group
     int32_t wk;                    // 1: cbp_warp_kernel (one frame per warp, K check slots per lane)
     int32_t kslots, lanes;         // cbp_warp_kernel: K and L = ceil(Z / K)
+    int32_t tex2;                  // cbp_warp_kernel phi rows: 0 C2B through TEX, 1 both (no smem table), 2 none
 };
 
 // launch (cbp_kernels.cu); returns cudaError_t as int

@@ -1495,6 +1495,7 @@ static int dispatch_alg(const Geometry& g, Args... args)
         return sm == 2 ? Fn<true, 2, 512, ALG, 1>::run(g, args...)
              : sm == 1 ? Fn<true, 1, 512, ALG, 1>::run(g, args...) : Fn<true, 0, 512, ALG, 1>::run(g, args...);
     if (g.threads <= 768 && sm == 2) return Fn<true, 2, 768, ALG, 1>::run(g, args...);   // split layout
+    if (g.threads <= 768 && sm == 0) return Fn<true, 0, 768, ALG, 1>::run(g, args...);   // 2 C4 teams, 85 registers
     return sm == 2 ? Fn<true, 2, 1024, ALG, 1>::run(g, args...)
          : sm == 1 ? Fn<true, 1, 1024, ALG, 1>::run(g, args...) : Fn<true, 0, 1024, ALG, 1>::run(g, args...);
 }

@@ -56,102 +56,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 }
 
 // ---------------------------------------------------------------- the rows
-// One slot's check of a base row with DC edges (producer-side update, cbp_kernel.cuh): the
-// row's schedule entries, all loads, phase 1, phase 2.  rrow: this lane's R word of (row entry 0,
-// this slot); the word of edge e is rrow[e K 32].  A slot beyond Z (vk false) computes on a
-// valid address and stores nothing but its private R words.  The slots of a row run in a loop
-// (not unrolled): the unrolled K x DC bodies overflowed the 32 KB L1.5 instruction cache
-// (ncu: no_instruction stalls 2.3 per issue, issue active 37 %).
-template <int DC, int K, int ALG>
-__device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int rq,
-                                     bool vk, const Lane& L, TexH tex, char* qp, float* rrow, RowAcc<1>& acc)
-{
-    constexpr bool LBP = ALG == 2;
-    int aqp[DC];
-    float vs[DC][2], ro[DC][1], q[DC][1], ph[DC][1];
-    acc.Ssum[0] = 0.0f;
-    acc.negw[0] = acc.flipw[0] = acc.oldbits[0] = 0u;
-#pragma unroll
-    for (int e = 0; e < DC; ++e) {
-        const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e));
-        aqp[e] = A.x + wrap(rq + A.y, L.ZQ);
-        CBP_CHECK(aqp[e] >= 0 && aqp[e] + 8 <= L.slot_bytes);
-        ldf<2>(qp, aqp[e], vs[e]);                                 // {Lambda_v, H_v}
-        ro[e][0] = rrow[e * K * 32];                               // R_{c->v}
-        if constexpr (LBP) vs[e][1] = vs[e][0];
-    }
-#pragma unroll
-    for (int e = 0; e < DC; ++e) cbp_phase1<1>(vs[e], ro[e], q[e], ph[e], ptab, L, tex, acc);
-#pragma unroll
-    for (int e = 0; e < DC; ++e) {
-        float rn[1], lamn[1];
-        cbp_phase2<1>(acc, q[e], ph[e], rn, lamn, ptab, L, tex);
-        if (vk) {
-            const float st[2] = {lamn[0], LBP ? lamn[0] : vs[e][0]};
-            stf<2>(qp, aqp[e], st);
-        }
-        rrow[e * K * 32] = rn[0];                                  // equ_s4e22 commit of R_{c->v}
-    }
-}
-
-// rows longer than CBP_DC_REG: two passes over the edges, parking {Q^new, Phi | sign of the
-// decision} in the variable's slot between the phases (as cbp_row_park)
-template <int K, int ALG>
-__device__ __forceinline__ void wrow_park(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int dc,
-                                          int rq, bool vk, const Lane& L, char* qp, float* rrow, RowAcc<1>& acc)
-{
-    constexpr bool LBP = ALG == 2;
-    acc.Ssum[0] = 0.0f;
-    acc.negw[0] = acc.flipw[0] = acc.oldbits[0] = 0u;
-    for (int e = 0; e < dc; ++e) {
-        const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e));
-        const int a = A.x + wrap(rq + A.y, L.ZQ);
-        float v[2], ro[1] = {rrow[e * K * 32]}, q[1], ph[1];
-        ldf<2>(qp, a, v);
-        if (LBP) v[1] = v[0];
-        cbp_phase1<1, false>(v, ro, q, ph, ptab, L, 0, acc);
-        if (vk) {
-            const float st[2] = {q[0], __uint_as_float(__float_as_uint(ph[0]) | (__float_as_uint(v[0]) & kSign))};
-            stf<2>(qp, a, st);
-        }
-    }
-    for (int e = 0; e < dc; ++e) {
-        const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e));
-        const int a = A.x + wrap(rq + A.y, L.ZQ);
-        float v[2], rn[1], lamn[1];
-        ldf<2>(qp, a, v);
-        const float q[1] = {v[0]}, ph[1] = {fabsf(v[1])};
-        cbp_phase2<1, false>(acc, q, ph, rn, lamn, ptab, L, 0);
-        if (vk) {
-            const float st[2] = {lamn[0], LBP ? lamn[0] : v[1]};
-            stf<2>(qp, a, st);
-        }
-        rrow[e * K * 32] = rn[0];
-    }
-}
-
-template <int K, int ALG>
-__device__ __forceinline__ void wrow_dispatch(int dc, const int4* __restrict__ ent, const float4* __restrict__ ptab,
-                                              int e0, int rq, bool vk, const Lane& L, TexH tex, char* qp, float* rrow,
-                                              RowAcc<1>& acc)
-{
-    switch (dc) {
-#if CBP_DC_REG >= 1
-    case 1: wrow<1, K, ALG>(ent, ptab, e0, rq, vk, L, tex, qp, rrow, acc); break;
-    case 2: wrow<2, K, ALG>(ent, ptab, e0, rq, vk, L, tex, qp, rrow, acc); break;
-    case 3: wrow<3, K, ALG>(ent, ptab, e0, rq, vk, L, tex, qp, rrow, acc); break;
-    case 4: wrow<4, K, ALG>(ent, ptab, e0, rq, vk, L, tex, qp, rrow, acc); break;
-    case 5: wrow<5, K, ALG>(ent, ptab, e0, rq, vk, L, tex, qp, rrow, acc); break;
-    case 6: wrow<6, K, ALG>(ent, ptab, e0, rq, vk, L, tex, qp, rrow, acc); break;
+#ifndef CBP_WARP_LEAN
+#define CBP_WARP_LEAN 0     // 1: entries and R re-read per slot (fewer registers, A/B runs)
 #endif
-#if CBP_DC_REG >= 8
-    case 7: wrow<7, K, ALG>(ent, ptab, e0, rq, vk, L, tex, qp, rrow, acc); break;
-    case 8: wrow<8, K, ALG>(ent, ptab, e0, rq, vk, L, tex, qp, rrow, acc); break;
-#endif
-    default: wrow_park<K, ALG>(ent, ptab, e0, dc, rq, vk, L, qp, rrow, acc); break;
-    }
-}
-
 // K per-slot values in registers, written / read at a runtime slot index by predicated moves
 // (a dynamically indexed array would live in local memory)
 template <int K, typename T>
@@ -163,22 +70,196 @@ struct SlotVals {
         for (int j = 0; j < K; ++j)
             if (j == k) v[j] = x;
     }
-    __device__ __forceinline__ T get(int k) const
-    {
-        T x = v[0];
-#pragma unroll
-        for (int j = 1; j < K; ++j)
-            if (j == k) x = v[j];
-        return x;
-    }
 };
+
+// What a row reports to the stop logic: first / last unclean check, and for a possible mid-row
+// stop the slots' previous decision bits and check records (old / new).
+template <int K>
+struct WRow {
+    int first_bad, last_bad;
+    SlotVals<K, uint32_t> oldb;
+    SlotVals<K, float> sold, snew;
+};
+
+// The per-row context of a lane.
+struct WCtx {
+    int l, Lk, Z;
+    bool fire_possible, keepS;   // the window may fill in this row; S records are kept (Omega output)
+    char* qp;
+    float* rrow;                 // this lane's R word of (row entry 0, slot 0); (edge e, slot k) at rrow[(e K + k) 32]
+    float* Srow;                 // S records of this row (keepS)
+};
+
+// Slot k's check update done: its record, the rollback values and its stop flags (equ_s4e2, equ_s4e24).
+template <int K, bool LBP>
+__device__ __forceinline__ void wslot_done(const WCtx& c, int k, int rr, bool v, const RowAcc<1>& acc, WRow<K>& o)
+{
+    const float sn = __uint_as_float(__float_as_uint(acc.Ssum[0]) | (acc.negw[0] & kSign));
+    if (c.keepS && !LBP && v) c.Srow[rr] = sn;                  // equ_s4e23
+    if (c.fire_possible) {
+        o.oldb.set(k, acc.oldbits[0]);
+        o.snew.set(k, sn);
+    }
+    const unsigned m = __ballot_sync(kFull, v && (((acc.negw[0] | acc.flipw[0]) & kSign) != 0u));
+    if (m) {
+        o.first_bad = min(o.first_bad, k * c.Lk + __ffs(m) - 1);
+        o.last_bad = max(o.last_bad, k * c.Lk + 31 - __clz(m));
+    }
+}
+
+// One base row with DC edges for the K slots of the lane (producer-side update, cbp_kernel.cuh):
+// the row's schedule entries once, then per slot all loads, phase 1, phase 2.  The slots run in
+// a loop that is not unrolled: the unrolled K x DC bodies overflowed the 32 KB L1.5 instruction
+// cache (ncu: no_instruction stalls 2.3 per issue, issue active 37 %).  A slot beyond Z (v false)
+// computes on check Z - 1 and stores nothing but its private R words.
+template <int DC, int K, int ALG, int TM>
+__device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
+                                     const Lane& L, TexH tex, const WCtx& c, WRow<K>& o)
+{
+    constexpr bool LBP = ALG == 2;
+    constexpr bool TEXC = TM != 2, TEXB = TM == 1;             // phi rows: C2B / B2V through the texture pipe
+#if !CBP_WARP_LEAN
+    int2 A[DC];
+#pragma unroll
+    for (int e = 0; e < DC; ++e) A[e] = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e));
+    // R words of the next slot are requested before the current slot's update (their global /
+    // L2 latency then overlaps it); slot 0's are loaded here
+    float rnext[DC];
+#pragma unroll
+    for (int e = 0; e < DC; ++e) rnext[e] = c.rrow[e * K * 32];
+#endif
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) {
+        const int r = c.l + k * c.Lk;
+        const bool v = c.l < c.Lk && r < c.Z;
+        const int rr = v ? r : c.Z - 1;
+        if (c.keepS && c.fire_possible) o.sold.set(k, c.Srow[rr]);
+        float* rk = c.rrow + k * 32;
+        float ro[DC][1];
+#if CBP_WARP_LEAN
+        int2 A[DC];
+#pragma unroll
+        for (int e = 0; e < DC; ++e) {
+            A[e] = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e));
+            ro[e][0] = rk[e * K * 32];
+        }
+#else
+#pragma unroll
+        for (int e = 0; e < DC; ++e) ro[e][0] = rnext[e];          // R_{c->v}
+        if (k + 1 < K) {
+#pragma unroll
+            for (int e = 0; e < DC; ++e) rnext[e] = rk[32 + e * K * 32];
+        }
+#endif
+        RowAcc<1> acc;
+        acc.Ssum[0] = 0.0f;
+        acc.negw[0] = acc.flipw[0] = acc.oldbits[0] = 0u;
+        int aqp[DC];
+        float vs[DC][2], q[DC][1], ph[DC][1];
+#pragma unroll
+        for (int e = 0; e < DC; ++e) {
+            aqp[e] = A[e].x + wrap(rr * 8 + A[e].y, L.ZQ);
+            CBP_CHECK(aqp[e] >= 0 && aqp[e] + 8 <= L.slot_bytes);
+            ldf<2>(c.qp, aqp[e], vs[e]);                           // {Lambda_v, H_v}
+            if constexpr (LBP) vs[e][1] = vs[e][0];
+        }
+#pragma unroll
+        for (int e = 0; e < DC; ++e) cbp_phase1<1, TEXC>(vs[e], ro[e], q[e], ph[e], ptab, L, tex, acc);
+#pragma unroll
+        for (int e = 0; e < DC; ++e) {
+            float rn[1], lamn[1];
+            cbp_phase2<1, TEXB>(acc, q[e], ph[e], rn, lamn, ptab, L, tex);
+            if (v) {
+                const float st[2] = {lamn[0], LBP ? lamn[0] : vs[e][0]};
+                stf<2>(c.qp, aqp[e], st);
+            }
+            rk[e * K * 32] = rn[0];                                // equ_s4e22 commit of R_{c->v}
+        }
+        wslot_done<K, LBP>(c, k, rr, v, acc, o);
+    }
+}
+
+// Rows longer than CBP_DC_REG: per slot two passes over the edges, parking {Q^new, Phi | sign
+// of the decision} in the variable's slot between the phases (only this lane touches the
+// variable during the row).  (Chunks of 4 edges with masked tails measured 8 % slower on C3b.)
+template <int K, int ALG, int TM>
+__device__ __forceinline__ void wrow_park(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int dc,
+                                          const Lane& L, TexH tex, const WCtx& c, WRow<K>& o)
+{
+    constexpr bool LBP = ALG == 2;
+    // one edge at a time: the texture latency would be exposed on every edge, so both phi rows
+    // come from the shared-memory table (TEX for C2B here measured 30 % slower on C3b) unless
+    // the table is not staged (TM 1)
+    constexpr bool TEXC = TM == 1, TEXB = TM == 1;
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) {
+        const int r = c.l + k * c.Lk;
+        const bool v = c.l < c.Lk && r < c.Z;
+        const int rr = v ? r : c.Z - 1;
+        if (c.keepS && c.fire_possible) o.sold.set(k, c.Srow[rr]);
+        float* rk = c.rrow + k * 32;
+        RowAcc<1> acc;
+        acc.Ssum[0] = 0.0f;
+        acc.negw[0] = acc.flipw[0] = acc.oldbits[0] = 0u;
+        for (int e = 0; e < dc; ++e) {
+            const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e));
+            const int a = A.x + wrap(rr * 8 + A.y, L.ZQ);
+            float vv[2], ro[1] = {rk[e * K * 32]}, q[1], ph[1];
+            ldf<2>(c.qp, a, vv);
+            if (LBP) vv[1] = vv[0];
+            cbp_phase1<1, TEXC>(vv, ro, q, ph, ptab, L, tex, acc);
+            if (v) {
+                const float st[2] = {q[0], __uint_as_float(__float_as_uint(ph[0]) | (__float_as_uint(vv[0]) & kSign))};
+                stf<2>(c.qp, a, st);
+            }
+        }
+        for (int e = 0; e < dc; ++e) {
+            const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e));
+            const int a = A.x + wrap(rr * 8 + A.y, L.ZQ);
+            float vv[2], rn[1], lamn[1];
+            ldf<2>(c.qp, a, vv);
+            const float q[1] = {vv[0]}, ph[1] = {fabsf(vv[1])};
+            cbp_phase2<1, TEXB>(acc, q, ph, rn, lamn, ptab, L, tex);
+            if (v) {
+                const float st[2] = {lamn[0], LBP ? lamn[0] : vv[1]};
+                stf<2>(c.qp, a, st);
+            }
+            rk[e * K * 32] = rn[0];
+        }
+        wslot_done<K, LBP>(c, k, rr, v, acc, o);
+    }
+}
+
+template <int K, int ALG, int TM>
+__device__ __forceinline__ void wrow_dispatch(int dc, const int4* __restrict__ ent, const float4* __restrict__ ptab,
+                                              int e0, const Lane& L, TexH tex, const WCtx& c, WRow<K>& o)
+{
+    switch (dc) {
+#if CBP_DC_REG >= 1
+    case 1: wrow<1, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
+    case 2: wrow<2, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
+    case 3: wrow<3, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
+    case 4: wrow<4, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
+    case 5: wrow<5, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
+    case 6: wrow<6, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
+#endif
+#if CBP_DC_REG >= 8
+    case 7: wrow<7, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
+    case 8: wrow<8, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
+#endif
+    default: wrow_park<K, ALG, TM>(ent, ptab, e0, dc, L, tex, c, o); break;
+    }
+}
 
 // ---------------------------------------------------------------- the kernel
 // RG: R in a global slot per warp (else in the warp's shared state).  Modes: decode (fp32 /
 // int8 LLRs from HBM) and the fused ber_sim; cbp_channel runs on cbp_kernel.
-template <int K, bool RG, int MAXT, int ALG>
+// TM: phi table rows for C2B / B2V through the texture pipe (0: C2B only, 1: both -- the table
+// is then not staged in shared memory, 2: neither).
+template <int K, bool RG, int MAXT, int ALG, int TM>
 __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant__ KernelArgs a)
 {
+    constexpr bool TEXB = TM == 1;
     constexpr bool LBP = ALG == 2;
     extern __shared__ __align__(16) uint32_t smem[];
     const DevCode& C = a.code;
@@ -186,16 +267,17 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
 
     // ---- a1: stage the phi table and the schedule entries with the bulk-copy engine (one
     // elected thread arms an mbarrier with the byte count, every thread waits on its phase)
+    constexpr int kTabWords = TEXB ? 0 : 4 * kPhiSegs;
     float4* ptab = reinterpret_cast<float4*>(smem);
-    int4* ent = reinterpret_cast<int4*>(smem + 4 * kPhiSegs);
-    int32_t* row_ptr = reinterpret_cast<int32_t*>(smem + 4 * kPhiSegs + 8 * C.nent);
+    int4* ent = reinterpret_cast<int4*>(smem + kTabWords);
+    int32_t* row_ptr = reinterpret_cast<int32_t*>(smem + kTabWords + 8 * C.nent);
     int16_t* pshift = reinterpret_cast<int16_t*>(row_ptr + mb + 1);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.table_words - 4);
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
-        const uint32_t tb = 16u * kPhiSegs, eb = 32u * static_cast<uint32_t>(C.nent);
+        const uint32_t tb = 4u * kTabWords, eb = 32u * static_cast<uint32_t>(C.nent);
         mbar_expect_tx(bar, tb + eb);
-        bulk_g2s(ptab, C.phi_tab, tb, bar);
+        if (tb) bulk_g2s(ptab, C.phi_tab, tb, bar);
         bulk_g2s(ent, a.ent_dev, eb, bar);
     }
     for (int k = threadIdx.x; k <= mb; k += blockDim.x) row_ptr[k] = a.row_ptr[k];
@@ -212,16 +294,17 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
         rk[k] = vk[k] ? r : Z - 1;                            // invalid slots compute on check Z - 1, store nothing
         rq[k] = rk[k] * 8;
     }
-    // per-warp shared state: counters (8 x u64) | QP [2N] | S [M] | cw [nwords] | R (if !RG)
+    // per-warp shared state: counters (8 x u64) | QP [2N] | cw [nwords] | R (if !RG) | S [M] (if the
+    // launch outputs Omega: the geometry then has room for it)
     unsigned long long* wcnt =
         reinterpret_cast<unsigned long long*>(smem + a.table_words + static_cast<size_t>(warp) * a.slot_words);
     float* st0 = reinterpret_cast<float*>(wcnt + 8);
     char* qp = reinterpret_cast<char*>(st0);
-    float* S = st0 + 2 * N;
-    uint32_t* cw = reinterpret_cast<uint32_t*>(S + C.M);
+    uint32_t* cw = reinterpret_cast<uint32_t*>(st0 + 2 * N);
     const int rwords = C.nent * K * 32;
-    float* Rw = RG ? a.rstate + (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * a.r_words
-                   : reinterpret_cast<float*>(cw + ((C.nwords + 3) & ~3));
+    float* const Rs = reinterpret_cast<float*>(cw + ((C.nwords + 3) & ~3));
+    float* Rw = RG ? a.rstate + (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * a.r_words : Rs;
+    float* S = RG ? Rs : Rs + rwords;
     const Lane lane{0, 0, 0, Z * 8, 0, 0, 4 * a.slot_words, 0, a.phi_m19, a.phi_one};
     if (l < 8) wcnt[l] = 0ull;
     __syncthreads();
@@ -230,7 +313,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
     const bool belief = a.stop_rule <= 1;
     const int W = (a.stop_rule == 1) ? N : C.M;               // R4
     const bool ber = a.mode == MODE_BER_SIM;
-    const bool keep_S = a.omega != nullptr;                   // S only feeds the Omega output
+    const bool keep_S = a.omega != nullptr && !LBP;           // S only feeds the Omega output (none for LBP)
     const uint32_t key0 = static_cast<uint32_t>(a.seed), key1 = static_cast<uint32_t>(a.seed >> 32);
     unsigned long long bit_err = 0;                           // this lane's share (ber_sim)
 
@@ -329,7 +412,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                     uint32_t p0 = 0;
                     for (int i = 0; i < C.core; ++i) {
                         const uint32_t lam = info_parity<8>(ent, row_ptr, i, rk[k], Z, C.K, cw);
-                        S[i * Z + rk[k]] = __uint_as_float(lam);
+                        Qs[2 * (i * Z + rk[k]) + 1] = __uint_as_float(lam);   // lambda_i[r], kept in an H word
                         p0 ^= lam;
                     }
                     Qs[2 * (C.kb * Z + rk[k])] = p0 ? -1.0f : 1.0f;
@@ -341,7 +424,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                     const int r = rk[k];
                     uint32_t pprev = 0;
                     for (int t = 1; t < C.core; ++t) {
-                        uint32_t pt = __float_as_uint(S[(t - 1) * Z + r]);
+                        uint32_t pt = __float_as_uint(Qs[2 * ((t - 1) * Z + r) + 1]);
                         if (t >= 2) pt ^= pprev;
                         const int s0 = pshift[t - 1];
                         if (s0 >= 0) {
@@ -358,13 +441,10 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                     }
                 }
                 __syncwarp();
-                for (int w = l; w < C.nwords; w += 32) {      // transmitted codeword words
-                    uint32_t word = 0;
-                    for (int b = 0; b < 32; ++b) {
-                        const int v = 32 * w + b;
-                        if (v < N && Qs[2 * v] < 0.0f) word |= 1u << b;
-                    }
-                    cw[w] = word;
+                for (int w = 0; w < C.nwords; ++w) {          // transmitted codeword words: one ballot each
+                    const int v = 32 * w + l;
+                    const unsigned word = __ballot_sync(kFull, v < N && Qs[2 * v] < 0.0f);
+                    if (l == 0) cw[w] = word;
                 }
                 __syncwarp();
             }
@@ -405,33 +485,13 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
             for (int i = 0; i < mb; ++i) {
                 const int e0 = row_ptr[i], dc = row_ptr[i + 1] - e0;
                 // the window can fill in this row: keep what a mid-row stop has to roll back
-                const bool fire_possible = belief && W - consec - 1 < Z;
-                const bool keep = keep_S && fire_possible;
-                SlotVals<K, uint32_t> oldb;
-                SlotVals<K, float> sold, snew;
-                int first_bad = Z, last_bad = -1;
-#pragma unroll 1
-                for (int k = 0; k < K; ++k) {
-                    const int r = l + k * Lk;
-                    const bool v = l < Lk && r < Z;
-                    const int rr = v ? r : Z - 1;
-                    if (keep) sold.set(k, S[i * Z + rr]);
-                    RowAcc<1> acc;
-                    wrow_dispatch<K, ALG>(dc, ent, ptab, e0, rr * 8, v, lane, static_cast<TexH>(C.phi_tex), qp,
-                                          Rw + static_cast<size_t>(e0) * K * 32 + k * 32 + l, acc);
-                    const float sn = __uint_as_float(__float_as_uint(acc.Ssum[0]) | (acc.negw[0] & kSign));
-                    if (keep_S && !LBP && v) S[i * Z + rr] = sn;                     // equ_s4e23
-                    if (fire_possible) {
-                        oldb.set(k, acc.oldbits[0]);
-                        snew.set(k, sn);
-                    }
-                    // Step 2(3) flags of this slot's check (equ_s4e2, equ_s4e24)
-                    const unsigned m = __ballot_sync(kFull, v && (((acc.negw[0] | acc.flipw[0]) & kSign) != 0u));
-                    if (m) {
-                        first_bad = min(first_bad, k * Lk + __ffs(m) - 1);
-                        last_bad = max(last_bad, k * Lk + 31 - __clz(m));
-                    }
-                }
+                WCtx cx{l, Lk, Z, belief && W - consec - 1 < Z, keep_S, qp,
+                        Rw + static_cast<size_t>(e0) * K * 32 + l, S + i * Z};
+                WRow<K> ro;
+                ro.first_bad = Z;
+                ro.last_bad = -1;
+                wrow_dispatch<K, ALG, TM>(dc, ent, ptab, e0, lane, static_cast<TexH>(C.phi_tex), cx, ro);
+                const int first_bad = ro.first_bad, last_bad = ro.last_bad;
                 __syncwarp();
                 if (!belief) {
                     ev += static_cast<long long>(dc) * Z;
@@ -451,8 +511,8 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 for (int k = 0; k < K; ++k) {
                     newbits.v[k] = 0;
                     if (vk[k] && rk[k] > rstar) {
-                        newbits.v[k] = swap_bits(rq[k], e0, dc, oldb.v[k]);
-                        if (keep_S && !LBP) S[i * Z + rk[k]] = sold.v[k];
+                        newbits.v[k] = swap_bits(rq[k], e0, dc, ro.oldb.v[k]);
+                        if (keep_S && !LBP) S[i * Z + rk[k]] = ro.sold.v[k];
                     }
                 }
                 __syncwarp();
@@ -468,7 +528,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 for (int k = 0; k < K; ++k)
                     if (vk[k] && rk[k] > rstar) {
                         swap_bits(rq[k], e0, dc, newbits.v[k]);
-                        if (keep_S && !LBP) S[i * Z + rk[k]] = snew.v[k];
+                        if (keep_S && !LBP) S[i * Z + rk[k]] = ro.snew.v[k];
                     }
                 __syncwarp();
             }
@@ -485,22 +545,24 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
         if (!conv) synd_zero = !syndrome_nz();
         const uint8_t flags = static_cast<uint8_t>((conv ? 1 : 0) | (synd_zero ? 2 : 0) | (fires > 0 ? 4 : 0));
         if (!ber) {
+            // packed hard decisions (sign of H), one ballot per word: lane l reads variable 32 w + l
             uint32_t* out = a.bits + static_cast<size_t>(f) * a.ld_words;
-            for (int w = l; w < a.ld_words; w += 32) {
-                uint32_t word = 0;
-                if (w < C.nwords)
-                    for (int b = 0; b < 32; ++b) {
-                        const int v = 32 * w + b;
-                        if (v < N) word |= (__float_as_uint(st0[2 * v + 1]) >> 31) << b;
-                    }
-                out[w] = word;
+            for (int w = 0; w < a.ld_words; ++w) {
+                const int v = 32 * w + l;
+                const unsigned word = __ballot_sync(kFull, v < N && (__float_as_uint(st0[2 * v + 1]) >> 31));
+                if (l == (w & 31)) out[w] = word;
             }
             if (a.omega) {
                 float* om = a.omega + static_cast<size_t>(f) * C.M;
                 for (int c = l; c < C.M; c += 32) {
+                    if (LBP) {
+                        om[c] = 0.0f;                         // layered BP: no check-beliefs
+                        continue;
+                    }
                     const float Sv = S[c];
-                    const float m = LBP ? 0.0f : phi32(fabsf(Sv), ptab, a.phi_m19, a.phi_one);   // Omega = sgn phi(S)
-                    om[c] = LBP ? 0.0f : ((__float_as_uint(Sv) >> 31) ? -m : m);
+                    const float m = TEXB ? phi32_tex(fabsf(Sv), static_cast<TexH>(C.phi_tex), a.phi_m19, a.phi_one)
+                                         : phi32(fabsf(Sv), ptab, a.phi_m19, a.phi_one);   // Omega = sgn phi(S)
+                    om[c] = (__float_as_uint(Sv) >> 31) ? -m : m;
                 }
             }
             if (l == 0) {
@@ -509,22 +571,18 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 if (a.ev) a.ev[f] = ev;
             }
         } else {
+            // decided vs sent: lane l compares variable 32 w + l, a ballot counts the word's errors
             bool info_err = false, cw_err = false;
-            for (int w = l; w < C.nwords; w += 32) {
-                uint32_t word = 0;
-                for (int b = 0; b < 32; ++b) {
-                    const int v = 32 * w + b;
-                    if (v < N) word |= (__float_as_uint(st0[2 * v + 1]) >> 31) << b;
-                }
-                const uint32_t d = word ^ cw[w];
-                uint32_t im = 0;
-                if (32 * w + 32 <= C.K) im = kFull;
-                else if (32 * w < C.K) im = (1u << (C.K - 32 * w)) - 1u;
-                bit_err += __popc(d & im);
-                info_err |= (d & im) != 0u;
+            for (int w = 0; w < C.nwords; ++w) {
+                const int v = 32 * w + l;
+                const bool dv = v < N && ((__float_as_uint(st0[2 * v + 1]) >> 31) != ((cw[w] >> l) & 1u));
+                const unsigned d = __ballot_sync(kFull, dv);
+                const unsigned ie = __ballot_sync(kFull, dv && v < C.K);
+                bit_err += (l == 0) ? __popc(ie) : 0;
+                info_err |= ie != 0u;
                 cw_err |= d != 0u;
             }
-            const bool fe = __any_sync(kFull, info_err), ce = __any_sync(kFull, cw_err);
+            const bool fe = info_err, ce = cw_err;
             if (l == 0) {
                 wcnt[0] += 1;
                 wcnt[2] += fe;
@@ -549,38 +607,45 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
 }
 
 // ---------------------------------------------------------------- launch of one instantiation
-template <int K, bool RG, int MAXT, int ALG>
+template <int K, bool RG, int MAXT, int ALG, int TM>
 static int wlaunch_t(const KernelArgs& a, const Geometry& g, int grid, cudaStream_t st)
 {
-    auto k = cbp_warp_kernel<K, RG, MAXT, ALG>;
+    auto k = cbp_warp_kernel<K, RG, MAXT, ALG, TM>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
     k<<<grid, g.threads, g.smem_bytes, st>>>(a);
     return static_cast<int>(cudaGetLastError());
 }
 
-template <int K, bool RG, int MAXT, int ALG>
+template <int K, bool RG, int MAXT, int ALG, int TM>
 static int wocc_t(const Geometry& g, int* out)
 {
-    auto k = cbp_warp_kernel<K, RG, MAXT, ALG>;
+    auto k = cbp_warp_kernel<K, RG, MAXT, ALG, TM>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
     return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, g.threads, g.smem_bytes));
 }
 
-// K = 1: up to 512 threads (128 registers); K = 2..4: up to 384 threads (170 registers)
+// K = 1: up to CBP_WARPK1_MAXT threads (512: 128 registers); K = 2..4: CBP_WARPK_MAXT (384: 170 registers)
 template <int ALG>
 static int wdispatch(const Geometry& g, const KernelArgs* a, int grid, cudaStream_t st, int* occ)
 {
     const bool rg = g.r_global != 0;
-#define CBP_W(KK, MT)                                                                                     \
-    if (g.kslots == KK)                                                                                   \
-        return occ ? (rg ? wocc_t<KK, true, MT, ALG>(g, occ) : wocc_t<KK, false, MT, ALG>(g, occ))        \
-                   : (rg ? wlaunch_t<KK, true, MT, ALG>(*a, g, grid, st) : wlaunch_t<KK, false, MT, ALG>(*a, g, grid, st));
-    CBP_W(1, 512)
-    CBP_W(2, 384)
-    CBP_W(3, 384)
-    CBP_W(4, 384)
+    const int tm = g.tex2;                    // 0 C2B through TEX, 1 both, 2 none
+#define CBP_WT(KK, RGV, MT)                                                                                   \
+    if (tm == 1) return occ ? wocc_t<KK, RGV, MT, ALG, 1>(g, occ) : wlaunch_t<KK, RGV, MT, ALG, 1>(*a, g, grid, st); \
+    if (tm == 2) return occ ? wocc_t<KK, RGV, MT, ALG, 2>(g, occ) : wlaunch_t<KK, RGV, MT, ALG, 2>(*a, g, grid, st); \
+    return occ ? wocc_t<KK, RGV, MT, ALG, 0>(g, occ) : wlaunch_t<KK, RGV, MT, ALG, 0>(*a, g, grid, st);
+#define CBP_W(KK, MT)                 \
+    if (g.kslots == KK) {             \
+        if (rg) { CBP_WT(KK, true, MT) } \
+        CBP_WT(KK, false, MT)         \
+    }
+    CBP_W(1, CBP_WARPK1_MAXT)
+    CBP_W(2, CBP_WARPK_MAXT)
+    CBP_W(3, CBP_WARPK_MAXT)
+    CBP_W(4, CBP_WARPK_MAXT)
+#undef CBP_WT
 #undef CBP_W
     return static_cast<int>(cudaErrorInvalidConfiguration);
 }
