@@ -357,6 +357,26 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         cbp::Geometry G{};
         G.alg = alg;
         G.P = P;
+        if (use_warp && allow_warp && (alg == 0 || alg == 2) && P == 1 && Z > 128 && Z <= 512 && tex2_env < 0) {
+            // cbp_warp_kernel with the per-warp state in a global slot (frames too large for shared memory:
+            // C4 0.6 MB): K in {8, 12, 16} check slots per lane, tables only in shared memory
+            G.wk = 1;
+            const int kmin = (Z + 31) / 32;
+            G.kslots = kmin <= 8 ? 8 : (kmin <= 12 ? 12 : 16);
+            G.lanes = (Z + G.kslots - 1) / G.kslots;
+            G.multi = 0; G.F = 1; G.Zp = 32; G.team_threads = 32; G.state_in_smem = 0; G.r_global = 1;
+            G.tex2 = 0;
+            const int64_t rw = static_cast<int64_t>(nent) * G.kslots * 32;
+            G.table_words = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4 + 4;
+            G.r_words = 0;
+            G.slot_words = static_cast<int32_t>((16 + 2LL * c->N + (nwords + 3) / 4 * 4 + rw + (with_S ? c->M : 0) + 3) / 4 * 4);
+            const char* gw = std::getenv("CBP_GS_WARPS");      // A/B runs: warps per CTA
+            const int gwn = gw ? std::atoi(gw) : 0;
+            G.teams = (gwn >= 1 && gwn <= CBP_WARPK_MAXT / 32) ? gwn : CBP_WARPK_MAXT / 32;
+            G.threads = 32 * G.teams;
+            G.smem_bytes = static_cast<int32_t>(4LL * G.table_words);
+            return G;
+        }
         if (use_warp && allow_warp && (alg == 0 || alg == 2) && P == 1 && Z >= 17 && Z <= 128) {
             // cbp_warp_kernel: one frame per warp, K = ceil(Z/32) check slots per lane
             G.wk = 1;

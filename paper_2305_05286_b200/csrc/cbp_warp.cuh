@@ -256,7 +256,9 @@ __device__ __forceinline__ void wrow_dispatch(int dc, const int4* __restrict__ e
 // int8 LLRs from HBM) and the fused ber_sim; cbp_channel runs on cbp_kernel.
 // TM: phi table rows for C2B / B2V through the texture pipe (0: C2B only, 1: both -- the table
 // is then not staged in shared memory, 2: neither).
-template <int K, bool RG, int MAXT, int ALG, int TM>
+// GS: the warp's whole state (counters, QP, codeword, R, S) in a global slot per warp (large frames:
+// C4's 0.6 MB does not fit on chip; L2 / HBM-served, coalesced), shared memory holds the tables only.
+template <int K, bool RG, int MAXT, int ALG, int TM, bool GS = false>
 __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant__ KernelArgs a)
 {
     constexpr bool TEXB = TM == 1;
@@ -297,16 +299,19 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
     // per-warp shared state: counters (8 x u64) | QP [2N] | cw [nwords] | R (if !RG) | S [M] (if the
     // launch outputs Omega: the geometry then has room for it)
     unsigned long long* wcnt =
-        reinterpret_cast<unsigned long long*>(smem + a.table_words + static_cast<size_t>(warp) * a.slot_words);
+        GS ? reinterpret_cast<unsigned long long*>(a.gstate + (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp) *
+                                                               static_cast<size_t>(a.slot_words))
+           : reinterpret_cast<unsigned long long*>(smem + a.table_words + static_cast<size_t>(warp) * a.slot_words);
     float* st0 = reinterpret_cast<float*>(wcnt + 8);
     char* qp = reinterpret_cast<char*>(st0);
     uint32_t* cw = reinterpret_cast<uint32_t*>(st0 + 2 * N);
     const int rwords = C.nent * K * 32;
     float* const Rs = reinterpret_cast<float*>(cw + ((C.nwords + 3) & ~3));
-    float* Rw = RG ? a.rstate + (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * a.r_words : Rs;
-    float* S = RG ? Rs : Rs + rwords;
+    float* Rw = (RG && !GS) ? a.rstate + (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * a.r_words : Rs;
+    float* S = (RG && !GS) ? Rs : Rs + rwords;
     const Lane lane{0, 0, 0, Z * 8, 0, 0, 4 * a.slot_words, 0, a.phi_m19, a.phi_one};
     if (l < 8) wcnt[l] = 0ull;
+    __syncwarp();
     __syncthreads();
     mbar_wait(bar, 0);
 
@@ -607,20 +612,20 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
 }
 
 // ---------------------------------------------------------------- launch of one instantiation
-template <int K, bool RG, int MAXT, int ALG, int TM>
+template <int K, bool RG, int MAXT, int ALG, int TM, bool GS = false>
 static int wlaunch_t(const KernelArgs& a, const Geometry& g, int grid, cudaStream_t st)
 {
-    auto k = cbp_warp_kernel<K, RG, MAXT, ALG, TM>;
+    auto k = cbp_warp_kernel<K, RG, MAXT, ALG, TM, GS>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
     k<<<grid, g.threads, g.smem_bytes, st>>>(a);
     return static_cast<int>(cudaGetLastError());
 }
 
-template <int K, bool RG, int MAXT, int ALG, int TM>
+template <int K, bool RG, int MAXT, int ALG, int TM, bool GS = false>
 static int wocc_t(const Geometry& g, int* out)
 {
-    auto k = cbp_warp_kernel<K, RG, MAXT, ALG, TM>;
+    auto k = cbp_warp_kernel<K, RG, MAXT, ALG, TM, GS>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
     return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, g.threads, g.smem_bytes));
@@ -632,6 +637,17 @@ static int wdispatch(const Geometry& g, const KernelArgs* a, int grid, cudaStrea
 {
     const bool rg = g.r_global != 0;
     const int tm = g.tex2;                    // 0 C2B through TEX, 1 both, 2 none
+    if (!g.state_in_smem) {                   // global-state warps (129 <= Z <= 512)
+#define CBP_WG(KK)                                                                                            \
+        if (g.kslots == KK)                                                                                   \
+            return occ ? wocc_t<KK, true, CBP_WARPK_MAXT, ALG, 0, true>(g, occ)                                 \
+                       : wlaunch_t<KK, true, CBP_WARPK_MAXT, ALG, 0, true>(*a, g, grid, st);
+        CBP_WG(8)
+        CBP_WG(12)
+        CBP_WG(16)
+#undef CBP_WG
+        return static_cast<int>(cudaErrorInvalidConfiguration);
+    }
 #define CBP_WT(KK, RGV, MT)                                                                                   \
     if (tm == 1) return occ ? wocc_t<KK, RGV, MT, ALG, 1>(g, occ) : wlaunch_t<KK, RGV, MT, ALG, 1>(*a, g, grid, st); \
     if (tm == 2) return occ ? wocc_t<KK, RGV, MT, ALG, 2>(g, occ) : wlaunch_t<KK, RGV, MT, ALG, 2>(*a, g, grid, st); \

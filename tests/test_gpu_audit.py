@@ -54,9 +54,10 @@ def _oracle_frames(job):
     return out
 
 
-def _gpu_pass(g, eb, seed, frames, mi, llr_mode, sample_set, chunk=1 << 20):
-    """Decode every frame on the GPU; return per-frame outputs of the flagged frames (up to CAP,
-    in frame order) and of the sample, and the total flagged count."""
+def _gpu_pass(g, eb, seed, frames, mi, llr_mode, sample_set, chunk=1 << 20, cap=None):
+    """Decode every frame on the GPU; return per-frame outputs of the flagged frames (up to `cap`,
+    default CAP, in frame order) and of the sample, and the total flagged count."""
+    cap = CAP if cap is None else cap
     keep, n_flag, words = {}, 0, g.words
     sample = torch.as_tensor(sorted(sample_set), dtype=torch.int64)
     for b in range(0, frames, chunk):
@@ -69,7 +70,7 @@ def _gpu_pass(g, eb, seed, frames, mi, llr_mode, sample_set, chunk=1 << 20):
         flagged = wrong | ((fl & 1) == 0) | ((fl & 4) != 0)
         idx = torch.nonzero(flagged).flatten()
         n_flag += int(idx.numel())
-        room = CAP - sum(1 for v in keep.values() if v[4])
+        room = cap - sum(1 for v in keep.values() if v[4])
         idx = idx[:max(room, 0)]
         s = sample[(sample >= b) & (sample < b + n)].to(idx.device) - b
         for sel, is_flag in ((idx, True), (s, False)):
@@ -123,3 +124,32 @@ def test_parity_audit(name, ebs, frames, llr_mode):
     out = os.environ.get("CBP_AUDIT_OUT")
     if out:
         Path(out).write_text(json.dumps({"what": __doc__.split("\n\n")[0], "audits": _REPORT}, indent=1) + "\n")
+
+
+@pytest.mark.parametrize("llr_mode", [0, 1], ids=["fp32", "int8"])
+def test_parity_audit_bench_slice(llr_mode):
+    """Frame-by-frame parity on the bench's own workload, run by default (the full audit above
+    needs CBP_AUDIT): the first bench step of C5 (BASELINE configs[4]: global frames [0, 4e6) at
+    2.5 dB) is decoded on the GPU; every flagged frame (error, not converged or failed
+    verification; all of them up to 5000) and 3000 uniform samples are decoded again by the
+    oracle and compared bit for bit (bits, iterations, flags, edge visits)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    base, Z = inputs.config_base("C5")
+    g = cbp.Code(base, Z)
+    mi, frames = 30, 4_000_000
+    rng = np.random.default_rng(7 + llr_mode)
+    sample = set(rng.integers(0, frames, 3000).tolist())
+    keep, n_flag = _gpu_pass(g, 2.5, 1, frames, mi, llr_mode, sample, cap=5000)
+    assert n_flag <= 5000, n_flag                              # every flagged frame is checked
+    order = sorted(keep)
+    jobs = [("C5", 2.5, 1, llr_mode, mi, order[k:k + 32]) for k in range(0, len(order), 32)]
+    bad = []
+    with mp.get_context("fork").Pool(os.cpu_count() or 1) as pool:
+        for res in pool.imap_unordered(_oracle_frames, jobs, chunksize=1):
+            for f, bits, it, fl, ev in res:
+                gb, gi, gf, gev, _ = keep[f]
+                if not ((gb == bits).all() and gi == it and gf == fl and gev == ev):
+                    bad.append(f)
+    assert not bad, sorted(bad)[:10]
+    assert len(keep) >= 3000
