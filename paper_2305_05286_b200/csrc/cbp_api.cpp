@@ -357,7 +357,11 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         cbp::Geometry G{};
         G.alg = alg;
         G.P = P;
-        if (use_warp && allow_warp && (alg == 0 || alg == 2) && P == 1 && Z > 128 && Z <= 512 && tex2_env < 0) {
+        // global-state warps for Z > 128: measured slower than cbp_kernel's global-state teams (C4 83 vs 66 ms
+        // per 3000 frames), so only on request (CBP_WARP_GS=1, A/B runs)
+        const char* gsv = std::getenv("CBP_WARP_GS");
+        const bool gs_on = gsv && gsv[0] == '1' && gsv[1] == 0;
+        if (use_warp && allow_warp && gs_on && (alg == 0 || alg == 2) && P == 1 && Z > 128 && Z <= 512 && tex2_env < 0) {
             // cbp_warp_kernel with the per-warp state in a global slot (frames too large for shared memory:
             // C4 0.6 MB): K in {8, 12, 16} check slots per lane, tables only in shared memory
             G.wk = 1;
@@ -395,6 +399,28 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
                 return static_cast<int>(std::min<int64_t>(w, maxt / 32));
             };
             const int ws = warps_of(false), wg = warps_of(true);
+            if (std::max(ws, wg) < 6 && !gs_on) {
+                // frames too large for 6 per SM even with R in global memory (P8192: 3 warps): cbp_kernel's
+                // global-state teams (8 per SM) measured faster than global-state warps (44.9 vs 48.0 ms)
+                G = cbp::Geometry{};
+                G.alg = alg;
+                G.P = P;
+                goto team_geometry;
+            }
+            if (std::max(ws, wg) < 6 && G.kslots >= 2 && tex2_env < 0 && split_r_env < 0) {
+                // frames too large for 6 per SM even with R in global memory (P8192: 3): the whole
+                // per-warp state in a global slot, 12 warps per SM
+                G.state_in_smem = 0;
+                G.r_global = 1;
+                G.r_words = 0;
+                G.tex2 = 0;
+                G.table_words = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4 + 4;
+                G.slot_words = static_cast<int32_t>((16 + 2LL * c->N + (nwords + 3) / 4 * 4 + rw + (with_S ? c->M : 0) + 3) / 4 * 4);
+                G.teams = CBP_WARPK_MAXT / 32;
+                G.threads = 32 * G.teams;
+                G.smem_bytes = static_cast<int32_t>(4LL * G.table_words);
+                return G;
+            }
             // R in global memory (coalesced, L1/L2-served) when shared memory holds fewer than 8 frames
             bool rg = ws < 8 && wg > ws;
             if (split_r_env == 0) rg = false;
@@ -410,6 +436,7 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
                 return G;
             }
         }
+    team_geometry:
         if (Z <= 16) {
             int zp = 1;
             while (zp < Z) zp <<= 1;

@@ -364,16 +364,80 @@ __device__ __forceinline__ RowAcc<P> cbp_row_reg(const int4* __restrict__ ent, c
     return acc;
 }
 
-// The same update for rows longer than CBP_DC_REG: chunks of 4 edges; between the phases each
-// variable's slot parks {Q^new, Phi | sign of the decision} (only this lane touches the variable
-// during the row).  Both phi lookups from the shared-memory table (a function that is not inlined
-// cannot keep the texture handle in a uniform register).
+// The same update for rows longer than CBP_DC_REG: two passes in chunks of U edges (all loads of
+// a chunk first: U independent phi chains) and a remainder one edge at a time; between the phases
+// each variable's slot parks {Q^new, Phi | sign of the decision} (only this lane touches the
+// variable during the row).  Both phi rows from the shared-memory table (a function that is not
+// inlined cannot keep the texture handle in a uniform register).
+template <int U, int P, int ALG>
+__device__ __forceinline__ void park_p1(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int k0,
+                                        int rrow, const Lane& L, const Grp<P, ALG>& g, RowAcc<P>& acc)
+{
+    constexpr bool LBP = ALG == 2;
+    int a[U];
+    float qp[U][2 * P], ro[U][P], q[U][P], ph[U][P];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + k0 + u));
+        a[u] = A.x + wrap(L.rq + A.y, L.ZQ);
+        ldf<2 * P>(g.qp, a[u], qp[u]);
+        ldf<P>(g.rb, rrow + (k0 + u) * L.ZR, ro[u]);
+        if (LBP) {
+#pragma unroll
+            for (int p = 0; p < P; ++p) qp[u][P + p] = qp[u][p];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) cbp_phase1<P, false>(qp[u], ro[u], q[u], ph[u], ptab, L, 0, acc);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        float st[2 * P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            st[p] = q[u][p];
+            st[P + p] = __uint_as_float(__float_as_uint(ph[u][p]) | (__float_as_uint(qp[u][p]) & kSign));
+        }
+        stf<2 * P>(g.qp, a[u], st);
+    }
+}
+
+template <int U, int P, int ALG>
+__device__ __forceinline__ void park_p2(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int k0,
+                                        int rrow, const Lane& L, const Grp<P, ALG>& g, const RowAcc<P>& acc)
+{
+    constexpr bool LBP = ALG == 2;
+    int a[U];
+    float qp[U][2 * P];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + k0 + u));
+        a[u] = A.x + wrap(L.rq + A.y, L.ZQ);
+        ldf<2 * P>(g.qp, a[u], qp[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        float q[P], ph[P], rn[P], lamn[P], st[2 * P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            q[p] = qp[u][p];
+            ph[p] = fabsf(qp[u][P + p]);
+        }
+        cbp_phase2<P, false>(acc, q, ph, rn, lamn, ptab, L, 0);
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            st[p] = lamn[p];
+            st[P + p] = LBP ? lamn[p] : qp[u][P + p];          // sign = the decision of this visit
+        }
+        stf<2 * P>(g.qp, a[u], st);
+        stf<P>(g.rb, rrow + (k0 + u) * L.ZR, rn);
+    }
+}
+
 template <int P, int ALG>
 __device__ __noinline__ RowAcc<P> cbp_row_park(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
                                                int dc, const Lane& L, const Grp<P, ALG>& g)
 {
     constexpr int U = 4;
-    constexpr bool LBP = ALG == 2;
     RowAcc<P> acc;
 #pragma unroll
     for (int p = 0; p < P; ++p) {
@@ -381,55 +445,16 @@ __device__ __noinline__ RowAcc<P> cbp_row_park(const int4* __restrict__ ent, con
         acc.negw[p] = acc.flipw[p] = acc.oldbits[p] = 0u;
     }
     const int rrow = r_slot(L, e0);
-    for (int k0 = 0; k0 < dc; k0 += U) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int k = k0 + u;
-            if (k >= dc) break;
-            const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + k));
-            const int a = A.x + wrap(L.rq + A.y, L.ZQ);
-            float qp[2 * P], ro[P], q[P], ph[P];
-            ldf<2 * P>(g.qp, a, qp);
-            ldf<P>(g.rb, rrow + k * L.ZR, ro);
-            if (LBP) {
-#pragma unroll
-                for (int p = 0; p < P; ++p) qp[P + p] = qp[p];
-            }
-            cbp_phase1<P, false>(qp, ro, q, ph, ptab, L, 0, acc);
-            float st[2 * P];
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                st[p] = q[p];
-                st[P + p] = __uint_as_float(__float_as_uint(ph[p]) | (__float_as_uint(qp[p]) & kSign));
-            }
-            stf<2 * P>(g.qp, a, st);
-        }
-    }
-    for (int k0 = 0; k0 < dc; k0 += U) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int k = k0 + u;
-            if (k >= dc) break;
-            const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + k));
-            const int a = A.x + wrap(L.rq + A.y, L.ZQ);
-            float qp[2 * P], q[P], ph[P], rn[P], lamn[P];
-            ldf<2 * P>(g.qp, a, qp);
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                q[p] = qp[p];
-                ph[p] = fabsf(qp[P + p]);
-            }
-            cbp_phase2<P, false>(acc, q, ph, rn, lamn, ptab, L, 0);
-            float st[2 * P];
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                st[p] = lamn[p];
-                st[P + p] = LBP ? lamn[p] : qp[P + p];          // sign = the decision of this visit
-            }
-            stf<2 * P>(g.qp, a, st);
-            stf<P>(g.rb, rrow + k * L.ZR, rn);
-        }
-    }
+    int k = 0;
+#pragma unroll 1
+    for (; k + U <= dc; k += U) park_p1<U, P, ALG>(ent, ptab, e0, k, rrow, L, g, acc);
+#pragma unroll 1
+    for (; k < dc; ++k) park_p1<1, P, ALG>(ent, ptab, e0, k, rrow, L, g, acc);
+    k = 0;
+#pragma unroll 1
+    for (; k + U <= dc; k += U) park_p2<U, P, ALG>(ent, ptab, e0, k, rrow, L, g, acc);
+#pragma unroll 1
+    for (; k < dc; ++k) park_p2<1, P, ALG>(ent, ptab, e0, k, rrow, L, g, acc);
     return acc;
 }
 

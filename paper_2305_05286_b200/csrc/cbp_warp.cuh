@@ -179,18 +179,68 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
     }
 }
 
-// Rows longer than CBP_DC_REG: per slot two passes over the edges, parking {Q^new, Phi | sign
-// of the decision} in the variable's slot between the phases (only this lane touches the
-// variable during the row).  (Chunks of 4 edges with masked tails measured 8 % slower on C3b.)
+// Rows longer than CBP_DC_REG: per slot two passes over the edges in chunks of U (all loads of a
+// chunk first, U independent phi chains), a remainder one edge at a time, parking {Q^new,
+// Phi | sign of the decision} in the variable's slot between the phases (only this lane touches
+// the variable during the row).  Both phi rows from the shared-memory table.
+template <int U, int K, int ALG>
+__device__ __forceinline__ void wpark_p1(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int e,
+                                         int rr, bool v, const Lane& L, const WCtx& c, float* rk, RowAcc<1>& acc)
+{
+    constexpr bool LBP = ALG == 2;
+    int a[U];
+    float vv[U][2], ro[U][1], q[U][1], ph[U][1];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e + u));
+        a[u] = A.x + wrap(rr * 8 + A.y, L.ZQ);
+        ldf<2>(c.qp, a[u], vv[u]);
+        ro[u][0] = rk[(e + u) * K * 32];
+        if (LBP) vv[u][1] = vv[u][0];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) cbp_phase1<1, false>(vv[u], ro[u], q[u], ph[u], ptab, L, 0, acc);
+    if (v) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float st[2] = {q[u][0], __uint_as_float(__float_as_uint(ph[u][0]) | (__float_as_uint(vv[u][0]) & kSign))};
+            stf<2>(c.qp, a[u], st);
+        }
+    }
+}
+
+template <int U, int K, int ALG>
+__device__ __forceinline__ void wpark_p2(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int e,
+                                         int rr, bool v, const Lane& L, const WCtx& c, float* rk, const RowAcc<1>& acc)
+{
+    constexpr bool LBP = ALG == 2;
+    int a[U];
+    float vv[U][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e + u));
+        a[u] = A.x + wrap(rr * 8 + A.y, L.ZQ);
+        ldf<2>(c.qp, a[u], vv[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const float q[1] = {vv[u][0]}, ph[1] = {fabsf(vv[u][1])};
+        float rn[1], lamn[1];
+        cbp_phase2<1, false>(acc, q, ph, rn, lamn, ptab, L, 0);
+        if (v) {
+            const float st[2] = {lamn[0], LBP ? lamn[0] : vv[u][1]};
+            stf<2>(c.qp, a[u], st);
+        }
+        rk[(e + u) * K * 32] = rn[0];
+    }
+}
+
 template <int K, int ALG, int TM>
 __device__ __forceinline__ void wrow_park(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int dc,
                                           const Lane& L, TexH tex, const WCtx& c, WRow<K>& o)
 {
-    constexpr bool LBP = ALG == 2;
-    // one edge at a time: the texture latency would be exposed on every edge, so both phi rows
-    // come from the shared-memory table (TEX for C2B here measured 30 % slower on C3b) unless
-    // the table is not staged (TM 1)
-    constexpr bool TEXC = TM == 1, TEXB = TM == 1;
+    constexpr int U = 4;
+    (void)tex;
 #pragma unroll 1
     for (int k = 0; k < K; ++k) {
         const int r = c.l + k * c.Lk;
@@ -201,32 +251,17 @@ __device__ __forceinline__ void wrow_park(const int4* __restrict__ ent, const fl
         RowAcc<1> acc;
         acc.Ssum[0] = 0.0f;
         acc.negw[0] = acc.flipw[0] = acc.oldbits[0] = 0u;
-        for (int e = 0; e < dc; ++e) {
-            const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e));
-            const int a = A.x + wrap(rr * 8 + A.y, L.ZQ);
-            float vv[2], ro[1] = {rk[e * K * 32]}, q[1], ph[1];
-            ldf<2>(c.qp, a, vv);
-            if (LBP) vv[1] = vv[0];
-            cbp_phase1<1, TEXC>(vv, ro, q, ph, ptab, L, tex, acc);
-            if (v) {
-                const float st[2] = {q[0], __uint_as_float(__float_as_uint(ph[0]) | (__float_as_uint(vv[0]) & kSign))};
-                stf<2>(c.qp, a, st);
-            }
-        }
-        for (int e = 0; e < dc; ++e) {
-            const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e));
-            const int a = A.x + wrap(rr * 8 + A.y, L.ZQ);
-            float vv[2], rn[1], lamn[1];
-            ldf<2>(c.qp, a, vv);
-            const float q[1] = {vv[0]}, ph[1] = {fabsf(vv[1])};
-            cbp_phase2<1, TEXB>(acc, q, ph, rn, lamn, ptab, L, tex);
-            if (v) {
-                const float st[2] = {lamn[0], LBP ? lamn[0] : vv[1]};
-                stf<2>(c.qp, a, st);
-            }
-            rk[e * K * 32] = rn[0];
-        }
-        wslot_done<K, LBP>(c, k, rr, v, acc, o);
+        int e = 0;
+#pragma unroll 1
+        for (; e + U <= dc; e += U) wpark_p1<U, K, ALG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
+#pragma unroll 1
+        for (; e < dc; ++e) wpark_p1<1, K, ALG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
+        e = 0;
+#pragma unroll 1
+        for (; e + U <= dc; e += U) wpark_p2<U, K, ALG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
+#pragma unroll 1
+        for (; e < dc; ++e) wpark_p2<1, K, ALG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
+        wslot_done<K, ALG == 2>(c, k, rr, v, acc, o);
     }
 }
 
@@ -642,6 +677,9 @@ static int wdispatch(const Geometry& g, const KernelArgs* a, int grid, cudaStrea
         if (g.kslots == KK)                                                                                   \
             return occ ? wocc_t<KK, true, CBP_WARPK_MAXT, ALG, 0, true>(g, occ)                                 \
                        : wlaunch_t<KK, true, CBP_WARPK_MAXT, ALG, 0, true>(*a, g, grid, st);
+        CBP_WG(2)
+        CBP_WG(3)
+        CBP_WG(4)
         CBP_WG(8)
         CBP_WG(12)
         CBP_WG(16)
