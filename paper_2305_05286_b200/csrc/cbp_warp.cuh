@@ -56,6 +56,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 }
 
 // ---------------------------------------------------------------- the rows
+#ifndef CBP_B2V_TEX_MASK
+#define CBP_B2V_TEX_MASK 0  // bit e: edge e (mod 8) of a row fetches its B2V phi row through TEX (A/B runs)
+#endif
 #ifndef CBP_WARP_LEAN
 #define CBP_WARP_LEAN 0     // 1: entries and R re-read per slot (fewer registers, A/B runs)
 #endif
@@ -85,6 +88,7 @@ struct WRow {
 struct WCtx {
     int l, Lk, Z;
     bool fire_possible, keepS;   // the window may fill in this row; S records are kept (Omega output)
+    bool r0;                     // sweep 1: every R_{c->v} still holds its initial 0 (equ_s4e17) -- not read
     char* qp;
     float* rrow;                 // this lane's R word of (row entry 0, slot 0); (edge e, slot k) at rrow[(e K + k) 32]
     float* Srow;                 // S records of this row (keepS)
@@ -126,7 +130,7 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
     // L2 latency then overlaps it); slot 0's are loaded here
     float rnext[DC];
 #pragma unroll
-    for (int e = 0; e < DC; ++e) rnext[e] = c.rrow[e * K * 32];
+    for (int e = 0; e < DC; ++e) rnext[e] = c.r0 ? 0.0f : c.rrow[e * K * 32];
 #endif
 #pragma unroll 1
     for (int k = 0; k < K; ++k) {
@@ -141,14 +145,14 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
 #pragma unroll
         for (int e = 0; e < DC; ++e) {
             A[e] = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e));
-            ro[e][0] = rk[e * K * 32];
+            ro[e][0] = c.r0 ? 0.0f : rk[e * K * 32];
         }
 #else
 #pragma unroll
         for (int e = 0; e < DC; ++e) ro[e][0] = rnext[e];          // R_{c->v}
         if (k + 1 < K) {
 #pragma unroll
-            for (int e = 0; e < DC; ++e) rnext[e] = rk[32 + e * K * 32];
+            for (int e = 0; e < DC; ++e) rnext[e] = c.r0 ? 0.0f : rk[32 + e * K * 32];
         }
 #endif
         RowAcc<1> acc;
@@ -168,7 +172,11 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
 #pragma unroll
         for (int e = 0; e < DC; ++e) {
             float rn[1], lamn[1];
-            cbp_phase2<1, TEXB>(acc, q[e], ph[e], rn, lamn, ptab, L, tex);
+            // B2V rows: through TEX for the edges CBP_B2V_TEX_MASK selects (balances the TEX and LSU pipes)
+            if (TEXB || (((CBP_B2V_TEX_MASK >> (e & 7)) & 1) != 0))   // folded after unrolling
+                cbp_phase2<1, true>(acc, q[e], ph[e], rn, lamn, ptab, L, tex);
+            else
+                cbp_phase2<1, false>(acc, q[e], ph[e], rn, lamn, ptab, L, tex);
             if (v) {
                 const float st[2] = {lamn[0], LBP ? lamn[0] : vs[e][0]};
                 stf<2>(c.qp, aqp[e], st);
@@ -195,7 +203,7 @@ __device__ __forceinline__ void wpark_p1(const int4* __restrict__ ent, const flo
         const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e + u));
         a[u] = A.x + wrap(rr * 8 + A.y, L.ZQ);
         ldf<2>(c.qp, a[u], vv[u]);
-        ro[u][0] = rk[(e + u) * K * 32];
+        ro[u][0] = c.r0 ? 0.0f : rk[(e + u) * K * 32];
         if (LBP) vv[u][1] = vv[u][0];
     }
 #pragma unroll
@@ -446,17 +454,37 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 // (a3) dual-diagonal encoder: systematic symbols, lambda_i[r] of the
                 // core rows (kept in S), p0 = XOR_i lambda_i, the parity chain, the extension
                 for (int v = l; v < C.K; v += 32) Qs[2 * v] = ((cw[v >> 5] >> (v & 31)) & 1u) ? -1.0f : 1.0f;
+                // lambda_i[r] = XOR of the info bits of check i Z + r: each entry read once per row for the K
+                // slots (kept in H words); p0 = XOR over the core rows
+                uint32_t p0[K];
 #pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    if (!vk[k]) continue;
-                    uint32_t p0 = 0;
-                    for (int i = 0; i < C.core; ++i) {
-                        const uint32_t lam = info_parity<8>(ent, row_ptr, i, rk[k], Z, C.K, cw);
-                        Qs[2 * (i * Z + rk[k]) + 1] = __uint_as_float(lam);   // lambda_i[r], kept in an H word
-                        p0 ^= lam;
+                for (int k = 0; k < K; ++k) p0[k] = 0u;
+                for (int i = 0; i < C.core; ++i) {
+                    uint32_t lam[K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) lam[k] = 0u;
+                    for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+                        const int jz = ent[2 * e].x >> 3;             // j Z (QS = 8)
+                        if (jz >= C.K) continue;                      // a parity column (warp-uniform)
+                        const int sft = ent[2 * e + 1].z >> 16;
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            int t = rk[k] + sft;
+                            t = (t >= Z) ? t - Z : t;
+                            const int v = jz + t;
+                            lam[k] ^= (cw[v >> 5] >> (v & 31)) & 1u;
+                        }
                     }
-                    Qs[2 * (C.kb * Z + rk[k])] = p0 ? -1.0f : 1.0f;
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+                        if (vk[k]) {
+                            Qs[2 * (i * Z + rk[k]) + 1] = __uint_as_float(lam[k]);
+                            p0[k] ^= lam[k];
+                        }
                 }
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    if (vk[k]) Qs[2 * (C.kb * Z + rk[k])] = p0[k] ? -1.0f : 1.0f;
                 __syncwarp();
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
@@ -511,7 +539,8 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 }
             }
         }
-        for (int w = l; w < rwords; w += 32) Rw[w] = 0.0f;    // equ_s4e17
+        // R = 0 (equ_s4e17) needs no stores: sweep 1 reads no R word (WCtx::r0), and every word is
+        // written in sweep 1 before sweep 2 reads it (a frame that stops in sweep 1 reads none)
         if (keep_S)
             for (int c = l; c < C.M; c += 32) S[c] = 0.0f;    // equ_s4e16: Omega = inf <=> S = 0
         __syncwarp();
@@ -525,7 +554,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
             for (int i = 0; i < mb; ++i) {
                 const int e0 = row_ptr[i], dc = row_ptr[i + 1] - e0;
                 // the window can fill in this row: keep what a mid-row stop has to roll back
-                WCtx cx{l, Lk, Z, belief && W - consec - 1 < Z, keep_S, qp,
+                WCtx cx{l, Lk, Z, belief && W - consec - 1 < Z, keep_S, sweep == 1, qp,
                         Rw + static_cast<size_t>(e0) * K * 32 + l, S + i * Z};
                 WRow<K> ro;
                 ro.first_bad = Z;
