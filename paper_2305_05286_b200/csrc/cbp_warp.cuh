@@ -62,6 +62,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 #ifndef CBP_WARP_LEAN
 #define CBP_WARP_LEAN 0     // 1: entries and R re-read per slot (fewer registers, A/B runs)
 #endif
+#ifndef CBP_R_CG
+#define CBP_R_CG 1          // R words in global memory: loads / stores cached in L2 only (keep L1 for the TEX phi rows)
+#endif
+// R word access: RG = R in the global workspace (L2-only when CBP_R_CG), else in shared memory
+template <bool RG>
+__device__ __forceinline__ float rld(const float* p)
+{
+    if constexpr (RG && CBP_R_CG) return __ldcg(p);
+    else return *p;
+}
+template <bool RG>
+__device__ __forceinline__ void rst(float* p, float v)
+{
+    if constexpr (RG && CBP_R_CG) __stcg(p, v);
+    else *p = v;
+}
+
 // K per-slot values in registers, written / read at a runtime slot index by predicated moves
 // (a dynamically indexed array would live in local memory)
 template <int K, typename T>
@@ -116,7 +133,7 @@ __device__ __forceinline__ void wslot_done(const WCtx& c, int k, int rr, bool v,
 // a loop that is not unrolled: the unrolled K x DC bodies overflowed the 32 KB L1.5 instruction
 // cache (ncu: no_instruction stalls 2.3 per issue, issue active 37 %).  A slot beyond Z (v false)
 // computes on check Z - 1 and stores nothing but its private R words.
-template <int DC, int K, int ALG, int TM>
+template <int DC, int K, int ALG, int TM, bool RG>
 __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
                                      const Lane& L, TexH tex, const WCtx& c, WRow<K>& o)
 {
@@ -130,7 +147,7 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
     // L2 latency then overlaps it); slot 0's are loaded here
     float rnext[DC];
 #pragma unroll
-    for (int e = 0; e < DC; ++e) rnext[e] = c.r0 ? 0.0f : c.rrow[e * K * 32];
+    for (int e = 0; e < DC; ++e) rnext[e] = c.r0 ? 0.0f : rld<RG>(c.rrow + e * K * 32);
 #endif
 #pragma unroll 1
     for (int k = 0; k < K; ++k) {
@@ -145,14 +162,14 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
 #pragma unroll
         for (int e = 0; e < DC; ++e) {
             A[e] = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e));
-            ro[e][0] = c.r0 ? 0.0f : rk[e * K * 32];
+            ro[e][0] = c.r0 ? 0.0f : rld<RG>(rk + e * K * 32);
         }
 #else
 #pragma unroll
         for (int e = 0; e < DC; ++e) ro[e][0] = rnext[e];          // R_{c->v}
         if (k + 1 < K) {
 #pragma unroll
-            for (int e = 0; e < DC; ++e) rnext[e] = c.r0 ? 0.0f : rk[32 + e * K * 32];
+            for (int e = 0; e < DC; ++e) rnext[e] = c.r0 ? 0.0f : rld<RG>(rk + 32 + e * K * 32);
         }
 #endif
         RowAcc<1> acc;
@@ -181,7 +198,7 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
                 const float st[2] = {lamn[0], LBP ? lamn[0] : vs[e][0]};
                 stf<2>(c.qp, aqp[e], st);
             }
-            rk[e * K * 32] = rn[0];                                // equ_s4e22 commit of R_{c->v}
+            rst<RG>(rk + e * K * 32, rn[0]);                       // equ_s4e22 commit of R_{c->v}
         }
         wslot_done<K, LBP>(c, k, rr, v, acc, o);
     }
@@ -191,7 +208,7 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
 // chunk first, U independent phi chains), a remainder one edge at a time, parking {Q^new,
 // Phi | sign of the decision} in the variable's slot between the phases (only this lane touches
 // the variable during the row).  Both phi rows from the shared-memory table.
-template <int U, int K, int ALG>
+template <int U, int K, int ALG, bool RG>
 __device__ __forceinline__ void wpark_p1(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int e,
                                          int rr, bool v, const Lane& L, const WCtx& c, float* rk, RowAcc<1>& acc)
 {
@@ -203,7 +220,7 @@ __device__ __forceinline__ void wpark_p1(const int4* __restrict__ ent, const flo
         const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e + u));
         a[u] = A.x + wrap(rr * 8 + A.y, L.ZQ);
         ldf<2>(c.qp, a[u], vv[u]);
-        ro[u][0] = c.r0 ? 0.0f : rk[(e + u) * K * 32];
+        ro[u][0] = c.r0 ? 0.0f : rld<RG>(rk + (e + u) * K * 32);
         if (LBP) vv[u][1] = vv[u][0];
     }
 #pragma unroll
@@ -217,7 +234,7 @@ __device__ __forceinline__ void wpark_p1(const int4* __restrict__ ent, const flo
     }
 }
 
-template <int U, int K, int ALG>
+template <int U, int K, int ALG, bool RG>
 __device__ __forceinline__ void wpark_p2(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int e,
                                          int rr, bool v, const Lane& L, const WCtx& c, float* rk, const RowAcc<1>& acc)
 {
@@ -239,11 +256,11 @@ __device__ __forceinline__ void wpark_p2(const int4* __restrict__ ent, const flo
             const float st[2] = {lamn[0], LBP ? lamn[0] : vv[u][1]};
             stf<2>(c.qp, a[u], st);
         }
-        rk[(e + u) * K * 32] = rn[0];
+        rst<RG>(rk + (e + u) * K * 32, rn[0]);
     }
 }
 
-template <int K, int ALG, int TM>
+template <int K, int ALG, int TM, bool RG>
 __device__ __forceinline__ void wrow_park(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int dc,
                                           const Lane& L, TexH tex, const WCtx& c, WRow<K>& o)
 {
@@ -261,36 +278,36 @@ __device__ __forceinline__ void wrow_park(const int4* __restrict__ ent, const fl
         acc.negw[0] = acc.flipw[0] = acc.oldbits[0] = 0u;
         int e = 0;
 #pragma unroll 1
-        for (; e + U <= dc; e += U) wpark_p1<U, K, ALG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
+        for (; e + U <= dc; e += U) wpark_p1<U, K, ALG, RG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
 #pragma unroll 1
-        for (; e < dc; ++e) wpark_p1<1, K, ALG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
+        for (; e < dc; ++e) wpark_p1<1, K, ALG, RG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
         e = 0;
 #pragma unroll 1
-        for (; e + U <= dc; e += U) wpark_p2<U, K, ALG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
+        for (; e + U <= dc; e += U) wpark_p2<U, K, ALG, RG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
 #pragma unroll 1
-        for (; e < dc; ++e) wpark_p2<1, K, ALG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
+        for (; e < dc; ++e) wpark_p2<1, K, ALG, RG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
         wslot_done<K, ALG == 2>(c, k, rr, v, acc, o);
     }
 }
 
-template <int K, int ALG, int TM>
+template <int K, int ALG, int TM, bool RG>
 __device__ __forceinline__ void wrow_dispatch(int dc, const int4* __restrict__ ent, const float4* __restrict__ ptab,
                                               int e0, const Lane& L, TexH tex, const WCtx& c, WRow<K>& o)
 {
     switch (dc) {
 #if CBP_DC_REG >= 1
-    case 1: wrow<1, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
-    case 2: wrow<2, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
-    case 3: wrow<3, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
-    case 4: wrow<4, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
-    case 5: wrow<5, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
-    case 6: wrow<6, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
+    case 1: wrow<1, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
+    case 2: wrow<2, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
+    case 3: wrow<3, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
+    case 4: wrow<4, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
+    case 5: wrow<5, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
+    case 6: wrow<6, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
 #endif
 #if CBP_DC_REG >= 8
-    case 7: wrow<7, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
-    case 8: wrow<8, K, ALG, TM>(ent, ptab, e0, L, tex, c, o); break;
+    case 7: wrow<7, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
+    case 8: wrow<8, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
 #endif
-    default: wrow_park<K, ALG, TM>(ent, ptab, e0, dc, L, tex, c, o); break;
+    default: wrow_park<K, ALG, TM, RG>(ent, ptab, e0, dc, L, tex, c, o); break;
     }
 }
 
@@ -559,7 +576,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 WRow<K> ro;
                 ro.first_bad = Z;
                 ro.last_bad = -1;
-                wrow_dispatch<K, ALG, TM>(dc, ent, ptab, e0, lane, static_cast<TexH>(C.phi_tex), cx, ro);
+                wrow_dispatch<K, ALG, TM, RG || GS>(dc, ent, ptab, e0, lane, static_cast<TexH>(C.phi_tex), cx, ro);
                 const int first_bad = ro.first_bad, last_bad = ro.last_bad;
                 __syncwarp();
                 if (!belief) {
