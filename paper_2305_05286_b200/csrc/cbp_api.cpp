@@ -429,6 +429,8 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
             G.r_words = rg ? static_cast<int32_t>(rw) : 0;
             G.slot_words = static_cast<int32_t>(per_warp(rg));
             G.teams = rg ? wg : ws;
+            static const int warps_env = [] { const char* e = std::getenv("CBP_WARPS"); return e ? std::atoi(e) : 0; }();
+            if (warps_env > 0) G.teams = std::min(G.teams, warps_env);   // A/B runs: fewer warps, more L1
             if (G.teams < 1) { G.wk = 0; G.teams = 0; }
             else {
                 G.threads = 32 * G.teams;

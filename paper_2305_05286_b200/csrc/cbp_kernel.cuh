@@ -349,17 +349,21 @@ __device__ __forceinline__ RowAcc<P> cbp_row_reg(const int4* __restrict__ ent, c
     }
 #pragma unroll
     for (int k = 0; k < DC; ++k) cbp_phase1<P>(vs[k], ro[k], q[k], ph[k], ptab, L, tex, acc);
+    // all B2V lookups before the first store (a table load may not move above a shared-memory
+    // store the compiler cannot prove disjoint)
+    float rn[DC][P], lamn[DC][P];
+#pragma unroll
+    for (int k = 0; k < DC; ++k) cbp_phase2<P>(acc, q[k], ph[k], rn[k], lamn[k], ptab, L, tex);
 #pragma unroll
     for (int k = 0; k < DC; ++k) {
-        float rn[P], lamn[P], st[2 * P];
-        cbp_phase2<P>(acc, q[k], ph[k], rn, lamn, ptab, L, tex);
+        float st[2 * P];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            st[p] = lamn[p];
-            st[P + p] = LBP ? lamn[p] : vs[k][p];               // H_v: this visit's decision (equ_s2e7)
+            st[p] = lamn[k][p];
+            st[P + p] = LBP ? lamn[k][p] : vs[k][p];            // H_v: this visit's decision (equ_s2e7)
         }
         stf<2 * P>(g.qp, aqp[k], st);
-        stf<P>(g.rb, rrow + k * L.ZR, rn);                      // equ_s4e22 commit of R_{c->v}
+        stf<P>(g.rb, rrow + k * L.ZR, rn[k]);                   // equ_s4e22 commit of R_{c->v}
     }
     return acc;
 }
@@ -414,22 +418,27 @@ __device__ __forceinline__ void park_p2(const int4* __restrict__ ent, const floa
         a[u] = A.x + wrap(L.rq + A.y, L.ZQ);
         ldf<2 * P>(g.qp, a[u], qp[u]);
     }
+    float rn[U][P], lamn[U][P];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-        float q[P], ph[P], rn[P], lamn[P], st[2 * P];
+    for (int u = 0; u < U; ++u) {                               // lookups first (see cbp_row_reg)
+        float q[P], ph[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             q[p] = qp[u][p];
             ph[p] = fabsf(qp[u][P + p]);
         }
-        cbp_phase2<P, false>(acc, q, ph, rn, lamn, ptab, L, 0);
+        cbp_phase2<P, false>(acc, q, ph, rn[u], lamn[u], ptab, L, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        float st[2 * P];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            st[p] = lamn[p];
-            st[P + p] = LBP ? lamn[p] : qp[u][P + p];          // sign = the decision of this visit
+            st[p] = lamn[u][p];
+            st[P + p] = LBP ? lamn[u][p] : qp[u][P + p];       // sign = the decision of this visit
         }
         stf<2 * P>(g.qp, a[u], st);
-        stf<P>(g.rb, rrow + (k0 + u) * L.ZR, rn);
+        stf<P>(g.rb, rrow + (k0 + u) * L.ZR, rn[u]);
     }
 }
 

@@ -186,19 +186,24 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
         }
 #pragma unroll
         for (int e = 0; e < DC; ++e) cbp_phase1<1, TEXC>(vs[e], ro[e], q[e], ph[e], ptab, L, tex, acc);
+        // all B2V lookups of the row before its first store: a table load may not move above a
+        // shared-memory store the compiler cannot prove disjoint (one dependent chain per edge otherwise)
+        float rn[DC][1], lamn[DC][1];
 #pragma unroll
         for (int e = 0; e < DC; ++e) {
-            float rn[1], lamn[1];
             // B2V rows: through TEX for the edges CBP_B2V_TEX_MASK selects (balances the TEX and LSU pipes)
             if (TEXB || (((CBP_B2V_TEX_MASK >> (e & 7)) & 1) != 0))   // folded after unrolling
-                cbp_phase2<1, true>(acc, q[e], ph[e], rn, lamn, ptab, L, tex);
+                cbp_phase2<1, true>(acc, q[e], ph[e], rn[e], lamn[e], ptab, L, tex);
             else
-                cbp_phase2<1, false>(acc, q[e], ph[e], rn, lamn, ptab, L, tex);
+                cbp_phase2<1, false>(acc, q[e], ph[e], rn[e], lamn[e], ptab, L, tex);
+        }
+#pragma unroll
+        for (int e = 0; e < DC; ++e) {
             if (v) {
-                const float st[2] = {lamn[0], LBP ? lamn[0] : vs[e][0]};
+                const float st[2] = {lamn[e][0], LBP ? lamn[e][0] : vs[e][0]};
                 stf<2>(c.qp, aqp[e], st);
             }
-            rst<RG>(rk + e * K * 32, rn[0]);                       // equ_s4e22 commit of R_{c->v}
+            rst<RG>(rk + e * K * 32, rn[e][0]);                    // equ_s4e22 commit of R_{c->v}
         }
         wslot_done<K, LBP>(c, k, rr, v, acc, o);
     }
@@ -247,16 +252,19 @@ __device__ __forceinline__ void wpark_p2(const int4* __restrict__ ent, const flo
         a[u] = A.x + wrap(rr * 8 + A.y, L.ZQ);
         ldf<2>(c.qp, a[u], vv[u]);
     }
+    float rn[U][1], lamn[U][1];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {                               // lookups first (see wrow)
+        const float q[1] = {vv[u][0]}, ph[1] = {fabsf(vv[u][1])};
+        cbp_phase2<1, false>(acc, q, ph, rn[u], lamn[u], ptab, L, 0);
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const float q[1] = {vv[u][0]}, ph[1] = {fabsf(vv[u][1])};
-        float rn[1], lamn[1];
-        cbp_phase2<1, false>(acc, q, ph, rn, lamn, ptab, L, 0);
         if (v) {
-            const float st[2] = {lamn[0], LBP ? lamn[0] : vv[u][1]};
+            const float st[2] = {lamn[u][0], LBP ? lamn[u][0] : vv[u][1]};
             stf<2>(c.qp, a[u], st);
         }
-        rst<RG>(rk + (e + u) * K * 32, rn[0]);
+        rst<RG>(rk + (e + u) * K * 32, rn[u][0]);
     }
 }
 
