@@ -352,6 +352,12 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
     // cbp_warp_kernel phi-row path (A/B runs): CBP_WARP_TEX=0 C2B rows through TEX (default), 1 both, 2 none
     const char* t2 = std::getenv("CBP_WARP_TEX");
     const int tex2_env = (t2 && t2[0] >= '0' && t2[0] <= '2' && t2[1] == 0) ? t2[0] - '0' : -1;
+    // cbp_warp_kernel per-warp state in words (cbp_internal.h): counters | Lambda | H bytes | cw |
+    // park buffer | R (r_words, if in the slot) | S [M] (Omega output only)
+    auto warp_state_words = [&](int64_t r_words, bool with_S) -> int64_t {
+        return (16 + static_cast<int64_t>(c->N) + cbp::warp_hb_words(c->N) + cbp::warp_cw_words(nwords) +
+                cbp::warp_pb_words(max_dc) + r_words + (with_S ? c->M : 0) + 3) / 4 * 4;
+    };
     auto make_geo = [&](int alg, int P, bool split_r, int multi_maxt = 512, bool allow_warp = true,
                         bool with_S = false) {
         cbp::Geometry G{};
@@ -373,7 +379,7 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
             const int64_t rw = static_cast<int64_t>(nent) * G.kslots * 32;
             G.table_words = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4 + 4;
             G.r_words = 0;
-            G.slot_words = static_cast<int32_t>((16 + 2LL * c->N + (nwords + 3) / 4 * 4 + rw + (with_S ? c->M : 0) + 3) / 4 * 4);
+            G.slot_words = static_cast<int32_t>(warp_state_words(rw, with_S));
             const char* gw = std::getenv("CBP_GS_WARPS");      // A/B runs: warps per CTA
             const int gwn = gw ? std::atoi(gw) : 0;
             G.teams = (gwn >= 1 && gwn <= CBP_WARPK_MAXT / 32) ? gwn : CBP_WARPK_MAXT / 32;
@@ -391,9 +397,7 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
             const int64_t rw = static_cast<int64_t>(nent) * G.kslots * 32;
             G.tex2 = tex2_env >= 0 ? tex2_env : 0;
             G.table_words = (G.tex2 == 1 ? 0 : 4 * cbp::kPhiTableSegs) + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4 + 4;
-            auto per_warp = [&](bool rg) {   // counters (8 x u64) | QP [2N] | cw | R | S [M] (Omega output only)
-                return (16 + 2LL * c->N + (nwords + 3) / 4 * 4 + (rg ? 0 : rw) + (with_S ? c->M : 0) + 3) / 4 * 4;
-            };
+            auto per_warp = [&](bool rg) { return warp_state_words(rg ? 0 : rw, with_S); };
             auto warps_of = [&](bool rg) {
                 const int64_t w = (smem_optin - 4LL * G.table_words) / (4 * per_warp(rg));
                 return static_cast<int>(std::min<int64_t>(w, maxt / 32));
@@ -415,7 +419,7 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
                 G.r_words = 0;
                 G.tex2 = 0;
                 G.table_words = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4 + 4;
-                G.slot_words = static_cast<int32_t>((16 + 2LL * c->N + (nwords + 3) / 4 * 4 + rw + (with_S ? c->M : 0) + 3) / 4 * 4);
+                G.slot_words = static_cast<int32_t>(warp_state_words(rw, with_S));
                 G.teams = CBP_WARPK_MAXT / 32;
                 G.threads = 32 * G.teams;
                 G.smem_bytes = static_cast<int32_t>(4LL * G.table_words);
@@ -552,9 +556,17 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         }
         c->ctas_per_sm[alg] = G.state_in_smem ? occ : 1;
         c->ent[alg] = make_ent(G.P, alg, G.r_global != 0);
-        const size_t eb = sizeof(int4) * c->ent[alg].size();
+        // cbp_warp_kernel (alg 0 / 2) reads its own entries, bulk-copied: {j Z, s, 0, 0}, {0, 0, s << 16, 0}
+        // (variable indices; the kernel parameters keep cbp_kernel's byte offsets for cbp_channel)
+        std::vector<int4> went = c->ent[alg];
+        if (alg == 0 || alg == 2)
+            for (int b = 0; b < nent; ++b) {
+                went[2 * b] = make_int4(ent_col[b] * Z, ent_s[b], 0, 0);
+                went[2 * b + 1] = make_int4(0, 0, ent_s[b] << 16, 0);
+            }
+        const size_t eb = sizeof(int4) * went.size();
         if (cudaMalloc(&c->ent_dev[alg], eb) != cudaSuccess ||
-            cudaMemcpy(c->ent_dev[alg], c->ent[alg].data(), eb, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaMemcpy(c->ent_dev[alg], went.data(), eb, cudaMemcpyHostToDevice) != cudaSuccess) {
             cudaGetLastError();
             cbp_code_destroy(c);
             return fail(CBP_E_NOMEM, "cbp_code_create: schedule table upload failed");

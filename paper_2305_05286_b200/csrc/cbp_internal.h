@@ -78,8 +78,23 @@ struct KernelArgs {
 #define CBP_WARPK1_MAXT 512
 #endif
 #ifndef CBP_WARPK_MAXT
-#define CBP_WARPK_MAXT 384
+#define CBP_WARPK_MAXT 640
 #endif
+
+// rows with at most CBP_DC_REG edges are updated from registers, longer rows by the park path
+#ifndef CBP_DC_REG
+#define CBP_DC_REG 8
+#endif
+#ifdef __CUDACC__
+#define CBP_HD __host__ __device__
+#else
+#define CBP_HD
+#endif
+// cbp_warp_kernel per-warp state, in 32-bit words (cbp_warp.cuh):
+//   counters [16] | Lambda [N floats] | H [N bytes] | cw [nwords] | park buffer | R (if in shared) | S [M] (Omega)
+CBP_HD inline int warp_hb_words(int N) { return (N + 15) / 16 * 4; }          // N bytes, 16-byte padded
+CBP_HD inline int warp_cw_words(int nwords) { return (nwords + 3) / 4 * 4; }
+CBP_HD inline int warp_pb_words(int max_dc) { return max_dc > CBP_DC_REG ? max_dc * 32 : 0; }   // park rows' Phi
 
 // thread limit (launch bound) of the one-frame-per-lane warp-team instantiation
 #ifndef CBP_WARP_MAXT

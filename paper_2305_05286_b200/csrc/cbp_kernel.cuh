@@ -467,10 +467,6 @@ __device__ __noinline__ RowAcc<P> cbp_row_park(const int4* __restrict__ ent, con
     return acc;
 }
 
-#ifndef CBP_DC_REG
-#define CBP_DC_REG 8
-#endif
-
 template <int P, int ALG>
 __device__ __forceinline__ RowAcc<P> cbp_row_dispatch(const int4* __restrict__ ent, const float4* __restrict__ ptab,
                                                       int e0, int dc, const Lane& L, TexH tex, const Grp<P, ALG>& g)

@@ -10,9 +10,12 @@
 // barriers, a finished frame is replaced at once (no sweep-boundary wait), and the per-row
 // control is paid once per K dc edges of a lane.
 //
-// Per-warp state in shared memory: QP[N] = {Lambda'_v, H_v} (cbp_kernel.cuh, producer-side
-// layout), S[M] (check records with sign = Omega < 0: Omega output and rollback only), the
-// transmitted codeword (ber_sim), and R (here, or in a global slot per warp: RG) laid out as
+// Per-warp state in shared memory: Lambda'[N] (the producer-side posterior, cbp_kernel.cuh) and
+// H[N] -- the decision of v's latest visit as one byte whose sign bit is the sign of the Lambda
+// that visit read (layered BP: of Lambda'), so a warp's frame takes 5 N bytes instead of 8 N and
+// more frames fit on an SM --, S[M] (check records with sign = Omega < 0: Omega output and
+// rollback only), the transmitted codeword (ber_sim), a park buffer for rows longer than
+// CBP_DC_REG, and R (here, or in a global slot per warp: RG) laid out as
 // R[(b K + k) 32 + l] -- coalesced, and the R words of a row's edges sit at compile-time
 // offsets from one row pointer.  The phi table and the schedule entries are staged once per
 // CTA by the bulk-copy (TMA) engine.
@@ -106,7 +109,9 @@ struct WCtx {
     int l, Lk, Z;
     bool fire_possible, keepS;   // the window may fill in this row; S records are kept (Omega output)
     bool r0;                     // sweep 1: every R_{c->v} still holds its initial 0 (equ_s4e17) -- not read
-    char* qp;
+    float* lam;                  // Lambda'[N]
+    int8_t* hb;                  // H[N]: sign = hard decision of v's latest visit
+    float* pb;                   // park buffer: Phi of edge e at pb[e 32 + l]
     float* rrow;                 // this lane's R word of (row entry 0, slot 0); (edge e, slot k) at rrow[(e K + k) 32]
     float* Srow;                 // S records of this row (keepS)
 };
@@ -175,14 +180,15 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
         RowAcc<1> acc;
         acc.Ssum[0] = 0.0f;
         acc.negw[0] = acc.flipw[0] = acc.oldbits[0] = 0u;
-        int aqp[DC];
+        int vi[DC];
         float vs[DC][2], q[DC][1], ph[DC][1];
 #pragma unroll
         for (int e = 0; e < DC; ++e) {
-            aqp[e] = A[e].x + wrap(rr * 8 + A[e].y, L.ZQ);
-            CBP_CHECK(aqp[e] >= 0 && aqp[e] + 8 <= L.slot_bytes);
-            ldf<2>(c.qp, aqp[e], vs[e]);                           // {Lambda_v, H_v}
-            if constexpr (LBP) vs[e][1] = vs[e][0];
+            vi[e] = A[e].x + wrap(rr + A[e].y, c.Z);                // variable j Z + (r + s) mod Z
+            CBP_CHECK(vi[e] >= 0 && vi[e] < L.slot_bytes);
+            vs[e][0] = c.lam[vi[e]];                                // Lambda_v
+            // H_v: the sign-extended byte carries the decision in bit 31 (layered BP: Lambda_v itself)
+            vs[e][1] = LBP ? vs[e][0] : __int_as_float(static_cast<int>(c.hb[vi[e]]));
         }
 #pragma unroll
         for (int e = 0; e < DC; ++e) cbp_phase1<1, TEXC>(vs[e], ro[e], q[e], ph[e], ptab, L, tex, acc);
@@ -200,8 +206,8 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
 #pragma unroll
         for (int e = 0; e < DC; ++e) {
             if (v) {
-                const float st[2] = {lamn[e][0], LBP ? lamn[e][0] : vs[e][0]};
-                stf<2>(c.qp, aqp[e], st);
+                c.lam[vi[e]] = lamn[e][0];
+                c.hb[vi[e]] = static_cast<int8_t>(__float_as_uint(LBP ? lamn[e][0] : vs[e][0]) >> 24);   // H_v
             }
             rst<RG>(rk + e * K * 32, rn[e][0]);                    // equ_s4e22 commit of R_{c->v}
         }
@@ -223,18 +229,20 @@ __device__ __forceinline__ void wpark_p1(const int4* __restrict__ ent, const flo
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e + u));
-        a[u] = A.x + wrap(rr * 8 + A.y, L.ZQ);
-        ldf<2>(c.qp, a[u], vv[u]);
+        a[u] = A.x + wrap(rr + A.y, c.Z);
+        vv[u][0] = c.lam[a[u]];
+        vv[u][1] = LBP ? vv[u][0] : __int_as_float(static_cast<int>(c.hb[a[u]]));
         ro[u][0] = c.r0 ? 0.0f : rld<RG>(rk + (e + u) * K * 32);
-        if (LBP) vv[u][1] = vv[u][0];
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) cbp_phase1<1, false>(vv[u], ro[u], q[u], ph[u], ptab, L, 0, acc);
+#pragma unroll
+    for (int u = 0; u < U; ++u) c.pb[(e + u) * 32] = ph[u][0];    // Phi, lane-private
     if (v) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const float st[2] = {q[u][0], __uint_as_float(__float_as_uint(ph[u][0]) | (__float_as_uint(vv[u][0]) & kSign))};
-            stf<2>(c.qp, a[u], st);
+            c.lam[a[u]] = q[u][0];                                // Q^new parked in the Lambda word
+            if (!LBP) c.hb[a[u]] = static_cast<int8_t>(__float_as_uint(vv[u][0]) >> 24);   // H_v (decided here)
         }
     }
 }
@@ -249,20 +257,21 @@ __device__ __forceinline__ void wpark_p2(const int4* __restrict__ ent, const flo
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e + u));
-        a[u] = A.x + wrap(rr * 8 + A.y, L.ZQ);
-        ldf<2>(c.qp, a[u], vv[u]);
+        a[u] = A.x + wrap(rr + A.y, c.Z);
+        vv[u][0] = c.lam[a[u]];                                   // Q^new
+        vv[u][1] = c.pb[(e + u) * 32];                            // Phi
     }
     float rn[U][1], lamn[U][1];
 #pragma unroll
     for (int u = 0; u < U; ++u) {                               // lookups first (see wrow)
-        const float q[1] = {vv[u][0]}, ph[1] = {fabsf(vv[u][1])};
+        const float q[1] = {vv[u][0]}, ph[1] = {vv[u][1]};
         cbp_phase2<1, false>(acc, q, ph, rn[u], lamn[u], ptab, L, 0);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         if (v) {
-            const float st[2] = {lamn[u][0], LBP ? lamn[u][0] : vv[u][1]};
-            stf<2>(c.qp, a[u], st);
+            c.lam[a[u]] = lamn[u][0];
+            if (LBP) c.hb[a[u]] = static_cast<int8_t>(__float_as_uint(lamn[u][0]) >> 24);
         }
         rst<RG>(rk + (e + u) * K * 32, rn[u][0]);
     }
@@ -355,29 +364,29 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
 
     const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
     const int Lk = a.lanes;                                   // L: lanes with check slots
-    int rk[K], rq[K];
+    int rk[K];
     bool vk[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int r = l + k * Lk;
         vk[k] = l < Lk && r < Z;
         rk[k] = vk[k] ? r : Z - 1;                            // invalid slots compute on check Z - 1, store nothing
-        rq[k] = rk[k] * 8;
     }
-    // per-warp shared state: counters (8 x u64) | QP [2N] | cw [nwords] | R (if !RG) | S [M] (if the
-    // launch outputs Omega: the geometry then has room for it)
+    // per-warp state (cbp_internal.h): counters (8 x u64) | Lambda [N] | H [N bytes] | cw [nwords] |
+    // park buffer | R (if !RG) | S [M] (if the launch outputs Omega: the geometry then has room for it)
     unsigned long long* wcnt =
         GS ? reinterpret_cast<unsigned long long*>(a.gstate + (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp) *
                                                                static_cast<size_t>(a.slot_words))
            : reinterpret_cast<unsigned long long*>(smem + a.table_words + static_cast<size_t>(warp) * a.slot_words);
-    float* st0 = reinterpret_cast<float*>(wcnt + 8);
-    char* qp = reinterpret_cast<char*>(st0);
-    uint32_t* cw = reinterpret_cast<uint32_t*>(st0 + 2 * N);
+    float* const lam = reinterpret_cast<float*>(wcnt + 8);
+    int8_t* const hb = reinterpret_cast<int8_t*>(lam + N);
+    uint32_t* cw = reinterpret_cast<uint32_t*>(lam + N + warp_hb_words(N));
+    float* const pb = reinterpret_cast<float*>(cw + warp_cw_words(C.nwords)) + l;
     const int rwords = C.nent * K * 32;
-    float* const Rs = reinterpret_cast<float*>(cw + ((C.nwords + 3) & ~3));
+    float* const Rs = reinterpret_cast<float*>(cw + warp_cw_words(C.nwords) + warp_pb_words(C.max_dc));
     float* Rw = (RG && !GS) ? a.rstate + (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * a.r_words : Rs;
     float* S = (RG && !GS) ? Rs : Rs + rwords;
-    const Lane lane{0, 0, 0, Z * 8, 0, 0, 4 * a.slot_words, 0, a.phi_m19, a.phi_one};
+    const Lane lane{0, 0, 0, 0, 0, 0, N, 0, a.phi_m19, a.phi_one};   // slot_bytes: variable bound (debug builds)
     if (l < 8) wcnt[l] = 0ull;
     __syncwarp();
     __syncthreads();
@@ -399,8 +408,8 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 const int2 A = *reinterpret_cast<const int2*>(ent + 2 * e);
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    const int at = A.x + wrap(rq[k] + A.y, Z * 8) + 4;
-                    par ^= vk[k] ? (__float_as_uint(*reinterpret_cast<const float*>(qp + at)) >> 31) << k : 0u;
+                    const int v = A.x + wrap(rk[k] + A.y, Z);
+                    par ^= vk[k] ? static_cast<uint32_t>(hb[v] < 0) << k : 0u;
                 }
             }
             nz |= par;
@@ -408,14 +417,13 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
         return __any_sync(kFull, nz != 0u);
     };
     // hard decisions of slot k's variables in row (e0, dc) <- bits (edge e at bit dc-1-e); returns the previous
-    auto swap_bits = [&](int rqk, int e0, int dc, uint32_t bits) -> uint32_t {
+    auto swap_bits = [&](int r, int e0, int dc, uint32_t bits) -> uint32_t {
         uint32_t prev = 0;
         for (int e = 0; e < dc; ++e) {
             const int2 A = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e));
-            float* h = reinterpret_cast<float*>(qp + A.x + wrap(rqk + A.y, Z * 8) + 4);
-            const uint32_t w = __float_as_uint(*h);
-            prev = (prev << 1) | (w >> 31);
-            *h = __uint_as_float((w & ~kSign) | (((bits >> (dc - 1 - e)) & 1u) << 31));
+            int8_t* h = hb + A.x + wrap(r + A.y, Z);
+            prev = (prev << 1) | static_cast<uint32_t>(*h < 0);
+            *h = ((bits >> (dc - 1 - e)) & 1u) ? static_cast<int8_t>(-128) : static_cast<int8_t>(0);
         }
         return prev;
     };
@@ -440,27 +448,41 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                         const int v = 16 * v16 + t;
                         const float x = __fadd_rn(__fmul_rn(static_cast<float>(static_cast<int8_t>(ws[t >> 2] >> (8 * (t & 3)))),
                                                             a.qscale), 0.0f);
-                        if (v < N) *reinterpret_cast<float2*>(qp + 8 * v) = make_float2(x, x);
+                        if (v < N) {
+                            lam[v] = x;
+                            hb[v] = static_cast<int8_t>(__float_as_uint(x) >> 24);
+                        }
                     }
                 }
             } else {
                 const float4* src = reinterpret_cast<const float4*>(a.llr + base);
                 for (int v4 = l; 4 * v4 < N; v4 += 32) {
                     const float4 x = __ldcs(src + v4);
-                    const float xs[4] = {x.x, x.y, x.z, x.w};
+                    const float4 x0 = make_float4(__fadd_rn(x.x, 0.0f), __fadd_rn(x.y, 0.0f), __fadd_rn(x.z, 0.0f),
+                                                  __fadd_rn(x.w, 0.0f));
+                    // H bytes = the sign bytes of the four posteriors, one 32-bit store
+                    const uint32_t hw4 = __byte_perm(__byte_perm(__float_as_uint(x0.x), __float_as_uint(x0.y), 0x0073),
+                                                     __byte_perm(__float_as_uint(x0.z), __float_as_uint(x0.w), 0x0073), 0x5410);
+                    if (4 * v4 + 3 < N) {
+                        *reinterpret_cast<float4*>(lam + 4 * v4) = x0;
+                        *reinterpret_cast<uint32_t*>(hb + 4 * v4) = hw4;
+                    } else {
+                        const float xs[4] = {x0.x, x0.y, x0.z, x0.w};
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const float x0 = __fadd_rn(xs[t], 0.0f);
-                        if (4 * v4 + t < N) *reinterpret_cast<float2*>(qp + 8 * (4 * v4 + t)) = make_float2(x0, x0);
+                        for (int t = 0; t < 4; ++t)
+                            if (4 * v4 + t < N) {
+                                lam[4 * v4 + t] = xs[t];
+                                hb[4 * v4 + t] = static_cast<int8_t>(__float_as_uint(xs[t]) >> 24);
+                            }
                     }
                 }
             }
         } else {
             const uint64_t gframe = static_cast<uint64_t>(a.frame_begin + f);
             const uint32_t flo = static_cast<uint32_t>(gframe), fhi = static_cast<uint32_t>(gframe >> 32);
-            float* Qs = st0;                                  // symbols 1 - 2c in the Lambda words during encoding
+            float* Qs = lam;                                  // symbols 1 - 2c in the Lambda words during encoding
             if (a.llr_mode & 2) {                             // all-zero codeword (R23)
-                for (int v = l; v < N; v += 32) Qs[2 * v] = 1.0f;
+                for (int v = l; v < N; v += 32) Qs[v] = 1.0f;
                 for (int w = l; w < C.nwords; w += 32) cw[w] = 0u;
                 __syncwarp();
             } else {
@@ -477,19 +499,19 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 }
                 __syncwarp();
                 // (a3) dual-diagonal encoder: systematic symbols, lambda_i[r] of the
-                // core rows (kept in S), p0 = XOR_i lambda_i, the parity chain, the extension
-                for (int v = l; v < C.K; v += 32) Qs[2 * v] = ((cw[v >> 5] >> (v & 31)) & 1u) ? -1.0f : 1.0f;
+                // core rows, p0 = XOR_i lambda_i, the parity chain, the extension
+                for (int v = l; v < C.K; v += 32) Qs[v] = ((cw[v >> 5] >> (v & 31)) & 1u) ? -1.0f : 1.0f;
                 // lambda_i[r] = XOR of the info bits of check i Z + r: each entry read once per row for the K
-                // slots (kept in H words); p0 = XOR over the core rows
+                // slots (kept in the H bytes, free until the channel step); p0 = XOR over the core rows
                 uint32_t p0[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) p0[k] = 0u;
                 for (int i = 0; i < C.core; ++i) {
-                    uint32_t lam[K];
+                    uint32_t lamb[K];
 #pragma unroll
-                    for (int k = 0; k < K; ++k) lam[k] = 0u;
+                    for (int k = 0; k < K; ++k) lamb[k] = 0u;
                     for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
-                        const int jz = ent[2 * e].x >> 3;             // j Z (QS = 8)
+                        const int jz = ent[2 * e].x;                  // j Z
                         if (jz >= C.K) continue;                      // a parity column (warp-uniform)
                         const int sft = ent[2 * e + 1].z >> 16;
 #pragma unroll
@@ -497,19 +519,19 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                             int t = rk[k] + sft;
                             t = (t >= Z) ? t - Z : t;
                             const int v = jz + t;
-                            lam[k] ^= (cw[v >> 5] >> (v & 31)) & 1u;
+                            lamb[k] ^= (cw[v >> 5] >> (v & 31)) & 1u;
                         }
                     }
 #pragma unroll
                     for (int k = 0; k < K; ++k)
                         if (vk[k]) {
-                            Qs[2 * (i * Z + rk[k]) + 1] = __uint_as_float(lam[k]);
-                            p0[k] ^= lam[k];
+                            hb[i * Z + rk[k]] = static_cast<int8_t>(lamb[k]);
+                            p0[k] ^= lamb[k];
                         }
                 }
 #pragma unroll
                 for (int k = 0; k < K; ++k)
-                    if (vk[k]) Qs[2 * (C.kb * Z + rk[k])] = p0[k] ? -1.0f : 1.0f;
+                    if (vk[k]) Qs[C.kb * Z + rk[k]] = p0[k] ? -1.0f : 1.0f;
                 __syncwarp();
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
@@ -517,26 +539,26 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                     const int r = rk[k];
                     uint32_t pprev = 0;
                     for (int t = 1; t < C.core; ++t) {
-                        uint32_t pt = __float_as_uint(Qs[2 * ((t - 1) * Z + r) + 1]);
+                        uint32_t pt = static_cast<uint32_t>(hb[(t - 1) * Z + r]);
                         if (t >= 2) pt ^= pprev;
                         const int s0 = pshift[t - 1];
                         if (s0 >= 0) {
                             int rr = r + s0;
                             rr = (rr >= Z) ? rr - Z : rr;
-                            pt ^= Qs[2 * (C.kb * Z + rr)] < 0.0f ? 1u : 0u;
+                            pt ^= Qs[C.kb * Z + rr] < 0.0f ? 1u : 0u;
                         }
-                        Qs[2 * ((C.kb + t) * Z + r)] = pt ? -1.0f : 1.0f;
+                        Qs[(C.kb + t) * Z + r] = pt ? -1.0f : 1.0f;
                         pprev = pt;
                     }
                     for (int x = 0; x < mb - C.core; ++x) {
-                        const uint32_t pe = info_parity<8>(ent, row_ptr, C.core + x, r, Z, C.K, cw);
-                        Qs[2 * ((C.kb + C.core + x) * Z + r)] = pe ? -1.0f : 1.0f;
+                        const uint32_t pe = info_parity<1>(ent, row_ptr, C.core + x, r, Z, C.K, cw);
+                        Qs[(C.kb + C.core + x) * Z + r] = pe ? -1.0f : 1.0f;
                     }
                 }
                 __syncwarp();
                 for (int w = 0; w < C.nwords; ++w) {          // transmitted codeword words: one ballot each
                     const int v = 32 * w + l;
-                    const unsigned word = __ballot_sync(kFull, v < N && Qs[2 * v] < 0.0f);
+                    const unsigned word = __ballot_sync(kFull, v < N && Qs[v] < 0.0f);
                     if (l == 0) cw[w] = word;
                 }
                 __syncwarp();
@@ -552,7 +574,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 for (int m = 0; m < 4; ++m) {
                     const int v = 4 * b + m;
                     if (v >= N) break;
-                    const float y = __fadd_rn(Qs[2 * v], __fmul_rn(a.sigma, n[m]));
+                    const float y = __fadd_rn(Qs[v], __fmul_rn(a.sigma, n[m]));
                     float Lv = __fmul_rn(a.scale, y);
                     if (a.llr_mode & 1) {
                         float qq = rintf(__fmul_rn(Lv, 4.0f));
@@ -560,7 +582,8 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                         Lv = __fmul_rn(qq, 0.25f);
                     }
                     const float x0 = __fadd_rn(Lv, 0.0f);
-                    *reinterpret_cast<float2*>(qp + 8 * v) = make_float2(x0, x0);
+                    lam[v] = x0;
+                    hb[v] = static_cast<int8_t>(__float_as_uint(x0) >> 24);
                 }
             }
         }
@@ -579,7 +602,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
             for (int i = 0; i < mb; ++i) {
                 const int e0 = row_ptr[i], dc = row_ptr[i + 1] - e0;
                 // the window can fill in this row: keep what a mid-row stop has to roll back
-                WCtx cx{l, Lk, Z, belief && W - consec - 1 < Z, keep_S, sweep == 1, qp,
+                WCtx cx{l, Lk, Z, belief && W - consec - 1 < Z, keep_S, sweep == 1, lam, hb, pb,
                         Rw + static_cast<size_t>(e0) * K * 32 + l, S + i * Z};
                 WRow<K> ro;
                 ro.first_bad = Z;
@@ -605,7 +628,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 for (int k = 0; k < K; ++k) {
                     newbits.v[k] = 0;
                     if (vk[k] && rk[k] > rstar) {
-                        newbits.v[k] = swap_bits(rq[k], e0, dc, ro.oldb.v[k]);
+                        newbits.v[k] = swap_bits(rk[k], e0, dc, ro.oldb.v[k]);
                         if (keep_S && !LBP) S[i * Z + rk[k]] = ro.sold.v[k];
                     }
                 }
@@ -621,7 +644,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
 #pragma unroll
                 for (int k = 0; k < K; ++k)
                     if (vk[k] && rk[k] > rstar) {
-                        swap_bits(rq[k], e0, dc, newbits.v[k]);
+                        swap_bits(rk[k], e0, dc, newbits.v[k]);
                         if (keep_S && !LBP) S[i * Z + rk[k]] = ro.snew.v[k];
                     }
                 __syncwarp();
@@ -639,11 +662,11 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
         if (!conv) synd_zero = !syndrome_nz();
         const uint8_t flags = static_cast<uint8_t>((conv ? 1 : 0) | (synd_zero ? 2 : 0) | (fires > 0 ? 4 : 0));
         if (!ber) {
-            // packed hard decisions (sign of H), one ballot per word: lane l reads variable 32 w + l
+            // packed hard decisions (sign of the H bytes), one ballot per word: lane l reads variable 32 w + l
             uint32_t* out = a.bits + static_cast<size_t>(f) * a.ld_words;
             for (int w = 0; w < a.ld_words; ++w) {
                 const int v = 32 * w + l;
-                const unsigned word = __ballot_sync(kFull, v < N && (__float_as_uint(st0[2 * v + 1]) >> 31));
+                const unsigned word = __ballot_sync(kFull, v < N && hb[v] < 0);
                 if (l == (w & 31)) out[w] = word;
             }
             if (a.omega) {
@@ -669,7 +692,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
             bool info_err = false, cw_err = false;
             for (int w = 0; w < C.nwords; ++w) {
                 const int v = 32 * w + l;
-                const bool dv = v < N && ((__float_as_uint(st0[2 * v + 1]) >> 31) != ((cw[w] >> l) & 1u));
+                const bool dv = v < N && (static_cast<uint32_t>(hb[v] < 0) != ((cw[w] >> l) & 1u));
                 const unsigned d = __ballot_sync(kFull, dv);
                 const unsigned ie = __ballot_sync(kFull, dv && v < C.K);
                 bit_err += (l == 0) ? __popc(ie) : 0;
