@@ -160,7 +160,7 @@ struct cbp_code {
     int ctas_per_sm[4] = {1, 1, 1, 1}, num_sms = 1;
     cbp::Geometry geo_chan{};          // cbp_channel: cbp_kernel (the warp kernel has no channel-only mode)
     int ctas_chan = 1;
-    cbp::Geometry geo_omega{};         // log-tanh decode with Omega output on cbp_warp_kernel: room for S
+    cbp::Geometry geo_omega{};         // log-tanh decode with Omega output (geo[0] is cbp_warp_kernel's): room for S
     int ctas_omega = 1;
     int4* ent_dev[4] = {};             // device copies of ent[] (bulk-copied by cbp_warp_kernel)
     ~cbp_code()
@@ -363,29 +363,34 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
         cbp::Geometry G{};
         G.alg = alg;
         G.P = P;
-        // global-state warps for Z > 128: measured slower than cbp_kernel's global-state teams (C4 83 vs 66 ms
-        // per 3000 frames), so only on request (CBP_WARP_GS=1, A/B runs)
-        const char* gsv = std::getenv("CBP_WARP_GS");
-        const bool gs_on = gsv && gsv[0] == '1' && gsv[1] == 0;
-        if (use_warp && allow_warp && gs_on && (alg == 0 || alg == 2) && P == 1 && Z > 128 && Z <= 512 && tex2_env < 0) {
-            // cbp_warp_kernel with the per-warp state in a global slot (frames too large for shared memory:
-            // C4 0.6 MB): K in {8, 12, 16} check slots per lane, tables only in shared memory
-            G.wk = 1;
-            const int kmin = (Z + 31) / 32;
-            G.kslots = kmin <= 8 ? 8 : (kmin <= 12 ? 12 : 16);
-            G.lanes = (Z + G.kslots - 1) / G.kslots;
-            G.multi = 0; G.F = 1; G.Zp = 32; G.team_threads = 32; G.state_in_smem = 0; G.r_global = 1;
-            G.tex2 = 0;
-            const int64_t rw = static_cast<int64_t>(nent) * G.kslots * 32;
-            G.table_words = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4 + 4;
-            G.r_words = 0;
-            G.slot_words = static_cast<int32_t>(warp_state_words(rw, with_S));
-            const char* gw = std::getenv("CBP_GS_WARPS");      // A/B runs: warps per CTA
-            const int gwn = gw ? std::atoi(gw) : 0;
-            G.teams = (gwn >= 1 && gwn <= CBP_WARPK_MAXT / 32) ? gwn : CBP_WARPK_MAXT / 32;
-            G.threads = 32 * G.teams;
-            G.smem_bytes = static_cast<int32_t>(4LL * G.table_words);
-            return G;
+        // cbp_warp_kernel team frames: one frame per CTA, its warps share the state in
+        // shared memory (5 N bytes), rows ordered by a CTA barrier.  For codes whose frames do not fit 6 per
+        // SM in warp mode (Z > 128: C4; P8192).  CBP_WARP_TEAM=0 keeps cbp_kernel's teams (A/B runs).
+        const char* tv = std::getenv("CBP_WARP_TEAM");
+        const bool team_on = !(tv && tv[0] == '0' && tv[1] == 0);
+        auto warp_team = [&]() -> bool {
+            if (!(use_warp && allow_warp && team_on && (alg == 0 || alg == 2) && P == 1 && Z >= 17 && tex2_env < 0))
+                return false;
+            const int K = Z <= CBP_WARPT_MAXT ? 1 : (Z <= 2 * CBP_WARPT_MAXT ? 2 : 0);
+            if (K == 0) return false;
+            const int lanes = (Z + K - 1) / K, W = (lanes + 31) / 32;
+            const int64_t tw = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4 + 4;
+            // counters | Lambda | H | cw | park buffer per warp | S (Omega) | row control [2][2][W] | frame index
+            const int64_t sw = (16 + static_cast<int64_t>(c->N) + cbp::warp_hb_words(c->N) + cbp::warp_cw_words(nwords) +
+                                static_cast<int64_t>(W) * cbp::warp_pb_words(max_dc) + (with_S ? c->M : 0) + 4 * W + 4 + 3) /
+                               4 * 4;
+            if (4 * (tw + sw) > smem_optin) return false;
+            G = cbp::Geometry{};
+            G.alg = alg; G.P = P; G.wk = 1; G.multi = 1; G.kslots = K; G.lanes = lanes; G.F = 1; G.Zp = 32;
+            G.team_threads = 32 * W; G.threads = 32 * W; G.teams = 1; G.state_in_smem = 1; G.r_global = 1;
+            G.r_words = static_cast<int32_t>(static_cast<int64_t>(W) * nent * K * 32);
+            G.slot_words = static_cast<int32_t>(sw); G.table_words = static_cast<int32_t>(tw); G.tex2 = 0;
+            G.smem_bytes = static_cast<int32_t>(4 * (tw + sw));
+            return true;
+        };
+        if (Z > 128) {
+            if (warp_team()) return G;
+            goto team_geometry;
         }
         if (use_warp && allow_warp && (alg == 0 || alg == 2) && P == 1 && Z >= 17 && Z <= 128) {
             // cbp_warp_kernel: one frame per warp, K = ceil(Z/32) check slots per lane
@@ -403,27 +408,14 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
                 return static_cast<int>(std::min<int64_t>(w, maxt / 32));
             };
             const int ws = warps_of(false), wg = warps_of(true);
-            if (std::max(ws, wg) < 6 && !gs_on) {
-                // frames too large for 6 per SM even with R in global memory (P8192: 3 warps): cbp_kernel's
-                // global-state teams (8 per SM) measured faster than global-state warps (44.9 vs 48.0 ms)
+            if (std::max(ws, wg) < 6) {
+                // frames too large for 6 per SM even with R in global memory (P8192: 5 warps): team frames,
+                // else cbp_kernel's teams
+                if (warp_team()) return G;
                 G = cbp::Geometry{};
                 G.alg = alg;
                 G.P = P;
                 goto team_geometry;
-            }
-            if (std::max(ws, wg) < 6 && G.kslots >= 2 && tex2_env < 0 && split_r_env < 0) {
-                // frames too large for 6 per SM even with R in global memory (P8192: 3): the whole
-                // per-warp state in a global slot, 12 warps per SM
-                G.state_in_smem = 0;
-                G.r_global = 1;
-                G.r_words = 0;
-                G.tex2 = 0;
-                G.table_words = 4 * cbp::kPhiTableSegs + (8 * nent + (mb + 1) + (mb + 1) / 2 + 3) / 4 * 4 + 4;
-                G.slot_words = static_cast<int32_t>(warp_state_words(rw, with_S));
-                G.teams = CBP_WARPK_MAXT / 32;
-                G.threads = 32 * G.teams;
-                G.smem_bytes = static_cast<int32_t>(4LL * G.table_words);
-                return G;
             }
             // R in global memory (coalesced, L1/L2-served) when shared memory holds fewer than 8 frames
             bool rg = ws < 8 && wg > ws;
@@ -578,9 +570,10 @@ cbp_status cbp_code_create_ex(const int16_t* base, int32_t mb, int32_t nb, int32
     c->geo_omega = c->geo[0];
     c->ctas_omega = c->ctas_per_sm[0];
     if (c->geo[0].wk) {
+        // (a frame plus S that no longer fits on chip -- C4's team frames -- runs on cbp_kernel's teams)
         c->geo_omega = make_geo(0, 1, false, 512, true, true);
         int occ = 0;
-        if (!c->geo_omega.wk || cbp::occupancy_ctas_per_sm(c->geo_omega, &occ) != 0 || occ < 1) {
+        if (cbp::occupancy_ctas_per_sm(c->geo_omega, &occ) != 0 || occ < 1) {
             cudaGetLastError();
             cbp_code_destroy(c);
             return fail(CBP_E_UNSUPPORTED, "cbp_code_create: Omega-output kernel does not fit on this device");

@@ -81,6 +81,11 @@ struct KernelArgs {
 #define CBP_WARPK_MAXT 640
 #endif
 
+// thread limit of cbp_warp_kernel's team instantiations (one frame per CTA)
+#ifndef CBP_WARPT_MAXT
+#define CBP_WARPT_MAXT 384
+#endif
+
 // rows with at most CBP_DC_REG edges are updated from registers, longer rows by the park path
 #ifndef CBP_DC_REG
 #define CBP_DC_REG 8

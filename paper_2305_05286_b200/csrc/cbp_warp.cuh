@@ -106,7 +106,8 @@ struct WRow {
 
 // The per-row context of a lane.
 struct WCtx {
-    int l, Lk, Z;
+    int l, Lk, Z;                // l: the lane's index in the frame's team (warp mode: lane)
+    int l0;                      // index of the warp's lane 0 in the team (warp mode: 0)
     bool fire_possible, keepS;   // the window may fill in this row; S records are kept (Omega output)
     bool r0;                     // sweep 1: every R_{c->v} still holds its initial 0 (equ_s4e17) -- not read
     float* lam;                  // Lambda'[N]
@@ -128,8 +129,8 @@ __device__ __forceinline__ void wslot_done(const WCtx& c, int k, int rr, bool v,
     }
     const unsigned m = __ballot_sync(kFull, v && (((acc.negw[0] | acc.flipw[0]) & kSign) != 0u));
     if (m) {
-        o.first_bad = min(o.first_bad, k * c.Lk + __ffs(m) - 1);
-        o.last_bad = max(o.last_bad, k * c.Lk + 31 - __clz(m));
+        o.first_bad = min(o.first_bad, k * c.Lk + c.l0 + __ffs(m) - 1);
+        o.last_bad = max(o.last_bad, k * c.Lk + c.l0 + 31 - __clz(m));
     }
 }
 
@@ -333,11 +334,14 @@ __device__ __forceinline__ void wrow_dispatch(int dc, const int4* __restrict__ e
 // int8 LLRs from HBM) and the fused ber_sim; cbp_channel runs on cbp_kernel.
 // TM: phi table rows for C2B / B2V through the texture pipe (0: C2B only, 1: both -- the table
 // is then not staged in shared memory, 2: neither).
-// GS: the warp's whole state (counters, QP, codeword, R, S) in a global slot per warp (large frames:
-// C4's 0.6 MB does not fit on chip; L2 / HBM-served, coalesced), shared memory holds the tables only.
-template <int K, bool RG, int MAXT, int ALG, int TM, bool GS = false>
+// TEAM: one frame per CTA instead of one per warp (large frames, C4: N = 26112, Z = 384): the CTA's
+// warps are the team, lane t of the team updates checks t + k L, rows are ordered by a CTA barrier
+// that also reduces the stop window's first / last unclean check; R stays lane-private in a global
+// slot per warp.
+template <int K, bool RG, int MAXT, int ALG, int TM, bool TEAM = false>
 __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant__ KernelArgs a)
 {
+    static_assert(!TEAM || RG, "team frames keep R in the global workspace");
     constexpr bool TEXB = TM == 1;
     constexpr bool LBP = ALG == 2;
     extern __shared__ __align__(16) uint32_t smem[];
@@ -362,32 +366,49 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
     for (int k = threadIdx.x; k <= mb; k += blockDim.x) row_ptr[k] = a.row_ptr[k];
     for (int k = threadIdx.x; k < mb; k += blockDim.x) pshift[k] = a.pshift[k];
 
-    const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5, l = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    const int tl = TEAM ? static_cast<int>(threadIdx.x) : l;  // lane index in the frame's team
+    const int TL = TEAM ? static_cast<int>(blockDim.x) : 32;  // team size
+    const int w0 = TEAM ? warp : 0, wstep = TEAM ? nwarps : 1;   // this warp's share of word-wise loops
     const int Lk = a.lanes;                                   // L: lanes with check slots
     int rk[K];
     bool vk[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        const int r = l + k * Lk;
-        vk[k] = l < Lk && r < Z;
+        const int r = tl + k * Lk;
+        vk[k] = tl < Lk && r < Z;
         rk[k] = vk[k] ? r : Z - 1;                            // invalid slots compute on check Z - 1, store nothing
     }
+    // team barrier (warp mode: the warp's) and team-wide any
+    auto tsync = [&]() {
+        if constexpr (TEAM) __syncthreads();
+        else __syncwarp();
+    };
+    auto tany = [&](bool p) -> bool {
+        if constexpr (TEAM) return __syncthreads_or(p) != 0;
+        else return __any_sync(kFull, p);
+    };
     // per-warp state (cbp_internal.h): counters (8 x u64) | Lambda [N] | H [N bytes] | cw [nwords] |
     // park buffer | R (if !RG) | S [M] (if the launch outputs Omega: the geometry then has room for it)
+    // (team: one state per CTA, its park buffer per warp, and 2 x 2 x nwarps control words after it)
     unsigned long long* wcnt =
-        GS ? reinterpret_cast<unsigned long long*>(a.gstate + (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp) *
-                                                               static_cast<size_t>(a.slot_words))
-           : reinterpret_cast<unsigned long long*>(smem + a.table_words + static_cast<size_t>(warp) * a.slot_words);
+        reinterpret_cast<unsigned long long*>(smem + a.table_words + static_cast<size_t>(TEAM ? 0 : warp) * a.slot_words);
     float* const lam = reinterpret_cast<float*>(wcnt + 8);
     int8_t* const hb = reinterpret_cast<int8_t*>(lam + N);
     uint32_t* cw = reinterpret_cast<uint32_t*>(lam + N + warp_hb_words(N));
-    float* const pb = reinterpret_cast<float*>(cw + warp_cw_words(C.nwords)) + l;
-    const int rwords = C.nent * K * 32;
-    float* const Rs = reinterpret_cast<float*>(cw + warp_cw_words(C.nwords) + warp_pb_words(C.max_dc));
-    float* Rw = (RG && !GS) ? a.rstate + (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * a.r_words : Rs;
-    float* S = (RG && !GS) ? Rs : Rs + rwords;
+    float* const pb = reinterpret_cast<float*>(cw + warp_cw_words(C.nwords)) + (TEAM ? warp * warp_pb_words(C.max_dc) : 0) + l;
+    const int rwords = C.nent * K * 32;                       // R words of one warp
+    float* const Rs = reinterpret_cast<float*>(cw + warp_cw_words(C.nwords) + (TEAM ? nwarps : 1) * warp_pb_words(C.max_dc));
+    float* Rw = !RG ? Rs
+                    : a.rstate + (TEAM ? static_cast<size_t>(blockIdx.x) * a.r_words + static_cast<size_t>(warp) * rwords
+                                       : (static_cast<size_t>(blockIdx.x) * nwarps + warp) * a.r_words);
+    float* S = RG ? Rs : Rs + rwords;
+    // team: [2 buffers][first | last][nwarps] (after S, which only the log-tanh Omega output keeps)
+    int* const tctl = reinterpret_cast<int*>(S + ((a.omega != nullptr && !LBP) ? C.M : 0));
+    long long* const tfrm = reinterpret_cast<long long*>((reinterpret_cast<uintptr_t>(tctl + 4 * nwarps) + 7) &
+                                                         ~static_cast<uintptr_t>(7));   // team: frame index
     const Lane lane{0, 0, 0, 0, 0, 0, N, 0, a.phi_m19, a.phi_one};   // slot_bytes: variable bound (debug builds)
-    if (l < 8) wcnt[l] = 0ull;
+    if (TEAM ? threadIdx.x < 8 : l < 8) wcnt[TEAM ? threadIdx.x : l] = 0ull;
     __syncwarp();
     __syncthreads();
     mbar_wait(bar, 0);
@@ -403,6 +424,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
     auto syndrome_nz = [&]() -> bool {
         uint32_t nz = 0;
         for (int i = 0; i < mb; ++i) {
+            if ((i & 3) == 0 && i && tany(nz != 0u)) return true;   // an unsatisfied check: done
             uint32_t par = 0;                                 // bit k: parity of check i Z + r_k
             for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
                 const int2 A = *reinterpret_cast<const int2*>(ent + 2 * e);
@@ -414,7 +436,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
             }
             nz |= par;
         }
-        return __any_sync(kFull, nz != 0u);
+        return tany(nz != 0u);
     };
     // hard decisions of slot k's variables in row (e0, dc) <- bits (edge e at bit dc-1-e); returns the previous
     auto swap_bits = [&](int r, int e0, int dc, uint32_t bits) -> uint32_t {
@@ -428,10 +450,18 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
         return prev;
     };
 
+    int rowpar = 0;                                           // team: control-word buffer of the row
     for (;;) {
         long long f = 0;
-        if (l == 0) f = static_cast<long long>(atomicAdd(a.queue, 1ull));
-        f = __shfl_sync(kFull, f, 0);
+        if constexpr (TEAM) {
+            if (threadIdx.x == 0) *tfrm = static_cast<long long>(atomicAdd(a.queue, 1ull));
+            __syncthreads();
+            f = *tfrm;
+            __syncthreads();                                  // every thread has the index before it is rewritten
+        } else {
+            if (l == 0) f = static_cast<long long>(atomicAdd(a.queue, 1ull));
+            f = __shfl_sync(kFull, f, 0);
+        }
         if (f >= a.frames) break;
         // ---- Step 1 (a2-a5): channel LLRs (decode: from HBM, 16 bytes per lane and load;
         // ber_sim: Philox info bits, encoder, BPSK/AWGN in the warp), {Lambda, H} = L + 0, R = 0
@@ -439,7 +469,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
             const size_t base = static_cast<size_t>(f) * a.ld;
             if (a.mode == MODE_DECODE_I8) {
                 const int4* src = reinterpret_cast<const int4*>(a.q + base);
-                for (int v16 = l; 16 * v16 < N; v16 += 32) {
+                for (int v16 = tl; 16 * v16 < N; v16 += TL) {
                     const int4 w = __ldcs(src + v16);
                     const uint32_t ws[4] = {static_cast<uint32_t>(w.x), static_cast<uint32_t>(w.y),
                                             static_cast<uint32_t>(w.z), static_cast<uint32_t>(w.w)};
@@ -456,7 +486,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 }
             } else {
                 const float4* src = reinterpret_cast<const float4*>(a.llr + base);
-                for (int v4 = l; 4 * v4 < N; v4 += 32) {
+                for (int v4 = tl; 4 * v4 < N; v4 += TL) {
                     const float4 x = __ldcs(src + v4);
                     const float4 x0 = make_float4(__fadd_rn(x.x, 0.0f), __fadd_rn(x.y, 0.0f), __fadd_rn(x.z, 0.0f),
                                                   __fadd_rn(x.w, 0.0f));
@@ -482,13 +512,13 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
             const uint32_t flo = static_cast<uint32_t>(gframe), fhi = static_cast<uint32_t>(gframe >> 32);
             float* Qs = lam;                                  // symbols 1 - 2c in the Lambda words during encoding
             if (a.llr_mode & 2) {                             // all-zero codeword (R23)
-                for (int v = l; v < N; v += 32) Qs[v] = 1.0f;
-                for (int w = l; w < C.nwords; w += 32) cw[w] = 0u;
-                __syncwarp();
+                for (int v = tl; v < N; v += TL) Qs[v] = 1.0f;
+                for (int w = tl; w < C.nwords; w += TL) cw[w] = 0u;
+                tsync();
             } else {
                 // (a2) info word w = Philox(w/4, f_lo, f_hi, 0)[w % 4]
                 const int nblk = (C.kwords + 3) / 4;
-                for (int b = l; b < nblk; b += 32) {
+                for (int b = tl; b < nblk; b += TL) {
                     const u32x4 x = philox4x32_10(u32x4{static_cast<uint32_t>(b), flo, fhi, 0u}, key0, key1);
                     const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -497,10 +527,10 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                         if (w < C.kwords) cw[w] = (w == C.kwords - 1 && (C.K & 31)) ? xs[m] & ((1u << (C.K & 31)) - 1u) : xs[m];
                     }
                 }
-                __syncwarp();
+                tsync();
                 // (a3) dual-diagonal encoder: systematic symbols, lambda_i[r] of the
                 // core rows, p0 = XOR_i lambda_i, the parity chain, the extension
-                for (int v = l; v < C.K; v += 32) Qs[v] = ((cw[v >> 5] >> (v & 31)) & 1u) ? -1.0f : 1.0f;
+                for (int v = tl; v < C.K; v += TL) Qs[v] = ((cw[v >> 5] >> (v & 31)) & 1u) ? -1.0f : 1.0f;
                 // lambda_i[r] = XOR of the info bits of check i Z + r: each entry read once per row for the K
                 // slots (kept in the H bytes, free until the channel step); p0 = XOR over the core rows
                 uint32_t p0[K];
@@ -532,7 +562,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
 #pragma unroll
                 for (int k = 0; k < K; ++k)
                     if (vk[k]) Qs[C.kb * Z + rk[k]] = p0[k] ? -1.0f : 1.0f;
-                __syncwarp();
+                tsync();
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     if (!vk[k]) continue;
@@ -555,17 +585,17 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                         Qs[(C.kb + C.core + x) * Z + r] = pe ? -1.0f : 1.0f;
                     }
                 }
-                __syncwarp();
-                for (int w = 0; w < C.nwords; ++w) {          // transmitted codeword words: one ballot each
+                tsync();
+                for (int w = w0; w < C.nwords; w += wstep) {  // transmitted codeword words: one ballot each
                     const int v = 32 * w + l;
                     const unsigned word = __ballot_sync(kFull, v < N && Qs[v] < 0.0f);
                     if (l == 0) cw[w] = word;
                 }
-                __syncwarp();
+                tsync();
             }
             // (a4) y = (1 - 2c) + sigma n, L = (2/sigma^2) y (equ_s4e15, R17); int8 stream
             const int nblk = (N + 3) / 4;
-            for (int b = l; b < nblk; b += 32) {
+            for (int b = tl; b < nblk; b += TL) {
                 const u32x4 x = philox4x32_10(u32x4{static_cast<uint32_t>(b), flo, fhi, 1u}, key0, key1);
                 float n[4];
                 box_muller(x.x, x.y, n[0], n[1]);
@@ -590,8 +620,8 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
         // R = 0 (equ_s4e17) needs no stores: sweep 1 reads no R word (WCtx::r0), and every word is
         // written in sweep 1 before sweep 2 reads it (a frame that stops in sweep 1 reads none)
         if (keep_S)
-            for (int c = l; c < C.M; c += 32) S[c] = 0.0f;    // equ_s4e16: Omega = inf <=> S = 0
-        __syncwarp();
+            for (int c = tl; c < C.M; c += TL) S[c] = 0.0f;   // equ_s4e16: Omega = inf <=> S = 0
+        tsync();
 
         // ---- Step 2: sweeps over the base rows (checks ascending, R12)
         int consec = 0, fires = 0, sweep = 1;
@@ -602,14 +632,30 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
             for (int i = 0; i < mb; ++i) {
                 const int e0 = row_ptr[i], dc = row_ptr[i + 1] - e0;
                 // the window can fill in this row: keep what a mid-row stop has to roll back
-                WCtx cx{l, Lk, Z, belief && W - consec - 1 < Z, keep_S, sweep == 1, lam, hb, pb,
+                WCtx cx{tl, Lk, Z, TEAM ? 32 * warp : 0, belief && W - consec - 1 < Z, keep_S, sweep == 1, lam, hb, pb,
                         Rw + static_cast<size_t>(e0) * K * 32 + l, S + i * Z};
                 WRow<K> ro;
                 ro.first_bad = Z;
                 ro.last_bad = -1;
-                wrow_dispatch<K, ALG, TM, RG || GS>(dc, ent, ptab, e0, lane, static_cast<TexH>(C.phi_tex), cx, ro);
-                const int first_bad = ro.first_bad, last_bad = ro.last_bad;
-                __syncwarp();
+                wrow_dispatch<K, ALG, TM, RG>(dc, ent, ptab, e0, lane, static_cast<TexH>(C.phi_tex), cx, ro);
+                int first_bad = ro.first_bad, last_bad = ro.last_bad;
+                if constexpr (TEAM) {
+                    // the team's first / last unclean check of the row (two buffers: a fast warp may write
+                    // the next row's values while a slow one still reads these)
+                    int* cb = tctl + rowpar * 2 * nwarps;
+                    if (l == 0) {
+                        cb[warp] = first_bad;
+                        cb[nwarps + warp] = last_bad;
+                    }
+                    __syncthreads();                          // also orders the row's stores before the next row
+                    if (belief) {                             // lane w reads warp w's pair, one reduction each
+                        first_bad = __reduce_min_sync(kFull, l < nwarps ? cb[l] : first_bad);
+                        last_bad = __reduce_max_sync(kFull, l < nwarps ? cb[nwarps + l] : last_bad);
+                    }
+                    rowpar ^= 1;
+                } else {
+                    __syncwarp();
+                }
                 if (!belief) {
                     ev += static_cast<long long>(dc) * Z;
                     continue;
@@ -632,7 +678,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                         if (keep_S && !LBP) S[i * Z + rk[k]] = ro.sold.v[k];
                     }
                 }
-                __syncwarp();
+                tsync();
                 if (!syndrome_nz()) {
                     conv = stop = true;                       // output = state after check i Z + rstar
                     ev += static_cast<long long>(dc) * (rstar + 1);
@@ -647,7 +693,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                         swap_bits(rk[k], e0, dc, newbits.v[k]);
                         if (keep_S && !LBP) S[i * Z + rk[k]] = ro.snew.v[k];
                     }
-                __syncwarp();
+                tsync();
             }
             if (stop) break;
             if (a.stop_rule == 2 && !syndrome_nz()) {         // R6: syndrome after every full sweep
@@ -664,14 +710,14 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
         if (!ber) {
             // packed hard decisions (sign of the H bytes), one ballot per word: lane l reads variable 32 w + l
             uint32_t* out = a.bits + static_cast<size_t>(f) * a.ld_words;
-            for (int w = 0; w < a.ld_words; ++w) {
+            for (int w = w0; w < a.ld_words; w += wstep) {
                 const int v = 32 * w + l;
                 const unsigned word = __ballot_sync(kFull, v < N && hb[v] < 0);
                 if (l == (w & 31)) out[w] = word;
             }
             if (a.omega) {
                 float* om = a.omega + static_cast<size_t>(f) * C.M;
-                for (int c = l; c < C.M; c += 32) {
+                for (int c = tl; c < C.M; c += TL) {
                     if (LBP) {
                         om[c] = 0.0f;                         // layered BP: no check-beliefs
                         continue;
@@ -682,7 +728,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                     om[c] = (__float_as_uint(Sv) >> 31) ? -m : m;
                 }
             }
-            if (l == 0) {
+            if (tl == 0) {
                 a.iters[f] = iters;
                 a.flags[f] = flags;
                 if (a.ev) a.ev[f] = ev;
@@ -690,7 +736,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
         } else {
             // decided vs sent: lane l compares variable 32 w + l, a ballot counts the word's errors
             bool info_err = false, cw_err = false;
-            for (int w = 0; w < C.nwords; ++w) {
+            for (int w = w0; w < C.nwords; w += wstep) {
                 const int v = 32 * w + l;
                 const bool dv = v < N && (static_cast<uint32_t>(hb[v] < 0) != ((cw[w] >> l) & 1u));
                 const unsigned d = __ballot_sync(kFull, dv);
@@ -699,8 +745,8 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 info_err |= ie != 0u;
                 cw_err |= d != 0u;
             }
-            const bool fe = info_err, ce = cw_err;
-            if (l == 0) {
+            const bool fe = tany(info_err), ce = tany(cw_err);
+            if (tl == 0) {
                 wcnt[0] += 1;
                 wcnt[2] += fe;
                 wcnt[3] += ce;
@@ -710,12 +756,17 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 wcnt[7] += fires;
             }
         }
-        __syncwarp();
+        tsync();
     }
     if (ber) {
         for (int o = 16; o > 0; o >>= 1) bit_err += __shfl_down_sync(kFull, bit_err, o);
         __syncwarp();
-        if (l == 0) {
+        if (TEAM) {                                           // every warp adds its bit errors, lane 0 of the team the rest
+            if (l == 0 && bit_err) atomicAdd(a.counts + 1, bit_err);
+            if (tl == 0)
+                for (int k = 0; k < 8; ++k)
+                    if (k != 1 && wcnt[k]) atomicAdd(a.counts + k, wcnt[k]);
+        } else if (l == 0) {
             wcnt[1] = bit_err;
             for (int k = 0; k < 8; ++k)
                 if (wcnt[k]) atomicAdd(a.counts + k, wcnt[k]);
@@ -724,20 +775,20 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
 }
 
 // ---------------------------------------------------------------- launch of one instantiation
-template <int K, bool RG, int MAXT, int ALG, int TM, bool GS = false>
+template <int K, bool RG, int MAXT, int ALG, int TM, bool TEAM = false>
 static int wlaunch_t(const KernelArgs& a, const Geometry& g, int grid, cudaStream_t st)
 {
-    auto k = cbp_warp_kernel<K, RG, MAXT, ALG, TM, GS>;
+    auto k = cbp_warp_kernel<K, RG, MAXT, ALG, TM, TEAM>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
     k<<<grid, g.threads, g.smem_bytes, st>>>(a);
     return static_cast<int>(cudaGetLastError());
 }
 
-template <int K, bool RG, int MAXT, int ALG, int TM, bool GS = false>
+template <int K, bool RG, int MAXT, int ALG, int TM, bool TEAM = false>
 static int wocc_t(const Geometry& g, int* out)
 {
-    auto k = cbp_warp_kernel<K, RG, MAXT, ALG, TM, GS>;
+    auto k = cbp_warp_kernel<K, RG, MAXT, ALG, TM, TEAM>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
     return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, g.threads, g.smem_bytes));
@@ -749,17 +800,13 @@ static int wdispatch(const Geometry& g, const KernelArgs* a, int grid, cudaStrea
 {
     const bool rg = g.r_global != 0;
     const int tm = g.tex2;                    // 0 C2B through TEX, 1 both, 2 none
-    if (!g.state_in_smem) {                   // global-state warps (129 <= Z <= 512)
+    if (g.multi) {                            // team frames (one per CTA), K = 1 or 2
 #define CBP_WG(KK)                                                                                            \
         if (g.kslots == KK)                                                                                   \
-            return occ ? wocc_t<KK, true, CBP_WARPK_MAXT, ALG, 0, true>(g, occ)                                 \
-                       : wlaunch_t<KK, true, CBP_WARPK_MAXT, ALG, 0, true>(*a, g, grid, st);
+            return occ ? wocc_t<KK, true, CBP_WARPT_MAXT, ALG, 0, true>(g, occ)                                 \
+                       : wlaunch_t<KK, true, CBP_WARPT_MAXT, ALG, 0, true>(*a, g, grid, st);
+        CBP_WG(1)
         CBP_WG(2)
-        CBP_WG(3)
-        CBP_WG(4)
-        CBP_WG(8)
-        CBP_WG(12)
-        CBP_WG(16)
 #undef CBP_WG
         return static_cast<int>(cudaErrorInvalidConfiguration);
     }

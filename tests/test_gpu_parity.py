@@ -50,12 +50,12 @@ def codes(fpl):
     return get
 
 
-def gpu_decode(g, llr_np, max_iter, rule=0, ld=None, **alg):
+def gpu_decode(g, llr_np, max_iter, rule=0, ld=None, omega=True, **alg):
     F, N = llr_np.shape
     ld = ld or (N + 3) // 4 * 4
     x = torch.zeros((F, ld), dtype=torch.float32)
     x[:, :N] = torch.from_numpy(llr_np)
-    out = g.decode(x.cuda(), max_iter, rule, omega=True, ev=True, **alg)
+    out = g.decode(x.cuda(), max_iter, rule, omega=omega, ev=True, **alg)
     torch.cuda.synchronize()
     return {k: v.cpu().numpy() for k, v in out.items()}
 
@@ -239,13 +239,39 @@ def test_ber_sim_full_size_sampled(codes):
 # ---------------------------------------------------------------- C4: Z = 384, state in global memory
 @pytest.mark.parametrize("rule", [oracle.STOP_SYNDROME, oracle.STOP_BELIEF_M])
 def test_c4_decode_parity(codes, rule):
-    """BASELINE config 4 (N=26112, 42 degree-1 extension columns): the per-frame
-    state (~0.7 MB) does not fit in shared memory, so the kernel keeps it in an
-    L2-resident global workspace; results must still equal the oracle."""
+    """BASELINE config 4 (N=26112, 42 degree-1 extension columns): one frame per CTA on
+    cbp_warp_kernel's team path (Lambda and the H bytes, 130 KB, in shared memory; 12 warps
+    ordered by a CTA barrier per row); with the Omega output (S, 70 KB more) the frame moves to
+    cbp_kernel's L2-resident global workspace.  Both equal the oracle."""
     g, o = codes("C4")
-    assert g.launch_info()["state_in_smem"] == 0
+    li = g.launch_info()
+    assert li["state_in_smem"] == 1 and li["threads"] == 384 and li["frames_per_cta"] == 1, li
     llr, _ = o.channel(1.5, seed=12, frame_begin=0, frames=6)
-    assert_same(gpu_decode(g, llr, 25, rule), o.decode(llr, 25, rule, want_omega=True), o.N)
+    want = o.decode(llr, 25, rule, want_omega=True)
+    assert_same(gpu_decode(g, llr, 25, rule), want, o.N)
+    assert_same(gpu_decode(g, llr, 25, rule, omega=False), want, o.N, omega=False)
+
+
+@pytest.mark.parametrize("env", [{}, {"CBP_WARP_TEAM": "0"}], ids=["team", "cbp_kernel"])
+@pytest.mark.parametrize("name,eb,frames,mi", [("C4", 1.5, 5, 12), ("P8192", 1.5, 24, 20), ("C3a", 2.0, 150, 30)])
+def test_team_frames_equal_oracle(monkeypatch, env, name, eb, frames, mi):
+    """Team frames (one frame per CTA) -- the automatic geometry of C4 and P8192 --
+    and, forced with CBP_WARP_TEAM=0, cbp_kernel's teams for the same codes: decode (no Omega, the
+    team path) and ber_sim (fp32 and int8 streams) equal the oracle frame by frame / counter by
+    counter.  C3a (warp mode) runs as a control."""
+    _need_gpu()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    base, Z = inputs.config_base(name)
+    g, o = cbp.Code(base, Z), oracle.OracleCode(base, Z)
+    lm = 2 if inputs.is_peg(name) else 0
+    llr, _ = o.channel(eb, seed=31, frame_begin=0, frames=frames, llr_mode=lm)
+    for rule in (oracle.STOP_BELIEF_M, oracle.STOP_SYNDROME):
+        assert_same(gpu_decode(g, llr, mi, rule, omega=False), o.decode(llr, mi, rule), o.N, omega=False)
+    for llr_mode in ((2,) if inputs.is_peg(name) else (0, 1)):
+        want = o.ber_sim(eb, 9, 0, frames, mi, llr_mode=llr_mode)
+        got = g.ber_sim(eb, 9, 0, frames, mi, llr_mode=llr_mode).cpu().numpy()
+        assert list(got) == list(want), (llr_mode, list(got), list(want))
 
 
 def test_c4_ber_sim_parity(codes):
