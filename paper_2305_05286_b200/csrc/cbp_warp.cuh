@@ -59,8 +59,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 }
 
 // ---------------------------------------------------------------- the rows
+// Pipe balance of the phi-row fetches (rows with K >= 2 slots per lane: C3a / C5, C3b): edge 0's
+// C2B row from shared memory instead of TEX, edge 6's B2V row through TEX instead of shared memory.
+// C5 -1.5..2 % (A/B over several boxes; K = 1 codes measured slower with it and keep 0).
 #ifndef CBP_B2V_TEX_MASK
-#define CBP_B2V_TEX_MASK 0  // bit e: edge e (mod 8) of a row fetches its B2V phi row through TEX (A/B runs)
+#define CBP_B2V_TEX_MASK 0x40  // bit e: edge e (mod 8) of a row fetches its B2V phi row through TEX
+#endif
+#ifndef CBP_C2B_LDS_MASK
+#define CBP_C2B_LDS_MASK 0x01  // bit e: edge e (mod 8) of a row fetches its C2B phi row from shared memory
 #endif
 #ifndef CBP_WARP_LEAN
 #define CBP_WARP_LEAN 0     // 1: entries and R re-read per slot (fewer registers, A/B runs)
@@ -93,7 +99,51 @@ struct SlotVals {
         for (int j = 0; j < K; ++j)
             if (j == k) v[j] = x;
     }
+    __device__ __forceinline__ T get(int k) const
+    {
+        T x = v[0];
+#pragma unroll
+        for (int j = 1; j < K; ++j)
+            if (j == k) x = v[j];
+        return x;
+    }
 };
+
+// ---------------------------------------------------------------- per-frame (cold) code
+// The per-frame code (channel, encoder, stop-window verification, final syndrome, outputs) runs
+// once per frame between long stretches of the row loop.  Its instructions share the SM's 32 KB
+// L1.5 instruction cache with the hot row body, so it is kept compact: loops over the K slots are
+// not unrolled, and the syndrome is one out-of-line function instead of three inlined copies
+// (C5 at 2.5 dB switches frames every ~7 sweeps; measured: one shared max-dc body -9 %).
+
+// parity of the team's valid checks over all rows from the hard decisions (sign of H): true if
+// some check is unsatisfied (early exit every 4 rows)
+template <int K, bool TEAM>
+__device__ __noinline__ bool w_syndrome_nz(const int4* __restrict__ ent, const int32_t* __restrict__ row_ptr,
+                                           const int8_t* __restrict__ hb, int mb, int Z, int tl, int Lk)
+{
+    auto tany = [&](bool p) -> bool {
+        if constexpr (TEAM) return __syncthreads_or(p) != 0;
+        else return __any_sync(0xffffffffu, p);
+    };
+    uint32_t nz = 0;
+    for (int i = 0; i < mb; ++i) {
+        if ((i & 3) == 0 && i && tany(nz != 0u)) return true;   // an unsatisfied check: done
+        uint32_t par = 0;                                     // bit k: parity of check i Z + r_k
+        for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+            const int2 A = *reinterpret_cast<const int2*>(ent + 2 * e);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int r = tl + k * Lk;
+                const bool v = tl < Lk && r < Z;
+                const int vv = A.x + wrap((v ? r : Z - 1) + A.y, Z);
+                par ^= v ? static_cast<uint32_t>(hb[vv] < 0) << k : 0u;
+            }
+        }
+        nz |= par;
+    }
+    return tany(nz != 0u);
+}
 
 // What a row reports to the stop logic: first / last unclean check, and for a possible mid-row
 // stop the slots' previous decision bits and check records (old / new).
@@ -139,9 +189,14 @@ __device__ __forceinline__ void wslot_done(const WCtx& c, int k, int rr, bool v,
 // a loop that is not unrolled: the unrolled K x DC bodies overflowed the 32 KB L1.5 instruction
 // cache (ncu: no_instruction stalls 2.3 per issue, issue active 37 %).  A slot beyond Z (v false)
 // computes on check Z - 1 and stores nothing but its private R words.
+// lastoff: the row has DC - 1 edges and runs this body with its last edge masked (CBP_DCMERGE:
+// rows of the code's max dc and of max dc - 1 share one body, halving the hot code that the
+// warps of an SMSP stream through the instruction caches).  The masked edge reads the previous
+// edge's variable (valid addresses), loads no R, adds nothing to S / the sign / flip / rollback
+// words and stores nothing.
 template <int DC, int K, int ALG, int TM, bool RG>
 __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
-                                     const Lane& L, TexH tex, const WCtx& c, WRow<K>& o)
+                                     const Lane& L, TexH tex, const WCtx& c, WRow<K>& o, bool lastoff = false)
 {
     constexpr bool LBP = ALG == 2;
     constexpr bool TEXC = TM != 2, TEXB = TM == 1;             // phi rows: C2B / B2V through the texture pipe
@@ -149,11 +204,13 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
     int2 A[DC];
 #pragma unroll
     for (int e = 0; e < DC; ++e) A[e] = *reinterpret_cast<const int2*>(ent + 2 * (e0 + e));
+    if constexpr (DC >= 2)
+        if (lastoff) A[DC - 1] = A[DC - 2];
     // R words of the next slot are requested before the current slot's update (their global /
     // L2 latency then overlaps it); slot 0's are loaded here
     float rnext[DC];
 #pragma unroll
-    for (int e = 0; e < DC; ++e) rnext[e] = c.r0 ? 0.0f : rld<RG>(c.rrow + e * K * 32);
+    for (int e = 0; e < DC; ++e) rnext[e] = (c.r0 || (e == DC - 1 && lastoff)) ? 0.0f : rld<RG>(c.rrow + e * K * 32);
 #endif
 #pragma unroll 1
     for (int k = 0; k < K; ++k) {
@@ -175,7 +232,8 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
         for (int e = 0; e < DC; ++e) ro[e][0] = rnext[e];          // R_{c->v}
         if (k + 1 < K) {
 #pragma unroll
-            for (int e = 0; e < DC; ++e) rnext[e] = c.r0 ? 0.0f : rld<RG>(rk + 32 + e * K * 32);
+            for (int e = 0; e < DC; ++e)
+                rnext[e] = (c.r0 || (e == DC - 1 && lastoff)) ? 0.0f : rld<RG>(rk + 32 + e * K * 32);
         }
 #endif
         RowAcc<1> acc;
@@ -192,25 +250,42 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
             vs[e][1] = LBP ? vs[e][0] : __int_as_float(static_cast<int>(c.hb[vi[e]]));
         }
 #pragma unroll
-        for (int e = 0; e < DC; ++e) cbp_phase1<1, TEXC>(vs[e], ro[e], q[e], ph[e], ptab, L, tex, acc);
+        for (int e = 0; e < DC; ++e) {
+            // C2B rows through TEX except for the edges CBP_C2B_LDS_MASK selects (folded after unrolling)
+            constexpr int kC2BLds = (K >= 2 && TM == 0) ? CBP_C2B_LDS_MASK : 0;   // TM 1: no table in shared memory
+            if (e == DC - 1 && DC >= 2) {                       // possibly masked (lastoff)
+                RowAcc<1> t = acc;
+                if (TEXC && ((kC2BLds >> (e & 7)) & 1) == 0)
+                    cbp_phase1<1, true>(vs[e], ro[e], q[e], ph[e], ptab, L, tex, t);
+                else
+                    cbp_phase1<1, false>(vs[e], ro[e], q[e], ph[e], ptab, L, tex, t);
+                if (!lastoff) acc = t;
+            } else if (TEXC && ((kC2BLds >> (e & 7)) & 1) == 0) {
+                cbp_phase1<1, true>(vs[e], ro[e], q[e], ph[e], ptab, L, tex, acc);
+            } else {
+                cbp_phase1<1, false>(vs[e], ro[e], q[e], ph[e], ptab, L, tex, acc);
+            }
+        }
         // all B2V lookups of the row before its first store: a table load may not move above a
         // shared-memory store the compiler cannot prove disjoint (one dependent chain per edge otherwise)
         float rn[DC][1], lamn[DC][1];
 #pragma unroll
         for (int e = 0; e < DC; ++e) {
             // B2V rows: through TEX for the edges CBP_B2V_TEX_MASK selects (balances the TEX and LSU pipes)
-            if (TEXB || (((CBP_B2V_TEX_MASK >> (e & 7)) & 1) != 0))   // folded after unrolling
+            constexpr int kB2VTex = (K >= 2 && TM == 0) ? CBP_B2V_TEX_MASK : 0;
+            if (TEXB || ((kB2VTex >> (e & 7)) & 1) != 0)   // folded after unrolling
                 cbp_phase2<1, true>(acc, q[e], ph[e], rn[e], lamn[e], ptab, L, tex);
             else
                 cbp_phase2<1, false>(acc, q[e], ph[e], rn[e], lamn[e], ptab, L, tex);
         }
 #pragma unroll
         for (int e = 0; e < DC; ++e) {
-            if (v) {
+            const bool on = !(e == DC - 1 && lastoff);
+            if (v && on) {
                 c.lam[vi[e]] = lamn[e][0];
                 c.hb[vi[e]] = static_cast<int8_t>(__float_as_uint(LBP ? lamn[e][0] : vs[e][0]) >> 24);   // H_v
             }
-            rst<RG>(rk + e * K * 32, rn[e][0]);                    // equ_s4e22 commit of R_{c->v}
+            if (on) rst<RG>(rk + e * K * 32, rn[e][0]);            // equ_s4e22 commit of R_{c->v}
         }
         wslot_done<K, LBP>(c, k, rr, v, acc, o);
     }
@@ -308,22 +383,30 @@ __device__ __forceinline__ void wrow_park(const int4* __restrict__ ent, const fl
     }
 }
 
+#ifndef CBP_DCMERGE
+#define CBP_DCMERGE 1
+#endif
 template <int K, int ALG, int TM, bool RG>
-__device__ __forceinline__ void wrow_dispatch(int dc, const int4* __restrict__ ent, const float4* __restrict__ ptab,
+__device__ __forceinline__ void wrow_dispatch(int dc, int max_dc, const int4* __restrict__ ent, const float4* __restrict__ ptab,
                                               int e0, const Lane& L, TexH tex, const WCtx& c, WRow<K>& o)
 {
+    // rows of max dc - 1 edges run the max-dc body with the last edge masked: one call site per body
+    // (wrow is inlined, so a second call site would be a second copy).  Only for K >= 2 slots per lane
+    // (C3a / C5); with K = 1 (C2, P2048) the merged body measured slower (+26 %, +2 %).
+    const bool lastoff = CBP_DCMERGE && K >= 2 && dc + 1 == max_dc && max_dc <= CBP_DC_REG && dc >= 2;
+    if (lastoff) dc += 1;
     switch (dc) {
 #if CBP_DC_REG >= 1
-    case 1: wrow<1, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
-    case 2: wrow<2, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
-    case 3: wrow<3, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
-    case 4: wrow<4, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
-    case 5: wrow<5, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
-    case 6: wrow<6, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
+    case 1: wrow<1, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
+    case 2: wrow<2, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
+    case 3: wrow<3, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
+    case 4: wrow<4, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
+    case 5: wrow<5, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
+    case 6: wrow<6, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
 #endif
 #if CBP_DC_REG >= 8
-    case 7: wrow<7, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
-    case 8: wrow<8, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o); break;
+    case 7: wrow<7, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
+    case 8: wrow<8, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
 #endif
     default: wrow_park<K, ALG, TM, RG>(ent, ptab, e0, dc, L, tex, c, o); break;
     }
@@ -420,24 +503,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
     const uint32_t key0 = static_cast<uint32_t>(a.seed), key1 = static_cast<uint32_t>(a.seed >> 32);
     unsigned long long bit_err = 0;                           // this lane's share (ber_sim)
 
-    // parity of this lane's valid checks over all rows from the hard decisions (sign of H)
-    auto syndrome_nz = [&]() -> bool {
-        uint32_t nz = 0;
-        for (int i = 0; i < mb; ++i) {
-            if ((i & 3) == 0 && i && tany(nz != 0u)) return true;   // an unsatisfied check: done
-            uint32_t par = 0;                                 // bit k: parity of check i Z + r_k
-            for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
-                const int2 A = *reinterpret_cast<const int2*>(ent + 2 * e);
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const int v = A.x + wrap(rk[k] + A.y, Z);
-                    par ^= vk[k] ? static_cast<uint32_t>(hb[v] < 0) << k : 0u;
-                }
-            }
-            nz |= par;
-        }
-        return tany(nz != 0u);
-    };
+    auto syndrome_nz = [&]() -> bool { return w_syndrome_nz<K, TEAM>(ent, row_ptr, hb, mb, Z, tl, Lk); };
     // hard decisions of slot k's variables in row (e0, dc) <- bits (edge e at bit dc-1-e); returns the previous
     auto swap_bits = [&](int r, int e0, int dc, uint32_t bits) -> uint32_t {
         uint32_t prev = 0;
@@ -563,10 +629,10 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 for (int k = 0; k < K; ++k)
                     if (vk[k]) Qs[C.kb * Z + rk[k]] = p0[k] ? -1.0f : 1.0f;
                 tsync();
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    if (!vk[k]) continue;
-                    const int r = rk[k];
+#pragma unroll 1
+                for (int k = 0; k < K; ++k) {                 // not unrolled: per-frame code
+                    const int r = tl + k * Lk;
+                    if (!(tl < Lk && r < Z)) continue;
                     uint32_t pprev = 0;
                     for (int t = 1; t < C.core; ++t) {
                         uint32_t pt = static_cast<uint32_t>(hb[(t - 1) * Z + r]);
@@ -637,7 +703,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 WRow<K> ro;
                 ro.first_bad = Z;
                 ro.last_bad = -1;
-                wrow_dispatch<K, ALG, TM, RG>(dc, ent, ptab, e0, lane, static_cast<TexH>(C.phi_tex), cx, ro);
+                wrow_dispatch<K, ALG, TM, RG>(dc, C.max_dc, ent, ptab, e0, lane, static_cast<TexH>(C.phi_tex), cx, ro);
                 int first_bad = ro.first_bad, last_bad = ro.last_bad;
                 if constexpr (TEAM) {
                     // the team's first / last unclean check of the row (two buffers: a fast warp may write
@@ -671,11 +737,13 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 // checks show their pre-row decisions and S while the syndrome is verified (R5)
                 SlotVals<K, uint32_t> newbits;
 #pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    newbits.v[k] = 0;
-                    if (vk[k] && rk[k] > rstar) {
-                        newbits.v[k] = swap_bits(rk[k], e0, dc, ro.oldb.v[k]);
-                        if (keep_S && !LBP) S[i * Z + rk[k]] = ro.sold.v[k];
+                for (int k = 0; k < K; ++k) newbits.v[k] = 0;
+#pragma unroll 1
+                for (int k = 0; k < K; ++k) {                 // not unrolled: per-frame code (see above)
+                    const int r = tl + k * Lk;
+                    if (tl < Lk && r < Z && r > rstar) {
+                        newbits.set(k, swap_bits(r, e0, dc, ro.oldb.get(k)));
+                        if (keep_S && !LBP) S[i * Z + r] = ro.sold.get(k);
                     }
                 }
                 tsync();
@@ -687,12 +755,14 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 fires += 1;                                   // failed verification: resume (R5)
                 ev += static_cast<long long>(dc) * Z;
                 consec = Z - 1 - max(last_bad, rstar);
-#pragma unroll
-                for (int k = 0; k < K; ++k)
-                    if (vk[k] && rk[k] > rstar) {
-                        swap_bits(rk[k], e0, dc, newbits.v[k]);
-                        if (keep_S && !LBP) S[i * Z + rk[k]] = ro.snew.v[k];
+#pragma unroll 1
+                for (int k = 0; k < K; ++k) {
+                    const int r = tl + k * Lk;
+                    if (tl < Lk && r < Z && r > rstar) {
+                        swap_bits(r, e0, dc, newbits.get(k));
+                        if (keep_S && !LBP) S[i * Z + r] = ro.snew.get(k);
                     }
+                }
                 tsync();
             }
             if (stop) break;
