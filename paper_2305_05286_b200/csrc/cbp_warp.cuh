@@ -88,6 +88,72 @@ __device__ __forceinline__ void rst(float* p, float v)
     else *p = v;
 }
 
+// ---------------------------------------------------------------- two edges on the packed FP32x2 pipe
+// CBP_PAIR: the fp32 steps of two independent edges of a row issue as one FADD2 / FFMA2 (sm_100
+// packed FP32: each element is the same IEEE operation with the same rounding, so every bit is
+// the contract's): Q^new = Lambda - R, the phi index's 16x magic (fma.rz), C - m, u_hi and u_lo,
+// S - Phi and Lambda' = Q^new + R^new.  The cubic stays scalar (its coefficients come from two
+// different table rows).  A/B switch, off: measured slower twice (C5 +1.3 % with the round-2 body,
+// +4 % after the instruction-cache work; C2 +2..4 %) although it issues ~4.5 fewer instructions per
+// edge visit -- the packed forms cost latency / register-pair moves on this dependent chain.
+#ifndef CBP_PAIR
+#define CBP_PAIR 0
+#endif
+
+// phi32 of |x.x| and |x.y| (contract.cuh phi32_index + phi32_cubic, the FP steps paired); TA / TB:
+// the row of element a / b through the texture pipe
+// (ta / tb are compile-time constants after the callers' unrolling)
+__device__ __forceinline__ float2 phi2_sel(float2 x, bool ta, bool tb, const float4* __restrict__ ptab, const Lane& L,
+                                           TexH tex)
+{
+    x.x = fminf(fmaxf(fabsf(x.x), kPhiLo), kPhiHi);
+    x.y = fminf(fmaxf(fabsf(x.y), kPhiLo), kPhiHi);
+    const uint32_t b0 = __float_as_uint(x.x), b1 = __float_as_uint(x.y);
+    uint32_t ub0, ub1;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(ub0) : "r"(b0), "r"(L.m19), "r"(L.one));   // (b & m19) | one
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(ub1) : "r"(b1), "r"(L.m19), "r"(L.one));
+    const float2 u_lo = __fadd2_rn(make_float2(__uint_as_float(ub0), __uint_as_float(ub1)), make_float2(-1.0f, -1.0f));
+    const float2 m = __ffma2_rz(x, make_float2(16.0f, 16.0f), make_float2(8388576.0f, 8388576.0f));
+    const float2 cm = __fadd2_rn(make_float2(8388576.0f, 8388576.0f), make_float2(-m.x, -m.y));
+    const float2 u_hi = __ffma2_rn(x, make_float2(16.0f, 16.0f), cm);
+    const bool h0 = x.x >= 2.0f, h1 = x.y >= 2.0f;
+    const int s0 = h0 ? static_cast<int>(__float_as_uint(m.x)) - (0x4b000000 - 704) : static_cast<int>(b0 >> 19) - 1344;
+    const int s1 = h1 ? static_cast<int>(__float_as_uint(m.y)) - (0x4b000000 - 704) : static_cast<int>(b1 >> 19) - 1344;
+    CBP_CHECK(s0 >= 0 && s0 < kPhiSegs && s1 >= 0 && s1 < kPhiSegs);
+    const float u0 = h0 ? u_hi.x : u_lo.x, u1 = h1 ? u_hi.y : u_lo.y;
+    const float4 c0 = ta ? tex1Dfetch<float4>(tex, s0) : ptab[s0];
+    const float4 c1 = tb ? tex1Dfetch<float4>(tex, s1) : ptab[s1];
+    return make_float2(phi32_cubic(c0, u0), phi32_cubic(c1, u1));
+}
+
+// cbp_phase1 (cbp_kernel.cuh) for edges a, b in this order: flip test, rollback bits, Q^new, C2B phi,
+// S in ascending order, sign
+__device__ __forceinline__ void wphase1_pair(const float (&va)[2], const float (&vb)[2], float ra, float rb, float2& q,
+                                             float2& ph, bool ta, bool tb, const float4* __restrict__ ptab,
+                                             const Lane& L, TexH tex, RowAcc<1>& acc)
+{
+    const uint32_t la = __float_as_uint(va[0]), ha = __float_as_uint(va[1]);
+    const uint32_t lb = __float_as_uint(vb[0]), hb = __float_as_uint(vb[1]);
+    acc.flipw[0] |= (la ^ ha) | (lb ^ hb);                      // equ_s4e24 (R7)
+    acc.oldbits[0] = __funnelshift_l(hb, __funnelshift_l(ha, acc.oldbits[0], 1), 1);
+    q = __fadd2_rn(make_float2(va[0], vb[0]), make_float2(-ra, -rb));   // equ_s4e19: Lambda - R (exact negation)
+    ph = phi2_sel(q, ta, tb, ptab, L, tex);                     // C2B (equ_s4e21)
+    acc.Ssum[0] = __fadd_rn(__fadd_rn(acc.Ssum[0], ph.x), ph.y);   // R12
+    acc.negw[0] ^= __float_as_uint(q.x) ^ __float_as_uint(q.y);
+}
+
+// cbp_phase2 for edges a, b: R^new = sgn(Omega) sgn(Q^new) phi(|S - Phi|), Lambda' = Q^new + R^new
+__device__ __forceinline__ void wphase2_pair(const RowAcc<1>& acc, float2 q, float2 ph, float2& rn, float2& lamn,
+                                             bool ta, bool tb, const float4* __restrict__ ptab, const Lane& L,
+                                             TexH tex)
+{
+    const float2 d = __fadd2_rn(make_float2(acc.Ssum[0], acc.Ssum[0]), make_float2(-ph.x, -ph.y));   // S - Phi (R10)
+    const float2 mag = phi2_sel(d, ta, tb, ptab, L, tex);
+    rn.x = __uint_as_float(__float_as_uint(mag.x) | ((acc.negw[0] ^ __float_as_uint(q.x)) & kSign));
+    rn.y = __uint_as_float(__float_as_uint(mag.y) | ((acc.negw[0] ^ __float_as_uint(q.y)) & kSign));
+    lamn = __fadd2_rn(q, rn);                                   // equ_s4e20 of the next visitor
+}
+
 // K per-slot values in registers, written / read at a runtime slot index by predicated moves
 // (a dynamically indexed array would live in local memory)
 template <int K, typename T>
@@ -115,6 +181,9 @@ struct SlotVals {
 // L1.5 instruction cache with the hot row body, so it is kept compact: loops over the K slots are
 // not unrolled, and the syndrome is one out-of-line function instead of three inlined copies
 // (C5 at 2.5 dB switches frames every ~7 sweeps; measured: one shared max-dc body -9 %).
+
+// Philox4x32-10 (contract.cuh) out of line: one copy for the info words and the noise
+static __device__ __noinline__ u32x4 w_philox(u32x4 c, uint32_t k0, uint32_t k1) { return philox4x32_10(c, k0, k1); }
 
 // parity of the team's valid checks over all rows from the hard decisions (sign of H): true if
 // some check is unsatisfied (early exit every 4 rows)
@@ -249,10 +318,25 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
             // H_v: the sign-extended byte carries the decision in bit 31 (layered BP: Lambda_v itself)
             vs[e][1] = LBP ? vs[e][0] : __int_as_float(static_cast<int>(c.hb[vi[e]]));
         }
+        // C2B rows through TEX except for the edges CBP_C2B_LDS_MASK selects, B2V rows from shared memory
+        // except for the edges CBP_B2V_TEX_MASK selects (folded after unrolling)
+        constexpr int kC2BLds = (K >= 2 && TM == 0) ? CBP_C2B_LDS_MASK : 0;   // TM 1: no table in shared memory
+        constexpr int kB2VTex = (K >= 2 && TM == 0) ? CBP_B2V_TEX_MASK : 0;
+        float rn[DC][1], lamn[DC][1];
+        // edges (0,1), (2,3), ... below the last on the packed pipe (CBP_PAIR); the last edge (maskable,
+        // lastoff) and an odd one alone
+        constexpr int NP = CBP_PAIR ? (DC - 1) / 2 : 0;
 #pragma unroll
-        for (int e = 0; e < DC; ++e) {
-            // C2B rows through TEX except for the edges CBP_C2B_LDS_MASK selects (folded after unrolling)
-            constexpr int kC2BLds = (K >= 2 && TM == 0) ? CBP_C2B_LDS_MASK : 0;   // TM 1: no table in shared memory
+        for (int j = 0; j < NP; ++j) {
+            const int e = 2 * j;
+            float2 q2, ph2;
+            wphase1_pair(vs[e], vs[e + 1], ro[e][0], ro[e + 1][0], q2, ph2, TEXC && ((kC2BLds >> (e & 7)) & 1) == 0,
+                         TEXC && ((kC2BLds >> ((e + 1) & 7)) & 1) == 0, ptab, L, tex, acc);
+            q[e][0] = q2.x; q[e + 1][0] = q2.y;
+            ph[e][0] = ph2.x; ph[e + 1][0] = ph2.y;
+        }
+#pragma unroll
+        for (int e = 2 * NP; e < DC; ++e) {
             if (e == DC - 1 && DC >= 2) {                       // possibly masked (lastoff)
                 RowAcc<1> t = acc;
                 if (TEXC && ((kC2BLds >> (e & 7)) & 1) == 0)
@@ -268,12 +352,19 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
         }
         // all B2V lookups of the row before its first store: a table load may not move above a
         // shared-memory store the compiler cannot prove disjoint (one dependent chain per edge otherwise)
-        float rn[DC][1], lamn[DC][1];
 #pragma unroll
-        for (int e = 0; e < DC; ++e) {
-            // B2V rows: through TEX for the edges CBP_B2V_TEX_MASK selects (balances the TEX and LSU pipes)
-            constexpr int kB2VTex = (K >= 2 && TM == 0) ? CBP_B2V_TEX_MASK : 0;
-            if (TEXB || ((kB2VTex >> (e & 7)) & 1) != 0)   // folded after unrolling
+        for (int j = 0; j < NP; ++j) {
+            const int e = 2 * j;
+            float2 rn2, lamn2;
+            wphase2_pair(acc, make_float2(q[e][0], q[e + 1][0]), make_float2(ph[e][0], ph[e + 1][0]), rn2, lamn2,
+                         TEXB || ((kB2VTex >> (e & 7)) & 1) != 0, TEXB || ((kB2VTex >> ((e + 1) & 7)) & 1) != 0, ptab,
+                         L, tex);
+            rn[e][0] = rn2.x; rn[e + 1][0] = rn2.y;
+            lamn[e][0] = lamn2.x; lamn[e + 1][0] = lamn2.y;
+        }
+#pragma unroll
+        for (int e = 2 * NP; e < DC; ++e) {
+            if (TEXB || ((kB2VTex >> (e & 7)) & 1) != 0)
                 cbp_phase2<1, true>(acc, q[e], ph[e], rn[e], lamn[e], ptab, L, tex);
             else
                 cbp_phase2<1, false>(acc, q[e], ph[e], rn[e], lamn[e], ptab, L, tex);
@@ -386,6 +477,9 @@ __device__ __forceinline__ void wrow_park(const int4* __restrict__ ent, const fl
 #ifndef CBP_DCMERGE
 #define CBP_DCMERGE 1
 #endif
+#ifndef CBP_DCMERGE_MINK
+#define CBP_DCMERGE_MINK 2   // smallest K (slots per lane) that merges
+#endif
 template <int K, int ALG, int TM, bool RG>
 __device__ __forceinline__ void wrow_dispatch(int dc, int max_dc, const int4* __restrict__ ent, const float4* __restrict__ ptab,
                                               int e0, const Lane& L, TexH tex, const WCtx& c, WRow<K>& o)
@@ -393,7 +487,7 @@ __device__ __forceinline__ void wrow_dispatch(int dc, int max_dc, const int4* __
     // rows of max dc - 1 edges run the max-dc body with the last edge masked: one call site per body
     // (wrow is inlined, so a second call site would be a second copy).  Only for K >= 2 slots per lane
     // (C3a / C5); with K = 1 (C2, P2048) the merged body measured slower (+26 %, +2 %).
-    const bool lastoff = CBP_DCMERGE && K >= 2 && dc + 1 == max_dc && max_dc <= CBP_DC_REG && dc >= 2;
+    const bool lastoff = CBP_DCMERGE && K >= CBP_DCMERGE_MINK && dc + 1 == max_dc && max_dc <= CBP_DC_REG && dc >= 2;
     if (lastoff) dc += 1;
     switch (dc) {
 #if CBP_DC_REG >= 1
@@ -585,7 +679,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 // (a2) info word w = Philox(w/4, f_lo, f_hi, 0)[w % 4]
                 const int nblk = (C.kwords + 3) / 4;
                 for (int b = tl; b < nblk; b += TL) {
-                    const u32x4 x = philox4x32_10(u32x4{static_cast<uint32_t>(b), flo, fhi, 0u}, key0, key1);
+                    const u32x4 x = w_philox(u32x4{static_cast<uint32_t>(b), flo, fhi, 0u}, key0, key1);
                     const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
                     for (int m = 0; m < 4; ++m) {
@@ -662,13 +756,14 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
             // (a4) y = (1 - 2c) + sigma n, L = (2/sigma^2) y (equ_s4e15, R17); int8 stream
             const int nblk = (N + 3) / 4;
             for (int b = tl; b < nblk; b += TL) {
-                const u32x4 x = philox4x32_10(u32x4{static_cast<uint32_t>(b), flo, fhi, 1u}, key0, key1);
-                float n[4];
-                box_muller(x.x, x.y, n[0], n[1]);
-                box_muller(x.z, x.w, n[2], n[3]);
+                const u32x4 x = w_philox(u32x4{static_cast<uint32_t>(b), flo, fhi, 1u}, key0, key1);
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {                 // one Box-Muller body for both pairs (per-frame code)
+                  float n[2];
+                  box_muller(h ? x.z : x.x, h ? x.w : x.y, n[0], n[1]);
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    const int v = 4 * b + m;
+                  for (int m = 0; m < 2; ++m) {
+                    const int v = 4 * b + 2 * h + m;
                     if (v >= N) break;
                     const float y = __fadd_rn(Qs[v], __fmul_rn(a.sigma, n[m]));
                     float Lv = __fmul_rn(a.scale, y);
@@ -680,6 +775,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                     const float x0 = __fadd_rn(Lv, 0.0f);
                     lam[v] = x0;
                     hb[v] = static_cast<int8_t>(__float_as_uint(x0) >> 24);
+                  }
                 }
             }
         }
