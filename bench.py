@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import re
 import os
 import socket
 import subprocess
@@ -131,7 +132,11 @@ def kernel_traffic(cfg_name: str):
     """DRAM bytes per frame of the dominant kernel from the latest committed `ncu --set full`
     capture of the same workload (profiles/r*_<config>_kernel_traffic.json, written by
     tools/profile_summary.py), or None."""
-    caps = sorted((ROOT / "profiles").glob(f"r*_{cfg_name.lower()}_kernel_traffic.json"))
+    def tag(f):   # r02s < r02ba < r02bo: round, then capture letters by length and order
+        m = re.match(r"r(\d+)([a-z]*)_", f.name)
+        return (int(m.group(1)), len(m.group(2)), m.group(2)) if m else (0, 0, "")
+
+    caps = sorted((ROOT / "profiles").glob(f"r*_{cfg_name.lower()}_kernel_traffic.json"), key=tag)
     if not caps:
         return None
     d = json.loads(caps[-1].read_text())
