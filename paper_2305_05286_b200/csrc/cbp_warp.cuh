@@ -481,13 +481,16 @@ __device__ __forceinline__ void wrow_park(const int4* __restrict__ ent, const fl
 #define CBP_DCMERGE_MINK 2   // smallest K (slots per lane) that merges
 #endif
 template <int K, int ALG, int TM, bool RG>
-__device__ __forceinline__ void wrow_dispatch(int dc, int max_dc, const int4* __restrict__ ent, const float4* __restrict__ ptab,
-                                              int e0, const Lane& L, TexH tex, const WCtx& c, WRow<K>& o)
+__device__ __forceinline__ void wrow_dispatch(int dc, int max_dc, bool merge, const int4* __restrict__ ent,
+                                              const float4* __restrict__ ptab, int e0, const Lane& L, TexH tex,
+                                              const WCtx& c, WRow<K>& o)
 {
     // rows of max dc - 1 edges run the max-dc body with the last edge masked: one call site per body
     // (wrow is inlined, so a second call site would be a second copy).  Only for K >= 2 slots per lane
-    // (C3a / C5); with K = 1 (C2, P2048) the merged body measured slower (+26 %, +2 %).
-    const bool lastoff = CBP_DCMERGE && K >= CBP_DCMERGE_MINK && dc + 1 == max_dc && max_dc <= CBP_DC_REG && dc >= 2;
+    // (C3a / C5); with K = 1 (C2, P2048) the merged body measured slower (+26 %, +2 %).  `merge`: only in
+    // the fused ber_sim, whose per-frame channel code competes for the instruction cache (C5 -4.5 %); plain
+    // decoding keeps one body per dc (the masked edge's work costs it 4 %).
+    const bool lastoff = CBP_DCMERGE && K >= CBP_DCMERGE_MINK && merge && dc + 1 == max_dc && max_dc <= CBP_DC_REG && dc >= 2;
     if (lastoff) dc += 1;
     switch (dc) {
 #if CBP_DC_REG >= 1
@@ -799,7 +802,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 WRow<K> ro;
                 ro.first_bad = Z;
                 ro.last_bad = -1;
-                wrow_dispatch<K, ALG, TM, RG>(dc, C.max_dc, ent, ptab, e0, lane, static_cast<TexH>(C.phi_tex), cx, ro);
+                wrow_dispatch<K, ALG, TM, RG>(dc, C.max_dc, ber, ent, ptab, e0, lane, static_cast<TexH>(C.phi_tex), cx, ro);
                 int first_bad = ro.first_bad, last_bad = ro.last_bad;
                 if constexpr (TEAM) {
                     // the team's first / last unclean check of the row (two buffers: a fast warp may write
