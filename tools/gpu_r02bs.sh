@@ -1,0 +1,11 @@
+#!/bin/bash
+# A/B: warp index through REDUX (uniform state bases, libcbp.so) vs threadIdx >> 5 (libcbp_nouw.so); parity subset
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+ab() { for lib in "$@"; do for c in "C5 2.5" "C3a 1.5" "C2 2.0" "C3b 4.0" "P2048 2.5"; do set -- $c
+  echo "== $lib $1 $2 $(CBP_LIB=$PWD/paper_2305_05286_b200/$lib timeout 200 python tools/prof_one.py --config $1 --ebn0 $2 --reps 5 --frames 100000 2>&1 | grep best)"; done; done; }
+{ ab libcbp_nouw.so libcbp.so libcbp_nouw.so libcbp.so
+  for lib in libcbp.so libcbp_nouw.so; do CBP_LIB=$PWD/paper_2305_05286_b200/$lib timeout 300 python tools/split_ber.py --config C5 --ebn0 2.5 --frames 200000 | head -1; done
+  timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -p no:cacheprovider -k "not all_frames" 2>&1 | tail -2
+} > gpurun_out/r02bs_ab.log 2>&1
+cat gpurun_out/r02bs_ab.log
