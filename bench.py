@@ -428,6 +428,32 @@ def main():
                "what": f"{pipeline.API_NAME} on {Fe} host-resident fp32 frames/GPU of the same workload (pinned host "
                        f"LLRs; H2D + decode + D2H of bits/iters/flags inside the timed region; host wall clock, "
                        f"max over ranks; {reps} reps)"}
+        # the same through cbp_decode_host_i8 with the int8 stream of the workload (a quarter of the H2D bytes:
+        # the fp32 e2e is bound by the pinned host-to-device copy, 7.8 KB per frame)
+        ld8 = (code.N + 15) // 16 * 16
+        host8 = torch.empty((Fe, ld8), dtype=torch.int8, pin_memory=True)
+        for b in range(0, Fe, 1 << 17):
+            n = min(1 << 17, Fe - b)
+            llr_, _ = code.channel(ebn0s[0], args.seed + 1, rank * Fe + b, n, llr_mode=1, want_cw=False)
+            q = torch.zeros((n, ld8), dtype=torch.int8, device=dev)
+            q[:, :code.N] = (llr_[:, :code.N] * 4.0).round().to(torch.int8)   # exact: the stream's L = q / 4
+            host8[b:b + n].copy_(q)
+        torch.cuda.synchronize()
+        code.decode_host(host8, cfg.max_iter, out=hout, scale=0.25)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            code.decode_host(host8, cfg.max_iter, out=hout, scale=0.25)
+        te8 = time.perf_counter() - t0
+        tmax = torch.tensor([te8], dtype=torch.float64, device=dev)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        te8 = tmax.item()
+        e2e["int8_stream"] = {"value": reps * Fe * world * code.K / te8 / 1e9, "unit": UNIT,
+                              "frames_per_s": reps * Fe * world / te8,
+                              "h2d_bytes_per_step": Fe * ld8 * world, "d2h_bytes_per_step": Fe * (code.words * 4 + 5) * world,
+                              "what": "cbp_decode_host_i8 on the int8 stream of the same frames (q = sat(rint(4L), "
+                                      "+-127), scale 0.25), same timing"}
+        del host8
 
     # the other BASELINE configs and variants, one timed fused launch each (after a warm-up launch)
     others = {}
