@@ -4,9 +4,11 @@
 Headline workload = BASELINE configs[4] (C5, the metric's "per GPU and 8xB200" scaling
 workload): the N=1944 rate-1/2 QC-LDPC code (C3a) at Eb/N0 = 2.5 dB, max_iter 30, fp32 LLR
 stream; the int8 stream (q = sat(rint(4L), +-127)) is measured the same way and reported
-beside it.  A step = one fused cbp_ber_sim launch over this rank's slice of the C5 frame range
-(Philox info bits -> encoder -> BPSK/AWGN -> CBP decode -> error counting), followed by the
-NCCL all-reduce of the 8 counters.  Step s of rank g simulates global frames
+beside it.  A step = this rank's slice of the C5 frame range through the two halves of cbp_ber_sim, per
+chunk of 2^20 frames: cbp_channel (Philox info bits -> encoder -> BPSK/AWGN, L and the
+codewords to an HBM buffer) -> cbp_ber_count (CBP decode -> error counting), followed by the
+NCCL all-reduce of the 8 counters (codes off the one-frame-per-warp kernel, e.g. C1: one fused
+cbp_ber_sim launch instead).  Step s of rank g simulates global frames
 [(s W + g) F, (s W + g + 1) F) of the 10^9-frame C5 range (weak scaling, F per GPU fixed).
 
   python bench.py [--gpus N --steps K --warmup W]      (N>1: re-launches itself under torchrun)
@@ -33,6 +35,7 @@ METRIC = "CBP info Gbit/s and frames/s per GPU and 8×B200 at Eb/N0, % of roofli
 UNIT = "info Gbit/s"
 I_EDGE = 38            # algorithmic fp32/int ops per edge visit of the arithmetic contract
 BASELINE_INDEX = {"C1": 0, "C2": 1, "C3a": 2, "C3b": 2, "C4": 3, "C5": 4}
+CHUNK = 1 << 20         # frames per cbp_channel -> cbp_ber_count pair (cbp_ber_sim's chunk)
 DEFAULT_STEP_FRAMES = {"C5": 4_000_000, "C3a": 4_000_000, "C3b": 4_000_000, "C1": 20_000_000, "C2": 1_000_000,
                        "C4": 20_000}
 CPU_FRAMES = {"C5": 1000, "C3a": 1000, "C3b": 600, "C1": 20000, "C2": 3000, "C4": 4}
@@ -153,7 +156,7 @@ def workload_label(cfg, ebn0s):
     tag = f"BASELINE configs[{idx}]" if idx is not None else "test code"
     what = {"C5": "C3a code, 10^9-frame scaling workload"}.get(cfg.name, "")
     return (f"{cfg.name} ({tag}{', ' + what if what else ''}): QC-LDPC N={nb * Z} K={(nb - mb) * Z} "
-            f"rate {1 - mb / nb:.3f}, Z={Z}, fused cbp_ber_sim at Eb/N0 {', '.join(f'{e:g}' for e in ebn0s)} dB")
+            f"rate {1 - mb / nb:.3f}, Z={Z}, cbp_ber_sim (cbp_channel + cbp_ber_count) at Eb/N0 {', '.join(f'{e:g}' for e in ebn0s)} dB")
 
 
 def config_block(cfg, ebn0s, frames, args, n_gpus, llr="fp32"):
@@ -162,7 +165,9 @@ def config_block(cfg, ebn0s, frames, args, n_gpus, llr="fp32"):
             "stop_rule": "belief W=M + syndrome verify", "llr": llr,
             "seed": args.seed, "parallelism": f"dp{n_gpus} (frame-range shards, NCCL allreduce of counters)",
             "frame_range": "step s of rank g: global frames [(s*W+g)*F, (s*W+g+1)*F)",
-            "l2": "flushed (256 MiB write) before every step; ber_sim reads no input from HBM"}
+            "step": "per point and per chunk of 2^20 frames: cbp_channel (L + codewords to an HBM buffer) -> "
+                    "cbp_ber_count (decode + error count), the two halves cbp_ber_sim runs",
+            "l2": "flushed (256 MiB write) before every step; a chunk's LLRs (8.2 GB) exceed L2"}
 
 
 # ------------------------------------------------------------------ reference arm (CPU oracle)
@@ -277,24 +282,53 @@ def main():
     def barrier():
         dist.barrier()
 
+    # the split step needs the code on cbp_warp_kernel (cbp_ber_count); others run the fused cbp_ber_sim
+    try:
+        l_, c_ = code.channel(ebn0s[0], 1, 0, 2)
+        code.ber_count(l_, c_, 1)
+        split = True
+    except cbp.CbpError:
+        split = False
+    chunk = min(frames, CHUNK) if split else frames
+    llr_buf = torch.empty((chunk, (code.N + 3) // 4 * 4), dtype=torch.float32, device=dev) if split else None
+    cw_buf = torch.empty((chunk, code.words), dtype=torch.int32, device=dev) if split else None
+    n_chunks = (frames + chunk - 1) // chunk
+
     def measure(llr_mode):
-        """W warm-up + K timed steps of the fused ber_sim on this rank's slices; returns
-        (seconds max over ranks, summed counters [points, 8], per-launch ms, local edge visits per launch)."""
+        """W warm-up + K timed steps on this rank's slices; a step is, per Eb/N0 point and per chunk of
+        2^20 frames, cbp_channel -> HBM -> cbp_ber_count (what cbp_ber_sim runs), each launch bracketed by
+        CUDA events on the launch stream.  Returns (seconds max over ranks, summed counters [points, 8],
+        decode ms per point and step, channel ms per point and step, local edge visits per point)."""
         counts = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in ebn0s]
         local_ev = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in ebn0s]
+
+        def ev():
+            return torch.cuda.Event(enable_timing=True)
 
         def step(s, launch_ms=None):
             for p, eb in enumerate(ebn0s):
                 c = counts[p]
                 c.zero_()
+                f_begin = (s * world + rank) * frames
+                for f0 in range(0, frames, chunk):
+                    n = min(chunk, frames - f0)
+                    marks = [ev() for _ in range(3)] if launch_ms is not None else None
+                    if marks:
+                        marks[0].record(stream)
+                    if split:
+                        code.channel(eb, args.seed, f_begin + f0, n, llr_mode, stream=stream,
+                                     out=(llr_buf[:n], cw_buf[:n]))
+                    if marks:
+                        marks[1].record(stream)
+                    if split:
+                        code.ber_count(llr_buf[:n], cw_buf[:n], cfg.max_iter, counts=c, stream=stream)
+                    else:
+                        code.ber_sim(eb, args.seed, f_begin + f0, n, cfg.max_iter, llr_mode=llr_mode, counts=c,
+                                     stream=stream)
+                    if marks:
+                        marks[2].record(stream)
+                        launch_ms.append((p, marks))
                 if launch_ms is not None:
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record(stream)
-                code.ber_sim(eb, args.seed, (s * world + rank) * frames, frames, cfg.max_iter, llr_mode=llr_mode,
-                             counts=c, stream=stream)
-                if launch_ms is not None:
-                    e1.record(stream)
-                    launch_ms.append((p, e0, e1))
                     local_ev[p].copy_(c)
                 reduce(c)
 
@@ -317,41 +351,53 @@ def main():
         t_ms = sum(a.elapsed_time(b) for a, b in step_ev)
         t_max = torch.tensor([t_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        per_launch = np.array([a.elapsed_time(b) for _, a, b in launches]).reshape(args.steps, len(ebn0s))
+        dec = np.array([m[1].elapsed_time(m[2]) for _, m in launches]).reshape(args.steps, len(ebn0s), n_chunks)
+        chn = np.array([m[0].elapsed_time(m[1]) for _, m in launches]).reshape(args.steps, len(ebn0s), n_chunks)
         tot = torch.stack(counts).cpu().numpy()                # last step, all ranks summed
-        ev_loc = torch.stack(local_ev).cpu().numpy()[:, 5]     # last step, this rank's edge visits per launch
-        return t_max.item() / 1e3, tot, per_launch, ev_loc, clk.summary()
+        ev_loc = torch.stack(local_ev).cpu().numpy()[:, 5]     # last step, this rank's edge visits per point
+        return t_max.item() / 1e3, tot, dec.sum(axis=2), chn.sum(axis=2), ev_loc, clk.summary()
 
-    T, tot, per_launch, ev_loc, clocks = measure(0)
+    T, tot, per_launch, per_chan, ev_loc, clocks = measure(0)
     frames_all = frames * len(ebn0s) * args.steps * world
     fps = frames_all / T
     gbps = fps * code.K / 1e9
 
-    # roofline of the dominant kernel (the fused cbp_kernel launch): I_edge x exact edge visits of a
-    # launch / its mean CUDA-event duration, against the derived issue peak
+    # roofline of the dominant kernel (the cbp_ber_count decode launches, cbp_warp_kernel in MODE_BER_LLR):
+    # I_edge x exact edge visits / the launches' CUDA-event durations, against the derived issue peak
+    # (DESIGN.md §7); the channel launches' share of the step is reported beside it
     li = code.launch_info()
     f_sm = peaks.get("sm_max_mhz", 1965.0)
     peak = li["num_sms"] * 128 * f_sm * 1e6
-    dur = per_launch.mean(axis=0) / 1e3
+    dur = per_launch.mean(axis=0) / 1e3                        # decode seconds per point and step
     achieved = float((ev_loc.astype(np.float64) * I_EDGE).sum() / dur.sum())
+    step_s = T / args.steps
     tr = kernel_traffic(cfg.name)
     roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Top/s",
                 "frac": achieved / peak,
-                "traffic": tr["bytes_per_frame"] * frames if tr else None,
-                "edge_visits_per_launch": int(ev_loc.mean()), "launch_ms": float(dur.mean() * 1e3),
+                "traffic": tr["bytes_per_frame"] * chunk if tr else None,
+                "kernel": ("cbp_warp_kernel (cbp_ber_count: decode + error count of a 2^20-frame chunk)" if split else
+                           "fused cbp_ber_sim launch"),
+                "launches_per_step": n_chunks * len(ebn0s),
+                "edge_visits_per_launch": int(ev_loc.sum() / (n_chunks * len(ebn0s))),
+                "launch_ms": float(dur.sum() * 1e3 / (n_chunks * len(ebn0s))),
                 "edge_visits_per_s": float(ev_loc.sum() / dur.sum()),
+                "share_of_step": float(dur.sum() * world / step_s) if world == 1 else None,
+                "channel_ms_per_step": float(per_chan.mean(axis=0).sum()),
+                "step_frac": float((ev_loc.astype(np.float64) * I_EDGE).sum() / step_s / peak) if world == 1 else None,
                 "note": f"I_edge={I_EDGE} contract ops/edge visit x exact edge visits / mean launch time (CUDA events "
                         f"on the launch stream); peak = {li['num_sms']} SM x 128 lanes x {f_sm:.0f} MHz (sm_max, "
-                        f"MEASURED_PEAKS.json; derived issue peak); traffic = DRAM bytes per launch scaled from the "
-                        f"per-frame bytes of {tr['file'] if tr else 'n/a'} (ncu --set full of this workload); "
-                        f"algorithmic HBM bytes of ber_sim: 0 in, 64 out"}
+                        f"MEASURED_PEAKS.json; derived issue peak); step_frac = the same ops over the whole step "
+                        f"(channel launches included); traffic = DRAM bytes per launch scaled from the per-frame "
+                        f"bytes of {tr['file'] if tr else 'n/a'} (ncu --set full of this workload); algorithmic HBM "
+                        f"bytes of a decode launch: {code.N * 4 + code.words * 4} in per frame (LLRs + codeword), "
+                        f"64 out"}
     if tr:
         roofline["ncu"] = {k: tr.get(k) for k in ("issue_active_pct", "lane_slots_per_edge_visit", "smem_pipe_pct",
                                                   "tex_pipe_pct", "alu_pipe_pct", "fma_pipe_pct", "file")}
 
     int8 = None
     if not args.no_int8:
-        T8, tot8, pl8, ev8, clk8 = measure(1)
+        T8, tot8, pl8, _, ev8, clk8 = measure(1)
         f8 = frames * len(ebn0s) * args.steps * world / T8
         d8 = pl8.mean(axis=0) / 1e3
         int8 = {"value": f8 * code.K / 1e9, "unit": UNIT, "frames_per_s": f8, "ms_per_step": 1e3 * T8 / args.steps,
@@ -535,7 +581,7 @@ def main():
             "config": config_block(cfg, ebn0s, frames, args, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "int8_stream": int8, "roofline_decode": decode_rl,
-            "gpu_launches": args.steps * len(ebn0s),
+            "gpu_launches": args.steps * len(ebn0s) * n_chunks * (2 if split else 1),
             "collectives": {"backend": dist.get_backend(), "world_size": world,
                             "counter_allreduce_calls": n_allreduce[0],
                             "per_timed_step": len(ebn0s)},

@@ -201,12 +201,29 @@ typedef struct {
     int64_t undetected_fires; /* failed syndrome verifications          */
 } cbp_counts;
 
-/* Fused channel + CBP decode + error counting for one Eb/N0 point (no LLR
- * traffic through HBM).  Equivalent to cbp_channel -> cbp_decode -> compare
- * (llr_mode as for cbp_channel; bit errors count over variables 0..K-1, the
- * systematic part for encoded codes). */
+/* Channel + CBP decode + error counting for one Eb/N0 point: counts the
+ * frames of cbp_channel -> cbp_decode -> compare (llr_mode as for cbp_channel;
+ * bit errors count over variables 0..K-1, the systematic part for encoded
+ * codes).  Codes on the one-frame-per-warp kernel run it as
+ * cbp_channel + cbp_ber_count per chunk of 2^20 frames through a stream-ordered
+ * HBM workspace (N floats + ceil(N/32) words per frame of the chunk); the
+ * others in one fused kernel.  The counters are the same either way. */
 cbp_status cbp_ber_sim(const cbp_code* code, double ebn0_db, uint64_t seed, int64_t frame_begin, int64_t frames,
                        const cbp_opts* opts, int32_t llr_mode, cbp_counts* d_counts, void* stream);
+
+/* Decode + error counting on given frames (the decode half of cbp_ber_sim, for
+ * LLRs from any source).  PAPER.md §IV (Steps 1-3, Algorithm 1) per frame as in
+ * cbp_decode; the decision bits are compared with the transmitted codeword and
+ * accumulated (+=) into d_counts as cbp_ber_sim does.
+ *   d_llr    : device float[frames][ld], ld >= N, ld % 4 == 0, 16-byte aligned
+ *   d_cw     : device uint32[frames][ld_words] transmitted codewords (bit v%32 of
+ *              word v/32), ld_words >= ceil(N/32)
+ *   d_counts : device cbp_counts, accumulated (caller zeroes it)
+ * Needs a code on the one-frame-per-warp kernel (17 <= Z <= 384) and the
+ * log-tanh CBP or layered-BP algorithm, else CBP_E_UNSUPPORTED.  Buffers are the
+ * caller's; nothing is retained after the call. */
+cbp_status cbp_ber_count(const cbp_code* code, const float* d_llr, int64_t ld, const uint32_t* d_cw, int64_t ld_words,
+                         int64_t frames, const cbp_opts* opts, cbp_counts* d_counts, void* stream);
 
 /* ----------------------------------------------------------- introspection */
 

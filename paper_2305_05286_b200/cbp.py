@@ -72,6 +72,7 @@ SIGNATURES = {
     "cbp_decode_host_i8": ([_p, _p, _i64, _f32, _i64, _p, _p, _i64, _p, _p, _i64, _i32], _i32),
     "cbp_channel": ([_p, _f64, _u64, _i64, _i64, _i32, _p, _i64, _p, _i64, _p], _i32),
     "cbp_ber_sim": ([_p, _f64, _u64, _i64, _i64, _p, _i32, _p, _p], _i32),
+    "cbp_ber_count": ([_p, _p, _i64, _p, _i64, _i64, _p, _p, _p], _i32),
     "cbp_get_launch_info": ([_p, _p], _i32),
     "cbp_eval_contract": ([_i32, _p, _p, _i64, _i32, _p], _i32),
     "cbp_phi_table": ([_i32, _p, _p], _i32),
@@ -261,14 +262,24 @@ class Code:
 
     # -------------------------------------------------------------- channel / ber
     def channel(self, ebn0_db: float, seed: int, frame_begin: int, frames: int, llr_mode: int = 0,
-                ld: int | None = None, want_llr: bool = True, want_cw: bool = True, stream=None):
-        """cbp_channel: returns (llr float32 [frames, ld] or None, codewords int32 [frames, words] or None)."""
+                ld: int | None = None, want_llr: bool = True, want_cw: bool = True, stream=None, out=None):
+        """cbp_channel: returns (llr float32 [frames, ld] or None, codewords int32 [frames, words] or None);
+        `out` = (llr, cw): caller's buffers (either may be None), written instead of new ones."""
         d = self.device
-        ld = ld or (self.N + 3) // 4 * 4
-        llr = torch.empty((frames, ld), dtype=torch.float32, device=d) if want_llr else None
-        cw = torch.empty((frames, self.words), dtype=torch.int32, device=d) if want_cw else None
+        if out is not None:
+            llr, cw = out
+            for t, nm, cols in ((llr, "llr", self.N), (cw, "cw", self.words)):
+                if t is not None and (t.dim() != 2 or t.shape[0] != frames or t.shape[1] < cols):
+                    raise CbpError(f"channel: out {nm} must be [frames={frames}, >= {cols}], got {tuple(t.shape)}")
+            ld = llr.shape[1] if llr is not None else (self.N + 3) // 4 * 4
+            wds = cw.shape[1] if cw is not None else self.words
+        else:
+            ld = ld or (self.N + 3) // 4 * 4
+            wds = self.words
+            llr = torch.empty((frames, ld), dtype=torch.float32, device=d) if want_llr else None
+            cw = torch.empty((frames, self.words), dtype=torch.int32, device=d) if want_cw else None
         rc = lib().cbp_channel(self._h, float(ebn0_db), seed, frame_begin, frames, llr_mode,
-                               _dptr(llr, torch.float32, d, "llr"), ld, _dptr(cw, torch.int32, d, "cw"), self.words,
+                               _dptr(llr, torch.float32, d, "llr"), ld, _dptr(cw, torch.int32, d, "cw"), wds,
                                _stream(stream))
         _check(rc, "cbp_channel")
         return llr, cw
@@ -285,6 +296,28 @@ class Code:
         rc = lib().cbp_ber_sim(self._h, float(ebn0_db), seed, frame_begin, frames, ctypes.byref(o), llr_mode,
                                _dptr(counts, torch.int64, self.device, "counts"), _stream(stream))
         _check(rc, "cbp_ber_sim")
+        return counts
+
+    def ber_count(self, llr: torch.Tensor, cw: torch.Tensor, max_iter: int, stop_rule: int = CBP_STOP_BELIEF_M,
+                  counts: torch.Tensor | None = None, stream=None, algorithm: int = CBP_ALG_LOG_TANH,
+                  alpha: float = ALPHA_DEFAULT) -> torch.Tensor:
+        """cbp_ber_count: decode fp32 LLRs [frames, ld] and count errors against the codewords [frames, words]
+        (int32 words, as `channel` returns them); accumulates into `counts` (zeroed if not given)."""
+        if counts is None:
+            counts = torch.zeros(8, dtype=torch.int64, device=self.device)
+        if counts.numel() != 8:
+            raise CbpError("ber_count: counts must hold the 8 int64 counters of cbp_counts")
+        if llr.dim() != 2 or cw.dim() != 2 or cw.shape[0] < llr.shape[0]:
+            raise CbpError(f"ber_count: llr [frames, ld] and cw [>= frames, words] expected, got {tuple(llr.shape)}, "
+                           f"{tuple(cw.shape)}")
+        if cw.shape[1] < self.words:
+            raise CbpError(f"ber_count: cw needs >= {self.words} words per frame")
+        frames, ld = llr.shape
+        o = _opts(max_iter, stop_rule, algorithm, alpha)
+        rc = lib().cbp_ber_count(self._h, _dptr(llr, torch.float32, self.device, "llr"), ld,
+                                 _dptr(cw, torch.int32, self.device, "cw"), cw.shape[1], frames, ctypes.byref(o),
+                                 _dptr(counts, torch.int64, self.device, "counts"), _stream(stream))
+        _check(rc, "cbp_ber_count")
         return counts
 
 

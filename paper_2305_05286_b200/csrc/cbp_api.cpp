@@ -623,11 +623,11 @@ cbp_status cbp_get_launch_info(const cbp_code* c, cbp_launch_info* o)
 
 namespace {
 
-// the geometry a launch runs with: cbp_channel on cbp_kernel; a log-tanh decode with Omega output
-// on the warp kernel's geometry that has room for the check records
+// the geometry a launch runs with: cbp_channel on the warp kernel of the code (else on cbp_kernel); a
+// log-tanh decode with Omega output on the warp kernel's geometry that has room for the check records
 const cbp::Geometry& geo_for(const cbp_code* c, int alg, bool chan, bool omega, int* ctas)
 {
-    if (chan) {
+    if (chan && !c->geo[alg].wk) {
         *ctas = c->ctas_chan;
         return c->geo_chan;
     }
@@ -722,6 +722,42 @@ cbp_status run(const cbp_code* c, cbp::KernelArgs& a, int64_t frames, void* stre
     if (gs) cudaFreeAsync(gs, st);
     if (le != 0) return cuda_fail(static_cast<cudaError_t>(le), who);
     return CBP_OK;
+}
+
+// decode of fp32 LLRs + error counting against the transmitted codewords (MODE_BER_LLR; arguments checked)
+cbp_status ber_count_launch(const cbp_code* c, const float* llr, int64_t ld, const uint32_t* cw, int64_t ld_words,
+                            int64_t frames, const cbp_opts* opts, cbp_counts* counts, void* stream, const char* who)
+{
+    cbp::KernelArgs a = base_args(c, opts->algorithm);
+    a.mode = cbp::MODE_BER_LLR;
+    a.max_iter = opts->max_iter;
+    a.stop_rule = opts->stop_rule;
+    a.algorithm = opts->algorithm;
+    a.alpha = opts->alpha;
+    a.frames = frames;
+    a.llr = llr;
+    a.ld = ld;
+    a.cw_in = cw;
+    a.ld_words = ld_words;
+    a.counts = reinterpret_cast<unsigned long long*>(counts);
+    return run(c, a, frames, stream, who);
+}
+
+// cbp_ber_sim as channel + decode launches through an HBM chunk (codes on cbp_warp_kernel with one
+// frame per warp); CBP_BER_SPLIT=0|1 overrides (A/B runs), CBP_BER_CHUNK sets the frames per chunk
+bool ber_split(const cbp_code* c, int alg)
+{
+    const cbp::Geometry& G = c->geo[alg];
+    if (!G.wk) return false;
+    static const int env = [] { const char* e = std::getenv("CBP_BER_SPLIT"); return e && *e ? std::atoi(e) : -1; }();
+    if (env >= 0) return env != 0;
+    return !G.multi;
+}
+
+int64_t ber_chunk_frames()
+{
+    static const int64_t env = [] { const char* e = std::getenv("CBP_BER_CHUNK"); return e ? std::atoll(e) : 0LL; }();
+    return env > 0 ? env : (int64_t{1} << 20);
 }
 
 void channel_params(const cbp_code* c, double ebn0_db, float* sigma, float* scale)
@@ -904,6 +940,23 @@ cbp_status cbp_channel(const cbp_code* c, double ebn0_db, uint64_t seed, int64_t
     return run(c, a, frames, stream, "cbp_channel");
 }
 
+cbp_status cbp_ber_count(const cbp_code* c, const float* d_llr, int64_t ld, const uint32_t* d_cw, int64_t ld_words,
+                         int64_t frames, const cbp_opts* opts, cbp_counts* d_counts, void* stream)
+{
+    if (!c) return fail(CBP_E_INVALID, "cbp_ber_count: null code");
+    cbp_status s = check_opts(c, opts);
+    if (s != CBP_OK) return s;
+    if (!c->geo[opts->algorithm].wk)
+        return fail(CBP_E_UNSUPPORTED, "cbp_ber_count: needs a code on cbp_warp_kernel (17 <= Z <= 384; log-tanh CBP or layered BP)");
+    if (frames < 0) return fail(CBP_E_INVALID, "cbp_ber_count: frames < 0");
+    if (frames == 0) return CBP_OK;
+    if (!d_llr || !d_cw || !d_counts) return fail(CBP_E_INVALID, "cbp_ber_count: null buffer");
+    if (ld < c->N || ld % 4 != 0) return fail(CBP_E_INVALID, "cbp_ber_count: need ld >= N and ld % 4 == 0");
+    if (reinterpret_cast<uintptr_t>(d_llr) % 16 != 0) return fail(CBP_E_INVALID, "cbp_ber_count: llr not 16-byte aligned");
+    if (ld_words < (c->N + 31) / 32) return fail(CBP_E_INVALID, "cbp_ber_count: ld_words < ceil(N/32)");
+    return ber_count_launch(c, d_llr, ld, d_cw, ld_words, frames, opts, d_counts, stream, "cbp_ber_count");
+}
+
 cbp_status cbp_ber_sim(const cbp_code* c, double ebn0_db, uint64_t seed, int64_t frame_begin, int64_t frames,
                        const cbp_opts* opts, int32_t llr_mode, cbp_counts* d_counts, void* stream)
 {
@@ -929,7 +982,47 @@ cbp_status cbp_ber_sim(const cbp_code* c, double ebn0_db, uint64_t seed, int64_t
     a.llr_mode = llr_mode;
     channel_params(c, ebn0_db, &a.sigma, &a.scale);
     a.counts = reinterpret_cast<unsigned long long*>(d_counts);
-    return run(c, a, frames, stream, "cbp_ber_sim");
+    if (!ber_split(c, opts->algorithm)) return run(c, a, frames, stream, "cbp_ber_sim");
+    // split: per chunk of frames, a channel-only launch writes L and the codewords to a workspace in HBM
+    // and a MODE_BER_LLR launch decodes and counts them.  Same kernel, same frames and arithmetic as the
+    // fused launch (bit-identical counters); the per-frame channel code then no longer shares the SM's
+    // instruction cache with the hot row bodies.
+    DeviceGuard g(c->device);
+    if (!g.ok) return fail(CBP_E_CUDA, "cbp_ber_sim: cudaSetDevice failed");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t chunk = std::min<int64_t>(frames, ber_chunk_frames());
+    const int64_t ld = (c->N + 3) / 4 * 4, ldw = (c->N + 31) / 32;   // 16-byte rows: 128-bit LLR loads
+    float* llr = nullptr;
+    uint32_t* cw = nullptr;
+    cudaMemPool_t pool = work_pool(c->device);
+    auto alloc = [&](void** p, size_t bytes) {
+        return pool ? cudaMallocFromPoolAsync(p, bytes, pool, st) : cudaMallocAsync(p, bytes, st);
+    };
+    cudaError_t e = alloc(reinterpret_cast<void**>(&llr), sizeof(float) * static_cast<size_t>(chunk * ld));
+    if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&cw), sizeof(uint32_t) * static_cast<size_t>(chunk * ldw));
+    if (e != cudaSuccess) {
+        if (llr) cudaFreeAsync(llr, st);
+        return fail(CBP_E_NOMEM, std::string("cbp_ber_sim: ") + cudaGetErrorString(e));
+    }
+    cbp_status s2 = CBP_OK;
+    for (int64_t f0 = 0; f0 < frames && s2 == CBP_OK; f0 += chunk) {
+        const int64_t n = std::min(chunk, frames - f0);
+        cbp::KernelArgs ch = a;
+        ch.mode = cbp::MODE_CHANNEL;
+        ch.frames = n;
+        ch.frame_begin = frame_begin + f0;
+        ch.llr_out = llr;
+        ch.ld = ld;
+        ch.cw_out = cw;
+        ch.ld_words = ldw;
+        ch.counts = nullptr;
+        s2 = run(c, ch, n, stream, "cbp_ber_sim (channel)");
+        if (s2 != CBP_OK) break;
+        s2 = ber_count_launch(c, llr, ld, cw, ldw, n, opts, d_counts, stream, "cbp_ber_sim");
+    }
+    cudaFreeAsync(llr, st);
+    cudaFreeAsync(cw, st);
+    return s2;
 }
 
 cbp_status cbp_eval_contract(int32_t fn, const float* d_x, float* d_y, int64_t n, int32_t device, void* stream)

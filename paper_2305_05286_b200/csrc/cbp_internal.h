@@ -16,7 +16,9 @@ struct DevCode {
     unsigned long long phi_tex;   // cudaTextureObject_t over phi_tab (float4 elements)
 };
 
-enum Mode : int32_t { MODE_DECODE_F32 = 0, MODE_DECODE_I8 = 1, MODE_BER_SIM = 2, MODE_CHANNEL = 3 };
+// MODE_BER_LLR: the decode half of a split cbp_ber_sim -- fp32 LLRs and the transmitted codewords from
+// HBM (written by a MODE_CHANNEL launch of the same kernel), error counting as in MODE_BER_SIM
+enum Mode : int32_t { MODE_DECODE_F32 = 0, MODE_DECODE_I8 = 1, MODE_BER_SIM = 2, MODE_CHANNEL = 3, MODE_BER_LLR = 4 };
 
 // Limits of the schedule tables carried in the kernel parameters (constant bank):
 // read through the constant cache, they take no shared-memory bandwidth.
@@ -63,6 +65,7 @@ struct KernelArgs {
     float* gstate;         // per-CTA global state (state_in_smem == 0)
     float* rstate;         // per-group R sections of the split layout (r_global), r_words each
     int32_t r_words;
+    const uint32_t* cw_in; // MODE_BER_LLR: transmitted codewords [frames][ld_words]
 };
 
 // phi lookups through the texture pipe (C2B default on, B2V default off)

@@ -603,7 +603,10 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
 
     const bool belief = a.stop_rule <= 1;
     const int W = (a.stop_rule == 1) ? N : C.M;               // R4
-    const bool ber = a.mode == MODE_BER_SIM;
+    // gen: channel generated in the warp (fused ber_sim, channel-only); ber: error counting against the
+    // transmitted codeword (fused ber_sim, and the decode half of a split one: LLRs and codewords from HBM)
+    const bool gen = a.mode == MODE_BER_SIM || a.mode == MODE_CHANNEL;
+    const bool ber = a.mode == MODE_BER_SIM || a.mode == MODE_BER_LLR;
     const bool keep_S = a.omega != nullptr && !LBP;           // S only feeds the Omega output (none for LBP)
     const uint32_t key0 = static_cast<uint32_t>(a.seed), key1 = static_cast<uint32_t>(a.seed >> 32);
     unsigned long long bit_err = 0;                           // this lane's share (ber_sim)
@@ -636,8 +639,12 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
         if (f >= a.frames) break;
         // ---- Step 1 (a2-a5): channel LLRs (decode: from HBM, 16 bytes per lane and load;
         // ber_sim: Philox info bits, encoder, BPSK/AWGN in the warp), {Lambda, H} = L + 0, R = 0
-        if (!ber) {
+        if (!gen) {
             const size_t base = static_cast<size_t>(f) * a.ld;
+            if (a.mode == MODE_BER_LLR) {                     // the frame's transmitted codeword (counting)
+                const uint32_t* src = a.cw_in + static_cast<size_t>(f) * a.ld_words;
+                for (int w = tl; w < C.nwords; w += TL) cw[w] = __ldcs(src + w);
+            }
             if (a.mode == MODE_DECODE_I8) {
                 const int4* src = reinterpret_cast<const int4*>(a.q + base);
                 for (int v16 = tl; 16 * v16 < N; v16 += TL) {
@@ -784,11 +791,24 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                         Lv = __fmul_rn(qq, 0.25f);
                     }
                     const float x0 = __fadd_rn(Lv, 0.0f);
-                    lam[v] = x0;
+                    lam[v] = (a.mode == MODE_CHANNEL) ? Lv : x0;   // channel only: L itself (decoders add the + 0)
                     hb[v] = static_cast<int8_t>(__float_as_uint(x0) >> 24);
                   }
                 }
             }
+        }
+        if (a.mode == MODE_CHANNEL) {                         // channel only: L and the codeword to HBM
+            tsync();
+            if (a.llr_out) {
+                float* out = a.llr_out + static_cast<size_t>(f) * a.ld;
+                for (int v = tl; v < N; v += TL) __stcs(out + v, lam[v]);
+            }
+            if (a.cw_out) {
+                uint32_t* out = a.cw_out + static_cast<size_t>(f) * a.ld_words;
+                for (int w = tl; w < a.ld_words; w += TL) __stcs(out + w, w < C.nwords ? cw[w] : 0u);
+            }
+            tsync();
+            continue;
         }
         // R = 0 (equ_s4e17) needs no stores: sweep 1 reads no R word (WCtx::r0), and every word is
         // written in sweep 1 before sweep 2 reads it (a frame that stops in sweep 1 reads none)
@@ -810,7 +830,7 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 WRow<K> ro;
                 ro.first_bad = Z;
                 ro.last_bad = -1;
-                wrow_dispatch<K, ALG, TM, RG>(dc, C.max_dc, ber, ent, ptab, e0, lane, static_cast<TexH>(C.phi_tex), cx, ro);
+                wrow_dispatch<K, ALG, TM, RG>(dc, C.max_dc, a.mode == MODE_BER_SIM, ent, ptab, e0, lane, static_cast<TexH>(C.phi_tex), cx, ro);
                 int first_bad = ro.first_bad, last_bad = ro.last_bad;
                 if constexpr (TEAM) {
                     // the team's first / last unclean check of the row (two buffers: a fast warp may write

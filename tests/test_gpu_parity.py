@@ -740,3 +740,86 @@ def test_state_layouts_equal_oracle(monkeypatch, env, name, eb, frames):
     assert list(got) == list(o.ber_sim(eb, 12, 100, frames, mi, llr_mode=lm))
     got = g.ber_sim(eb, 12, 100, frames // 2, mi, 2, llr_mode=lm, algorithm=3).cpu().numpy()
     assert list(got) == list(o.ber_sim(eb, 12, 100, frames // 2, mi, 2, llr_mode=lm, arith=oracle.FBP))
+
+
+# ---------------------------------------------------------------- split ber_sim: cbp_channel + cbp_ber_count
+@pytest.fixture(scope="module")
+def auto_codes():
+    """Codes in the default (automatic) geometry -- the one bench.py and cbp_ber_sim run."""
+    _need_gpu()
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            base, Z = inputs.config_base(name)
+            cache[name] = (cbp.Code(base, Z), oracle.OracleCode(base, Z))
+        return cache[name]
+    return get
+
+
+@pytest.mark.parametrize("name,ebn0,frames,llr_mode,alg", [
+    ("C2", 1.5, 1500, 0, 0), ("C2", 2.5, 1500, 1, 0), ("C3a", 2.5, 300, 0, 0), ("C3b", 4.0, 200, 1, 0),
+    ("C2", 2.0, 600, 0, 2)])
+def test_ber_count_parity(auto_codes, name, ebn0, frames, llr_mode, alg):
+    """cbp_ber_count on cbp_channel's frames (the two halves of the split cbp_ber_sim) equals the
+    oracle's ber_sim counters; so does cbp_ber_sim itself (split by default on these codes)."""
+    g, o = auto_codes(name)
+    mi = inputs.CONFIGS[name].max_iter
+    rule = oracle.STOP_SYNDROME if alg == 2 else oracle.STOP_BELIEF_M
+    kw = dict(arith=oracle.LBP) if alg == 2 else {}
+    want = o.ber_sim(ebn0, 77, 12345, frames, mi, rule, llr_mode, **kw)
+    llr, cw = g.channel(ebn0, 77, 12345, frames, llr_mode=llr_mode)
+    got = g.ber_count(llr, cw, mi, rule, algorithm=alg).cpu().numpy()
+    assert list(got) == list(want), dict(zip(oracle.COUNT_NAMES, zip(got, want)))
+    got2 = g.ber_sim(ebn0, 77, 12345, frames, mi, rule, llr_mode, algorithm=alg).cpu().numpy()
+    assert list(got2) == list(want)
+
+
+def test_ber_sim_fused_equals_split():
+    """CBP_BER_SPLIT=0 (one fused kernel) and the default split path give the same counters, with
+    chunks small enough (CBP_BER_CHUNK) that the split runs several channel + decode pairs and a
+    ragged last chunk; both equal the oracle's counters."""
+    _need_gpu()
+    import os
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, '.'); import inputs, paper_2305_05286_b200 as cbp; "
+            "b, Z = inputs.config_base('C3a'); g = cbp.Code(b, Z); "
+            "print(g.ber_sim(2.0, 5, 999, 2500, 30, llr_mode=1).cpu().tolist())")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({"CBP_BER_SPLIT": "0"}, {"CBP_BER_SPLIT": "1", "CBP_BER_CHUNK": "1000"}):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **env), capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1], outs
+    base, Z = inputs.config_base("C3a")
+    want = oracle.OracleCode(base, Z).ber_sim(2.0, 5, 999, 2500, 30, llr_mode=1)
+    assert outs[0] == str([int(x) for x in want])
+
+
+def test_ber_count_error_paths(auto_codes):
+    import ctypes
+    L = cbp.lib()
+    g, _ = auto_codes("C2")
+    dev = torch.device("cuda", 0)
+    llr, cw = g.channel(2.0, 1, 0, 4)
+    cnt = torch.zeros(8, dtype=torch.int64, device=dev)
+    ok = cbp.cbp._Opts(30, 0, 0, 0.75)
+
+    def bc(p=None, ld=648, c=cw.data_ptr(), lw=21, frames=4, opts=ok, n=cnt.data_ptr()):
+        return L.cbp_ber_count(g.handle, llr.data_ptr() if p is None else p, ld, c, lw, frames, ctypes.byref(opts), n,
+                               None)
+    assert bc() == 0 and int(cnt[0]) == 4
+    cnt.zero_()
+    assert bc(ld=640) == 1 and bc(ld=650) == 1                 # ld < N, ld % 4
+    assert bc(p=llr.data_ptr() + 4) == 1                      # misaligned
+    assert bc(c=None) == 1 and bc(n=None) == 1 and bc(lw=20) == 1 and bc(frames=-1) == 1
+    assert bc(opts=cbp.cbp._Opts(0, 0, 0, 0.75)) == 1
+    assert bc(frames=0, c=None) == 0                          # empty batch: no-op
+    assert int(cnt.sum()) == 0
+    g1, _ = auto_codes("C1")                                   # Z = 8: not on the one-frame-per-warp kernel
+    l1, c1 = g1.channel(2.0, 1, 0, 4)
+    with pytest.raises(cbp.CbpError, match="status 2"):
+        g1.ber_count(l1, c1, 20)
