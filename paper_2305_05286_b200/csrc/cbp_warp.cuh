@@ -77,18 +77,39 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 #ifndef CBP_R_CG
 #define CBP_R_CG 1          // R words in global memory: loads / stores cached in L2 only (keep L1 for the TEX phi rows)
 #endif
-// R word access: RG = R in the global workspace (L2-only when CBP_R_CG), else in shared memory
+// R word access: RG = R in the global workspace (L2-only when CBP_R_CG), else in shared memory.
+// CBP_R_CG == 2: L2-only with an L2 evict_last policy descriptor (createpolicy folds into a constant
+// descriptor in uniform registers: no extra instruction or register in the row body), A/B switch.
+// The asm statements are volatile (ordered among themselves: R is touched only through them) without a
+// memory clobber, so shared-memory accesses still move across them.
 template <bool RG>
 __device__ __forceinline__ float rld(const float* p)
 {
+#if CBP_R_CG == 2
+    if constexpr (RG) {
+        float v; unsigned long long pol;
+        asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("ld.global.cg.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+        return v;
+    } else return *p;
+#else
     if constexpr (RG && CBP_R_CG) return __ldcg(p);
     else return *p;
+#endif
 }
 template <bool RG>
 __device__ __forceinline__ void rst(float* p, float v)
 {
+#if CBP_R_CG == 2
+    if constexpr (RG) {
+        unsigned long long pol;
+        asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("st.global.cg.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(p), "f"(v), "l"(pol));
+    } else *p = v;
+#else
     if constexpr (RG && CBP_R_CG) __stcg(p, v);
     else *p = v;
+#endif
 }
 
 // ---------------------------------------------------------------- two edges on the packed FP32x2 pipe
