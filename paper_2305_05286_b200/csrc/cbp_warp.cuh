@@ -74,12 +74,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 #ifndef CBP_WARP_LEAN
 #define CBP_WARP_LEAN 0     // 1: entries and R re-read per slot (fewer registers, A/B runs)
 #endif
+#ifndef CBP_RPRE
+#define CBP_RPRE 0          // 1: a row's last slot requests the next row's slot-0 R words (A/B switch)
+#endif
+#ifndef CBP_LLR_BATCH
+#define CBP_LLR_BATCH 8     // 128-bit LLR loads in flight per lane at a frame's start (decode modes)
+#endif
 #ifndef CBP_R_CG
-#define CBP_R_CG 1          // R words in global memory: loads / stores cached in L2 only (keep L1 for the TEX phi rows)
+#define CBP_R_CG 2          // R words in global memory: 1 = loads / stores cached in L2 only (keep L1 for the TEX phi
+                            // rows), 2 = the same with an L2 evict_last policy (C5 -1.1 %, C3a at 1.5 dB -1.6 %, DRAM writes -43 %)
 #endif
 // R word access: RG = R in the global workspace (L2-only when CBP_R_CG), else in shared memory.
 // CBP_R_CG == 2: L2-only with an L2 evict_last policy descriptor (createpolicy folds into a constant
-// descriptor in uniform registers: no extra instruction or register in the row body), A/B switch.
+// descriptor in uniform registers: no extra instruction or register in the row body).
 // The asm statements are volatile (ordered among themselves: R is touched only through them) without a
 // memory clobber, so shared-memory accesses still move across them.
 template <bool RG>
@@ -258,6 +265,8 @@ struct WCtx {
     float* pb;                   // park buffer: Phi of edge e at pb[e 32 + l]
     float* rrow;                 // this lane's R word of (row entry 0, slot 0); (edge e, slot k) at rrow[(e K + k) 32]
     float* Srow;                 // S records of this row (keepS)
+    const float* nrow = nullptr; // CBP_RPRE: this lane's slot-0 R word of the next row's entry 0 (nullptr: no request)
+    int npre = 0;                // CBP_RPRE: words of rpre[] the previous row requested for this row
 };
 
 // Slot k's check update done: its record, the rollback values and its stop flags (equ_s4e2, equ_s4e24).
@@ -289,7 +298,8 @@ __device__ __forceinline__ void wslot_done(const WCtx& c, int k, int rr, bool v,
 // words and stores nothing.
 template <int DC, int K, int ALG, int TM, bool RG>
 __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0,
-                                     const Lane& L, TexH tex, const WCtx& c, WRow<K>& o, bool lastoff = false)
+                                     const Lane& L, TexH tex, const WCtx& c, WRow<K>& o, float (&rpre)[CBP_DC_REG],
+                                     bool lastoff = false)
 {
     constexpr bool LBP = ALG == 2;
     constexpr bool TEXC = TM != 2, TEXB = TM == 1;             // phi rows: C2B / B2V through the texture pipe
@@ -303,7 +313,10 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
     // L2 latency then overlaps it); slot 0's are loaded here
     float rnext[DC];
 #pragma unroll
-    for (int e = 0; e < DC; ++e) rnext[e] = (c.r0 || (e == DC - 1 && lastoff)) ? 0.0f : rld<RG>(c.rrow + e * K * 32);
+    for (int e = 0; e < DC; ++e)
+        rnext[e] = (c.r0 || (e == DC - 1 && lastoff)) ? 0.0f
+                   : (CBP_RPRE && RG && e < c.npre)   ? rpre[e]      // requested by the previous row's last slot
+                                                      : rld<RG>(c.rrow + e * K * 32);
 #endif
 #pragma unroll 1
     for (int k = 0; k < K; ++k) {
@@ -328,6 +341,12 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
             for (int e = 0; e < DC; ++e)
                 rnext[e] = (c.r0 || (e == DC - 1 && lastoff)) ? 0.0f : rld<RG>(rk + 32 + e * K * 32);
         }
+#if CBP_RPRE
+        else if (RG && c.nrow) {                                  // last slot: the next row's slot-0 words
+#pragma unroll
+            for (int e = 0; e < DC; ++e) rnext[e] = rld<RG>(c.nrow + e * K * 32);
+        }
+#endif
 #endif
         RowAcc<1> acc;
         acc.Ssum[0] = 0.0f;
@@ -404,6 +423,10 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
         }
         wslot_done<K, LBP>(c, k, rr, v, acc, o);
     }
+#if CBP_RPRE && !CBP_WARP_LEAN
+#pragma unroll
+    for (int e = 0; e < DC; ++e) rpre[e] = rnext[e];
+#endif
 }
 
 // Rows longer than CBP_DC_REG: per slot two passes over the edges in chunks of U (all loads of a
@@ -507,7 +530,7 @@ __device__ __forceinline__ void wrow_park(const int4* __restrict__ ent, const fl
 template <int K, int ALG, int TM, bool RG>
 __device__ __forceinline__ void wrow_dispatch(int dc, int max_dc, bool merge, const int4* __restrict__ ent,
                                               const float4* __restrict__ ptab, int e0, const Lane& L, TexH tex,
-                                              const WCtx& c, WRow<K>& o)
+                                              const WCtx& c, WRow<K>& o, float (&rpre)[CBP_DC_REG])
 {
     // rows of max dc - 1 edges run the max-dc body with the last edge masked: one call site per body
     // (wrow is inlined, so a second call site would be a second copy).  Only for K >= 2 slots per lane
@@ -518,16 +541,16 @@ __device__ __forceinline__ void wrow_dispatch(int dc, int max_dc, bool merge, co
     if (lastoff) dc += 1;
     switch (dc) {
 #if CBP_DC_REG >= 1
-    case 1: wrow<1, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
-    case 2: wrow<2, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
-    case 3: wrow<3, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
-    case 4: wrow<4, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
-    case 5: wrow<5, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
-    case 6: wrow<6, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
+    case 1: wrow<1, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, rpre, lastoff); break;
+    case 2: wrow<2, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, rpre, lastoff); break;
+    case 3: wrow<3, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, rpre, lastoff); break;
+    case 4: wrow<4, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, rpre, lastoff); break;
+    case 5: wrow<5, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, rpre, lastoff); break;
+    case 6: wrow<6, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, rpre, lastoff); break;
 #endif
 #if CBP_DC_REG >= 8
-    case 7: wrow<7, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
-    case 8: wrow<8, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, lastoff); break;
+    case 7: wrow<7, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, rpre, lastoff); break;
+    case 8: wrow<8, K, ALG, TM, RG>(ent, ptab, e0, L, tex, c, o, rpre, lastoff); break;
 #endif
     default: wrow_park<K, ALG, TM, RG>(ent, ptab, e0, dc, L, tex, c, o); break;
     }
@@ -684,25 +707,35 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                     }
                 }
             } else {
+                // CBP_LLR_BATCH 128-bit loads in flight per lane before the first use: the frame's LLRs come from
+                // HBM (~1 us), and a loop of load -> use exposed that latency once per 512 bytes of the frame
                 const float4* src = reinterpret_cast<const float4*>(a.llr + base);
-                for (int v4 = tl; 4 * v4 < N; v4 += TL) {
-                    const float4 x = __ldcs(src + v4);
-                    const float4 x0 = make_float4(__fadd_rn(x.x, 0.0f), __fadd_rn(x.y, 0.0f), __fadd_rn(x.z, 0.0f),
-                                                  __fadd_rn(x.w, 0.0f));
-                    // H bytes = the sign bytes of the four posteriors, one 32-bit store
-                    const uint32_t hw4 = __byte_perm(__byte_perm(__float_as_uint(x0.x), __float_as_uint(x0.y), 0x0073),
-                                                     __byte_perm(__float_as_uint(x0.z), __float_as_uint(x0.w), 0x0073), 0x5410);
-                    if (4 * v4 + 3 < N) {
-                        *reinterpret_cast<float4*>(lam + 4 * v4) = x0;
-                        *reinterpret_cast<uint32_t*>(hb + 4 * v4) = hw4;
-                    } else {
-                        const float xs[4] = {x0.x, x0.y, x0.z, x0.w};
+                for (int v0 = tl; 4 * v0 < N; v0 += CBP_LLR_BATCH * TL) {
+                    float4 xb[CBP_LLR_BATCH];
 #pragma unroll
-                        for (int t = 0; t < 4; ++t)
-                            if (4 * v4 + t < N) {
-                                lam[4 * v4 + t] = xs[t];
-                                hb[4 * v4 + t] = static_cast<int8_t>(__float_as_uint(xs[t]) >> 24);
-                            }
+                    for (int u = 0; u < CBP_LLR_BATCH; ++u)
+                        xb[u] = (4 * (v0 + u * TL) < N) ? __ldcs(src + v0 + u * TL) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+                    for (int u = 0; u < CBP_LLR_BATCH; ++u) {
+                        const int v4 = v0 + u * TL;
+                        const float4 x = xb[u];
+                        const float4 x0 = make_float4(__fadd_rn(x.x, 0.0f), __fadd_rn(x.y, 0.0f), __fadd_rn(x.z, 0.0f),
+                                                      __fadd_rn(x.w, 0.0f));
+                        // H bytes = the sign bytes of the four posteriors, one 32-bit store
+                        const uint32_t hw4 = __byte_perm(__byte_perm(__float_as_uint(x0.x), __float_as_uint(x0.y), 0x0073),
+                                                         __byte_perm(__float_as_uint(x0.z), __float_as_uint(x0.w), 0x0073), 0x5410);
+                        if (4 * v4 + 3 < N) {
+                            *reinterpret_cast<float4*>(lam + 4 * v4) = x0;
+                            *reinterpret_cast<uint32_t*>(hb + 4 * v4) = hw4;
+                        } else if (4 * v4 < N) {
+                            const float xs[4] = {x0.x, x0.y, x0.z, x0.w};
+#pragma unroll
+                            for (int t = 0; t < 4; ++t)
+                                if (4 * v4 + t < N) {
+                                    lam[4 * v4 + t] = xs[t];
+                                    hb[4 * v4 + t] = static_cast<int8_t>(__float_as_uint(xs[t]) >> 24);
+                                }
+                        }
                     }
                 }
             }
@@ -730,8 +763,10 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 // (a3) dual-diagonal encoder: systematic symbols, lambda_i[r] of the
                 // core rows, p0 = XOR_i lambda_i, the parity chain, the extension
                 for (int v = tl; v < C.K; v += TL) Qs[v] = ((cw[v >> 5] >> (v & 31)) & 1u) ? -1.0f : 1.0f;
-                // lambda_i[r] = XOR of the info bits of check i Z + r: each entry read once per row for the K
-                // slots (kept in the H bytes, free until the channel step); p0 = XOR over the core rows
+                tsync();
+                // lambda_i[r] = XOR of the info bits of check i Z + r (the sign bits of their symbols: one load
+                // and one XOR per bit): each entry read once per row for the K slots (kept in the H bytes, free
+                // until the channel step); p0 = XOR over the core rows
                 uint32_t p0[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) p0[k] = 0u;
@@ -747,15 +782,14 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                         for (int k = 0; k < K; ++k) {
                             int t = rk[k] + sft;
                             t = (t >= Z) ? t - Z : t;
-                            const int v = jz + t;
-                            lamb[k] ^= (cw[v >> 5] >> (v & 31)) & 1u;
+                            lamb[k] ^= __float_as_uint(Qs[jz + t]);
                         }
                     }
 #pragma unroll
                     for (int k = 0; k < K; ++k)
                         if (vk[k]) {
-                            hb[i * Z + rk[k]] = static_cast<int8_t>(lamb[k]);
-                            p0[k] ^= lamb[k];
+                            hb[i * Z + rk[k]] = static_cast<int8_t>(lamb[k] >> 31);
+                            p0[k] ^= lamb[k] >> 31;
                         }
                 }
 #pragma unroll
@@ -794,6 +828,49 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
             }
             // (a4) y = (1 - 2c) + sigma n, L = (2/sigma^2) y (equ_s4e15, R17); int8 stream
             const int nblk = (N + 3) / 4;
+            if (a.mode == MODE_CHANNEL) {
+                // channel-only launch (cbp_channel, the first half of a split cbp_ber_sim): no row body shares
+                // the instruction cache, so this is the throughput form of the loop below -- two Philox blocks
+                // per step, Philox and the four Box-Muller bodies inline (independent chains), and the four
+                // LLRs of a block stored from registers with one 128-bit streaming store (rows of ld % 4 == 0
+                // floats on a 16-byte aligned buffer; else one by one).  Same counters, same operations per value.
+                if (a.llr_out) {
+                    float* out = a.llr_out + static_cast<size_t>(f) * a.ld;
+                    const bool vec = (a.ld & 3) == 0 && (reinterpret_cast<uintptr_t>(a.llr_out) & 15) == 0;
+                    auto emit = [&](int b, const float (&n)[4]) {
+                        float Lv[4];
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const int v = min(4 * b + m, N - 1);
+                            const float y = __fadd_rn(Qs[v], __fmul_rn(a.sigma, n[m]));
+                            Lv[m] = __fmul_rn(a.scale, y);
+                            if (a.llr_mode & 1) {
+                                float qq = rintf(__fmul_rn(Lv[m], 4.0f));
+                                qq = fminf(fmaxf(qq, -127.0f), 127.0f);
+                                Lv[m] = __fmul_rn(qq, 0.25f);
+                            }
+                        }
+                        if (vec && 4 * b + 3 < N) {
+                            __stcs(reinterpret_cast<float4*>(out + 4 * b), make_float4(Lv[0], Lv[1], Lv[2], Lv[3]));
+                        } else {
+#pragma unroll
+                            for (int m = 0; m < 4; ++m)
+                                if (4 * b + m < N) __stcs(out + 4 * b + m, Lv[m]);
+                        }
+                    };
+                    for (int b = tl; b < nblk; b += 2 * TL) {
+                        const u32x4 x0 = philox4x32_10(u32x4{static_cast<uint32_t>(b), flo, fhi, 1u}, key0, key1);
+                        const u32x4 x1 = philox4x32_10(u32x4{static_cast<uint32_t>(b + TL), flo, fhi, 1u}, key0, key1);
+                        float n0[4], n1[4];
+                        box_muller(x0.x, x0.y, n0[0], n0[1]);
+                        box_muller(x0.z, x0.w, n0[2], n0[3]);
+                        box_muller(x1.x, x1.y, n1[0], n1[1]);
+                        box_muller(x1.z, x1.w, n1[2], n1[3]);
+                        emit(b, n0);
+                        if (b + TL < nblk) emit(b + TL, n1);
+                    }
+                }
+            } else
             for (int b = tl; b < nblk; b += TL) {
                 const u32x4 x = w_philox(u32x4{static_cast<uint32_t>(b), flo, fhi, 1u}, key0, key1);
 #pragma unroll 1
@@ -820,10 +897,6 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
         }
         if (a.mode == MODE_CHANNEL) {                         // channel only: L and the codeword to HBM
             tsync();
-            if (a.llr_out) {
-                float* out = a.llr_out + static_cast<size_t>(f) * a.ld;
-                for (int v = tl; v < N; v += TL) __stcs(out + v, lam[v]);
-            }
             if (a.cw_out) {
                 uint32_t* out = a.cw_out + static_cast<size_t>(f) * a.ld_words;
                 for (int w = tl; w < a.ld_words; w += TL) __stcs(out + w, w < C.nwords ? cw[w] : 0u);
@@ -839,6 +912,9 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
 
         // ---- Step 2: sweeps over the base rows (checks ascending, R12)
         int consec = 0, fires = 0, sweep = 1;
+        float rpre[CBP_DC_REG];                               // CBP_RPRE: R words requested for the next row
+        int npre = 0;
+        (void)rpre; (void)npre;
         long long ev = 0;
         bool conv = false;
         for (;; ++sweep) {
@@ -848,10 +924,21 @@ __global__ void __launch_bounds__(MAXT, 1) cbp_warp_kernel(const __grid_constant
                 // the window can fill in this row: keep what a mid-row stop has to roll back
                 WCtx cx{tl, Lk, Z, TEAM ? 32 * warp : 0, belief && W - consec - 1 < Z, keep_S, sweep == 1, lam, hb, pb,
                         Rw + static_cast<size_t>(e0) * K * 32 + l, S + i * Z};
+#if CBP_RPRE
+                // the row's last slot requests the next row's slot-0 R words (their L2 latency then overlaps the
+                // slot's update): from sweep 2 on, register rows only, dc words that lie inside the R array, and
+                // not in the fused launch's merged body (whose row may run with a masked edge)
+                const int e0n = row_ptr[i + 1 < mb ? i + 1 : 0], dcn = row_ptr[(i + 1 < mb ? i + 1 : 0) + 1] - e0n;
+                const bool pf = RG && sweep > 1 && a.mode != MODE_BER_SIM && dc <= CBP_DC_REG && dcn <= CBP_DC_REG &&
+                                e0n + dc <= C.nent;
+                cx.nrow = pf ? Rw + static_cast<size_t>(e0n) * K * 32 + l : nullptr;
+                cx.npre = npre;
+                npre = pf ? min(dc, dcn) : 0;
+#endif
                 WRow<K> ro;
                 ro.first_bad = Z;
                 ro.last_bad = -1;
-                wrow_dispatch<K, ALG, TM, RG>(dc, C.max_dc, a.mode == MODE_BER_SIM, ent, ptab, e0, lane, static_cast<TexH>(C.phi_tex), cx, ro);
+                wrow_dispatch<K, ALG, TM, RG>(dc, C.max_dc, a.mode == MODE_BER_SIM, ent, ptab, e0, lane, static_cast<TexH>(C.phi_tex), cx, ro, rpre);
                 int first_bad = ro.first_bad, last_bad = ro.last_bad;
                 if constexpr (TEAM) {
                     // the team's first / last unclean check of the row (two buffers: a fast warp may write

@@ -194,6 +194,26 @@ def test_channel_parity(codes, name, llr_mode):
         assert (cw_g.cpu().numpy().view(np.uint32) == cw_o).all()
 
 
+@pytest.mark.parametrize("name", ["C2", "C3a"])
+def test_channel_row_pitch_and_alignment(codes, name):
+    """cbp_channel with rows of ld % 4 != 0 floats and with a buffer that is only 4-byte aligned (the
+    channel-only launch then stores the LLRs one by one instead of 128 bits at a time): same bits,
+    and the padding columns stay untouched."""
+    g, o = codes(name)
+    F, N = 33, o.N
+    l_o, cw_o = o.channel(2.0, seed=77, frame_begin=5, frames=F, llr_mode=0)
+    for ld, off in ((N + 1, 0), (N + 4, 1), (N + 3, 3)):
+        flat = torch.full((F * ld + 4,), 123.0, dtype=torch.float32, device="cuda")
+        llr = flat[off:off + F * ld].view(F, ld)
+        cw = torch.zeros((F, g.words), dtype=torch.int32, device="cuda")
+        g.channel(2.0, seed=77, frame_begin=5, frames=F, llr_mode=0, out=(llr, cw))
+        torch.cuda.synchronize()
+        got = llr.cpu().numpy()
+        assert (got[:, :N].view(np.uint32) == l_o.view(np.uint32)).all(), (ld, off)
+        assert (got[:, N:] == 123.0).all(), (ld, off)
+        assert (cw.cpu().numpy().view(np.uint32) == cw_o).all()
+
+
 @pytest.mark.parametrize("name,ebn0,frames,llr_mode", [("C1", 2.0, 10_000, 0), ("C2", 1.5, 1500, 0),
                                                        ("C2", 2.5, 1500, 1), ("C3a", 2.5, 200, 0),
                                                        ("C3b", 4.0, 200, 0)])
