@@ -74,6 +74,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 #ifndef CBP_WARP_LEAN
 #define CBP_WARP_LEAN 0     // 1: entries and R re-read per slot (fewer registers, A/B runs)
 #endif
+#ifndef CBP_PARK_C2B_TEX
+#define CBP_PARK_C2B_TEX 0xF  // bit u: edge u of a 4-edge chunk of a long (parked) row fetches its C2B phi row through TEX
+                              // (all four: C3b -3.3 %; two of four -1.6 %; B2V rows through TEX as well: no better)
+#endif
+#ifndef CBP_PARK_B2V_TEX
+#define CBP_PARK_B2V_TEX 0x0  // the same for the B2V phi row
+#endif
 #ifndef CBP_RPRE
 #define CBP_RPRE 0          // 1: a row's last slot requests the next row's slot-0 R words (A/B switch)
 #endif
@@ -433,9 +440,9 @@ __device__ __forceinline__ void wrow(const int4* __restrict__ ent, const float4*
 // chunk first, U independent phi chains), a remainder one edge at a time, parking {Q^new,
 // Phi | sign of the decision} in the variable's slot between the phases (only this lane touches
 // the variable during the row).  Both phi rows from the shared-memory table.
-template <int U, int K, int ALG, bool RG>
+template <int U, int K, int ALG, bool RG, int TM>
 __device__ __forceinline__ void wpark_p1(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int e,
-                                         int rr, bool v, const Lane& L, const WCtx& c, float* rk, RowAcc<1>& acc)
+                                         int rr, bool v, const Lane& L, const WCtx& c, float* rk, RowAcc<1>& acc, TexH tex)
 {
     constexpr bool LBP = ALG == 2;
     int a[U];
@@ -449,7 +456,13 @@ __device__ __forceinline__ void wpark_p1(const int4* __restrict__ ent, const flo
         ro[u][0] = c.r0 ? 0.0f : rld<RG>(rk + (e + u) * K * 32);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) cbp_phase1<1, false>(vv[u], ro[u], q[u], ph[u], ptab, L, 0, acc);
+    for (int u = 0; u < U; ++u) {
+        // chunk edges CBP_PARK_C2B_TEX selects fetch their C2B phi row through TEX (pipe balance, as in wrow)
+        if (TM == 0 && U > 1 && ((CBP_PARK_C2B_TEX >> u) & 1))
+            cbp_phase1<1, true>(vv[u], ro[u], q[u], ph[u], ptab, L, tex, acc);
+        else
+            cbp_phase1<1, false>(vv[u], ro[u], q[u], ph[u], ptab, L, tex, acc);
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) c.pb[(e + u) * 32] = ph[u][0];    // Phi, lane-private
     if (v) {
@@ -461,9 +474,10 @@ __device__ __forceinline__ void wpark_p1(const int4* __restrict__ ent, const flo
     }
 }
 
-template <int U, int K, int ALG, bool RG>
+template <int U, int K, int ALG, bool RG, int TM>
 __device__ __forceinline__ void wpark_p2(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int e,
-                                         int rr, bool v, const Lane& L, const WCtx& c, float* rk, const RowAcc<1>& acc)
+                                         int rr, bool v, const Lane& L, const WCtx& c, float* rk, const RowAcc<1>& acc,
+                                         TexH tex)
 {
     constexpr bool LBP = ALG == 2;
     int a[U];
@@ -479,7 +493,10 @@ __device__ __forceinline__ void wpark_p2(const int4* __restrict__ ent, const flo
 #pragma unroll
     for (int u = 0; u < U; ++u) {                               // lookups first (see wrow)
         const float q[1] = {vv[u][0]}, ph[1] = {vv[u][1]};
-        cbp_phase2<1, false>(acc, q, ph, rn[u], lamn[u], ptab, L, 0);
+        if (TM == 0 && U > 1 && ((CBP_PARK_B2V_TEX >> u) & 1))
+            cbp_phase2<1, true>(acc, q, ph, rn[u], lamn[u], ptab, L, tex);
+        else
+            cbp_phase2<1, false>(acc, q, ph, rn[u], lamn[u], ptab, L, tex);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -496,7 +513,6 @@ __device__ __forceinline__ void wrow_park(const int4* __restrict__ ent, const fl
                                           const Lane& L, TexH tex, const WCtx& c, WRow<K>& o)
 {
     constexpr int U = 4;
-    (void)tex;
 #pragma unroll 1
     for (int k = 0; k < K; ++k) {
         const int r = c.l + k * c.Lk;
@@ -509,14 +525,14 @@ __device__ __forceinline__ void wrow_park(const int4* __restrict__ ent, const fl
         acc.negw[0] = acc.flipw[0] = acc.oldbits[0] = 0u;
         int e = 0;
 #pragma unroll 1
-        for (; e + U <= dc; e += U) wpark_p1<U, K, ALG, RG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
+        for (; e + U <= dc; e += U) wpark_p1<U, K, ALG, RG, TM>(ent, ptab, e0, e, rr, v, L, c, rk, acc, tex);
 #pragma unroll 1
-        for (; e < dc; ++e) wpark_p1<1, K, ALG, RG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
+        for (; e < dc; ++e) wpark_p1<1, K, ALG, RG, TM>(ent, ptab, e0, e, rr, v, L, c, rk, acc, tex);
         e = 0;
 #pragma unroll 1
-        for (; e + U <= dc; e += U) wpark_p2<U, K, ALG, RG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
+        for (; e + U <= dc; e += U) wpark_p2<U, K, ALG, RG, TM>(ent, ptab, e0, e, rr, v, L, c, rk, acc, tex);
 #pragma unroll 1
-        for (; e < dc; ++e) wpark_p2<1, K, ALG, RG>(ent, ptab, e0, e, rr, v, L, c, rk, acc);
+        for (; e < dc; ++e) wpark_p2<1, K, ALG, RG, TM>(ent, ptab, e0, e, rr, v, L, c, rk, acc, tex);
         wslot_done<K, ALG == 2>(c, k, rr, v, acc, o);
     }
 }
