@@ -574,7 +574,8 @@ __device__ __forceinline__ void wrow_dispatch(int dc, int max_dc, bool merge, co
 
 // ---------------------------------------------------------------- the kernel
 // RG: R in a global slot per warp (else in the warp's shared state).  Modes: decode (fp32 /
-// int8 LLRs from HBM) and the fused ber_sim; cbp_channel runs on cbp_kernel.
+// int8 LLRs from HBM), the fused ber_sim, and the two halves of a split one -- channel only
+// (MODE_CHANNEL: L and the codewords to HBM) and decode + error count (MODE_BER_LLR).
 // TM: phi table rows for C2B / B2V through the texture pipe (0: C2B only, 1: both -- the table
 // is then not staged in shared memory, 2: neither).
 // TEAM: one frame per CTA instead of one per warp (large frames, C4: N = 26112, Z = 384): the CTA's
