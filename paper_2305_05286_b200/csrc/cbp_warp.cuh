@@ -74,6 +74,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 #ifndef CBP_WARP_LEAN
 #define CBP_WARP_LEAN 0     // 1: entries and R re-read per slot (fewer registers, A/B runs)
 #endif
+#ifndef CBP_PARK_U
+#define CBP_PARK_U 4        // edges per chunk of a long (parked) row
+#endif
 #ifndef CBP_PARK_C2B_TEX
 #define CBP_PARK_C2B_TEX 0xF  // bit u: edge u of a 4-edge chunk of a long (parked) row fetches its C2B phi row through TEX
                               // (all four: C3b -3.3 %; two of four -1.6 %; B2V rows through TEX as well: no better)
@@ -512,7 +515,7 @@ template <int K, int ALG, int TM, bool RG>
 __device__ __forceinline__ void wrow_park(const int4* __restrict__ ent, const float4* __restrict__ ptab, int e0, int dc,
                                           const Lane& L, TexH tex, const WCtx& c, WRow<K>& o)
 {
-    constexpr int U = 4;
+    constexpr int U = CBP_PARK_U;
 #pragma unroll 1
     for (int k = 0; k < K; ++k) {
         const int r = c.l + k * c.Lk;
